@@ -1,0 +1,172 @@
+/*
+ * dbf_b200.h -- C ABI of the B200-native Double Binary Factorization (DBF) forward path.
+ *
+ * The reference (arxiv 2505.11076, package `dbf` 0.1.0 under /root/reference/pkg) exposes the
+ * hot path as plain Python functions with no FFI layer:
+ *
+ *   pack(dense) -> SignMatrix                pkg/src/dbf/bitcore.py:72-85
+ *   unpack(s)   -> ndarray                   pkg/src/dbf/bitcore.py:88-91
+ *   sign_matvec(s, x) -> ndarray             pkg/src/dbf/kernel.py:24-45
+ *   forward(X, layer) -> ndarray             pkg/src/dbf/kernel.py:48-62
+ *
+ * Each entry point below replaces one of them (cited per function).  The Python package
+ * `paper_2505_11076_b200` binds this ABI through ctypes and re-exposes the reference
+ * signatures and error messages; see INTEGRATION.md for the binding a maintainer would add.
+ *
+ * Conventions (all functions):
+ *   - plain C types only; pointers are DEVICE pointers unless stated otherwise;
+ *   - every call is asynchronous on the caller's `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream) and never synchronises the device;
+ *   - no hidden device allocation: scratch memory is a caller-provided workspace whose size
+ *     is returned by the matching *_workspace_bytes() query;
+ *   - return value is a dbf_status (0 = DBF_OK); nothing throws across the ABI;
+ *   - sign bit semantics follow the reference exactly: bit value 1 <=> +1, 0 <=> -1
+ *     (bitcore.py:7-9), columns LSB-first inside each byte/word.
+ *
+ * Device layouts:
+ *   canonical  : uint32 words, row-major, word j of a row holds columns 32j..32j+31 (bit i <->
+ *                column 32j+i).  This is the reference's uint8 row bytes viewed little-endian as
+ *                uint32, with the row pitch padded to `dbf_canonical_pitch_words(cols)` words
+ *                (a multiple of 4 words = 16 bytes) and every padding bit zero.
+ *   tiled      : the decode engine's operand layout.  Rows are grouped in blocks of 16, columns
+ *                in chunks of 256; one (row block, chunk) is 512 contiguous bytes = 32 lanes x
+ *                4 words, ordered so that one 128-bit load per lane yields the A fragments of
+ *                eight int8 m16n8k32 tensor-core MMAs after a single AND per register.
+ */
+#ifndef DBF_B200_H
+#define DBF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DBF_ABI_VERSION 1
+
+typedef enum {
+  DBF_OK = 0,
+  DBF_ERR_INVALID_ARGUMENT = 1, /* null pointer, negative/zero size, bad dtype              */
+  DBF_ERR_SHAPE = 2,            /* dimension mismatch between operands                       */
+  DBF_ERR_WORKSPACE = 3,        /* workspace too small                                       */
+  DBF_ERR_CUDA = 4,             /* a CUDA runtime call failed (see dbf_last_cuda_error)      */
+  DBF_ERR_UNSUPPORTED = 5       /* configuration not supported by this build                 */
+} dbf_status;
+
+typedef enum {
+  DBF_F16 = 0,
+  DBF_F32 = 1,
+  DBF_F64 = 2,
+  DBF_BF16 = 3
+} dbf_dtype;
+
+/* ---- library metadata ------------------------------------------------------------------ */
+int dbf_abi_version(void);
+const char* dbf_status_string(int status);
+/* cudaError_t of the last failing CUDA call made by this library on the calling thread. */
+int dbf_last_cuda_error(void);
+const char* dbf_last_cuda_error_string(void);
+
+/* ---- layout queries (host-only arithmetic, safe without a GPU) ------------------------- */
+/* bitcore.row_bytes (bitcore.py:67-69): bytes of one reference-packed row. */
+int64_t dbf_row_bytes(int64_t cols);
+/* words per row of the canonical device layout (multiple of 4). */
+int64_t dbf_canonical_pitch_words(int64_t cols);
+/* bytes of the tiled decode layout of a rows x cols sign matrix. */
+int64_t dbf_tiled_bytes(int64_t rows, int64_t cols);
+
+/* ---- bitcore: pack / unpack (bitcore.py:72-91) ------------------------------------------ */
+/*
+ * dbf_pack_signs -- replaces bitcore.pack (bitcore.py:72-85).
+ * dense: rows x cols values of `dtype` (F16/F32/F64/BF16) with leading dimension `ld`
+ * (elements).  Writes canonical words (pitch `word_pitch` >= dbf_canonical_pitch_words(cols)).
+ * Validation matches the reference: every entry must be exactly +1 or -1 (|v| == 1; NaN and 0
+ * are rejected).  *d_first_bad (a device int64) receives the row-major linear index r*cols+c of
+ * the FIRST offending entry, or -1 when all entries are valid.  The caller reads it back and
+ * raises ValueError("entry at (r, c) is v, expected -1 or +1") like bitcore.py:81-82.
+ */
+int dbf_pack_signs(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t ld,
+                   uint32_t* words, int64_t word_pitch, int64_t* d_first_bad, void* stream);
+
+/* dbf_unpack_signs -- replaces bitcore.unpack (bitcore.py:88-91): canonical words -> +-1. */
+int dbf_unpack_signs(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
+                     void* dense, int dtype, int64_t ld, void* stream);
+
+/*
+ * dbf_repack_u8 -- upload path of SignMatrix.bits (bitcore.py:40-64): reference row bytes
+ * (rows x dbf_row_bytes(cols), contiguous, device) -> canonical words.  Padding bits of the last
+ * byte are cleared, so flipped padding bits never contribute (test_kernel.py:35-45).
+ */
+int dbf_repack_u8(const uint8_t* bytes, int64_t rows, int64_t cols, uint32_t* words,
+                  int64_t word_pitch, void* stream);
+
+/* dbf_words_to_u8 -- canonical words -> reference row bytes (rows x dbf_row_bytes(cols)). */
+int dbf_words_to_u8(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
+                    uint8_t* bytes, void* stream);
+
+/* dbf_tile_signs -- canonical words -> tiled decode layout (dbf_tiled_bytes(rows, cols)). */
+int dbf_tile_signs(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
+                   void* tiled, void* stream);
+
+/* ---- kernel: sign_matvec / forward (kernel.py:24-62) ------------------------------------ */
+/*
+ * Workspace for dbf_sign_matvec / dbf_forward.  batch = number of input rows of X.
+ */
+size_t dbf_forward_workspace_bytes(int64_t n, int64_t k, int64_t m, int64_t batch);
+
+/*
+ * dbf_sign_matvec -- replaces kernel.sign_matvec (kernel.py:24-45), batched:
+ *   Y[i, r] = sum_c S[r, c] * X[i, c]      for i < batch, r < rows
+ * S is given in the tiled layout.  X: batch x cols of x_dtype (F16/F32/F64), row stride ldx
+ * elements.  Y: batch x rows of y_dtype (F16/F32/F64), row stride ldy.  The input row is
+ * quantized once to a 22-bit fixed-point grid relative to its max |value| and the sum is
+ * accumulated exactly in integers on the tensor cores, so the result is bitwise reproducible
+ * (kernel.py:26-28).
+ */
+int dbf_sign_matvec(const void* S_tiled, int64_t rows, int64_t cols, const void* X, int x_dtype,
+                    int64_t batch, int64_t ldx, void* Y, int y_dtype, int64_t ldy, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/*
+ * dbf_forward -- replaces kernel.forward (kernel.py:48-62):
+ *   Y[i] = a * (A . (mid * (B . (X[i] * b))))
+ * A: n x k, B: k x m, both tiled.  a (n), mid (k), b (m) are scale vectors of scale_dtype
+ * (F16, F32 or F64).  X: batch x m (x_dtype F16/F32/F64, stride ldx); Y: batch x n (y_dtype, stride
+ * ldy).  The intermediate t = mid * (B . (b * x)) lives in the workspace as fp32.
+ */
+int dbf_forward(const void* A_tiled, const void* B_tiled, const void* a, const void* mid,
+                const void* b, int scale_dtype, int64_t n, int64_t k, int64_t m, const void* X,
+                int x_dtype, int64_t batch, int64_t ldx, void* Y, int y_dtype, int64_t ldy,
+                void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * dbf_forward_partial -- one middle-dimension (k) shard of dbf_forward for multi-GPU
+ * tensor parallelism: the shard owns rows [k0,k1) of B, columns [k0,k1) of A
+ * (passed as their own tiled n x (k1-k0) matrix) and mid[k0:k1].  Writes the fp32 partial
+ *   P[i] = A_shard . (mid_shard * (B_shard . (X[i] * b)))      (no `a` scaling)
+ * so that y = a * sum_over_shards(P) after an all-reduce (dbf_finalize_partial).
+ */
+int dbf_forward_partial(const void* A_shard_tiled, const void* B_shard_tiled,
+                        const void* mid_shard, const void* b, int scale_dtype, int64_t n,
+                        int64_t k_shard, int64_t m, const void* X, int x_dtype, int64_t batch,
+                        int64_t ldx, float* P, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+/* y[i, r] = a[r] * P[i, r]  (P fp32 batch x n, contiguous) -> y_dtype with stride ldy. */
+int dbf_finalize_partial(const float* P, const void* a, int scale_dtype, int64_t n, int64_t batch,
+                         void* Y, int y_dtype, int64_t ldy, void* stream);
+
+/*
+ * Ablation kernel (north_star wording): the classic CUDA-core decode that XORs the fp16 sign
+ * bit of x with the packed sign and accumulates with HADD2.  Same semantics as
+ * dbf_sign_matvec for batch 1 but reads the canonical layout; kept only to measure against the
+ * tensor-core path.
+ */
+int dbf_sign_matvec_xor(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
+                        const void* x, int x_dtype, float* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBF_B200_H */

@@ -1,0 +1,61 @@
+"""B200-native Double Binary Factorization (DBF) forward -- drop-in for the reference ``dbf``
+package's hot path (pack / unpack / sign_matvec / forward, /root/reference/pkg/src/dbf).
+
+Everything computes on an sm_100a GPU through the C ABI in ``include/dbf_b200.h``
+(``libdbf_b200.so``); importing this package fails if the library is not built, and compute
+calls fail without a CUDA device -- there is no CPU fallback.
+"""
+
+from ._lib import DbfNativeError
+from .bitcore import (
+    DbfFormatError,
+    DbfLayer,
+    SignMatrix,
+    dumps_dbf,
+    load_dbf,
+    pack,
+    reconstruct,
+    row_bytes,
+    save_dbf,
+    unpack,
+)
+from .budget import middle_dim, storage_bits
+from .device import DeviceLayer, DeviceSignMatrix
+from .kernel import (
+    BENCH_CSV_HEADER,
+    BenchRow,
+    bench_forward,
+    forward,
+    forward_device,
+    random_device_layer,
+    sign_matvec,
+    sign_matvec_device,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BENCH_CSV_HEADER",
+    "BenchRow",
+    "DbfFormatError",
+    "DbfLayer",
+    "DbfNativeError",
+    "DeviceLayer",
+    "DeviceSignMatrix",
+    "SignMatrix",
+    "bench_forward",
+    "dumps_dbf",
+    "forward",
+    "forward_device",
+    "load_dbf",
+    "middle_dim",
+    "pack",
+    "random_device_layer",
+    "reconstruct",
+    "row_bytes",
+    "save_dbf",
+    "sign_matvec",
+    "sign_matvec_device",
+    "storage_bits",
+    "unpack",
+]

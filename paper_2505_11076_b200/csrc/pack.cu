@@ -1,0 +1,177 @@
+// Sign packing kernels: the B200 replacement of bitcore.pack / bitcore.unpack
+// (/root/reference/pkg/src/dbf/bitcore.py:72-91) plus the conversions between the reference's
+// uint8 row bytes, the canonical uint32 device layout and the tiled decode layout.
+#include "common.cuh"
+
+namespace dbf {
+
+// ---- pack: one warp per 32-column word; __ballot_sync turns 32 lanes' (v > 0) into the word.
+// Bit order: lane i <-> column 32*word + i <-> bit i  (LSB-first, bitcore.py:7-9).
+template <typename T>
+__global__ void pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols, int64_t ld,
+                            uint32_t* __restrict__ words, int64_t pitch,
+                            unsigned long long* __restrict__ first_bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= rows * pitch) return;
+  const int64_t r = warp / pitch, wj = warp % pitch;
+  const int64_t c = wj * 32 + lane;
+  bool plus = false;
+  if (c < cols) {
+    const double v = to_f64<T>(dense[r * ld + c]);
+    plus = v > 0.0;
+    // |v| != 1 also catches NaN and 0 (bitcore.py:79-80).
+    if (!(fabs(v) == 1.0)) atomicMin(first_bad, (unsigned long long)(r * cols + c));
+  }
+  const uint32_t w = __ballot_sync(0xffffffffu, plus);
+  if (lane == 0) words[r * pitch + wj] = w;
+}
+
+__global__ void init_first_bad_kernel(unsigned long long* p) { *p = ~0ull; }
+
+// ---- unpack: one thread per element (coalesced stores).
+template <typename T>
+__global__ void unpack_kernel(const uint32_t* __restrict__ words, int64_t rows, int64_t cols,
+                              int64_t pitch, T* __restrict__ dense, int64_t ld) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * cols) return;
+  const int64_t r = i / cols, c = i % cols;
+  const uint32_t w = __ldg(words + r * pitch + (c >> 5));
+  dense[r * ld + c] = from_f64<T>(((w >> (c & 31)) & 1u) ? 1.0 : -1.0);
+}
+
+// ---- reference bytes (rows x ceil(cols/8)) -> canonical words; padding bits cleared.
+__global__ void repack_u8_kernel(const uint8_t* __restrict__ bytes, int64_t rows, int64_t cols,
+                                 uint32_t* __restrict__ words, int64_t pitch) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * pitch) return;
+  const int64_t r = i / pitch, j = i % pitch;
+  const int64_t rb = (cols + 7) >> 3;
+  uint32_t w = 0;
+  const int64_t c0 = j * 32;
+  if (c0 < cols) {
+    const uint8_t* row = bytes + r * rb;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t bi = j * 4 + q;
+      if (bi < rb) w |= (uint32_t)row[bi] << (8 * q);
+    }
+    const int64_t valid = cols - c0;
+    if (valid < 32) w &= (1u << valid) - 1u;
+  }
+  words[i] = w;
+}
+
+// ---- canonical words -> reference bytes (padding bits of the last byte are zero).
+__global__ void words_to_u8_kernel(const uint32_t* __restrict__ words, int64_t rows, int64_t cols,
+                                   int64_t pitch, uint8_t* __restrict__ bytes) {
+  const int64_t rb = (cols + 7) >> 3;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * rb) return;
+  const int64_t r = i / rb, q = i % rb;
+  uint32_t v = (__ldg(words + r * pitch + (q >> 2)) >> (8 * (q & 3))) & 0xffu;
+  const int64_t valid = cols - q * 8;
+  if (valid < 8) v &= (1u << valid) - 1u;
+  bytes[i] = (uint8_t)v;
+}
+
+// ---- canonical words -> tiled decode layout.
+// Output word (rb, c, lane, i), lane = 4*g + tig:
+//   bit (8*b + r) <-> row 16*rb + g + 8*(i&1), column 256*c + 32*r + 4*tig + 16*(i>>1) + b.
+// i.e. register a_i of the int8 m16n8k32 A fragment for k-block r is (word_i & (0x01010101<<r)):
+// byte b of that register is column 4*tig+b (+16 for a2/a3) of row g (+8 for a1/a3), value
+// 2^r when the sign is +1 and 0 when it is -1.
+__global__ void tile_kernel(const uint32_t* __restrict__ words, int64_t rows, int64_t cols,
+                            int64_t pitch, int64_t nchunks, uint32_t* __restrict__ tiled,
+                            int64_t total_words) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= total_words) return;
+  const int i = (int)(o & 3);
+  const int lane = (int)((o >> 2) & 31);
+  const int64_t blk = o >> 7;  // rb * nchunks + c
+  const int64_t rb = blk / nchunks, c = blk % nchunks;
+  const int g = lane >> 2, tig = lane & 3;
+  const int64_t row = rb * 16 + g + 8 * (i & 1);
+  uint32_t out = 0;
+  if (row < rows) {
+    const int base = 4 * tig + 16 * (i >> 1);
+    const uint32_t* rw = words + row * pitch;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int64_t wi = c * 8 + r;
+      const uint32_t w = (wi < pitch) ? __ldg(rw + wi) : 0u;
+      const uint32_t nib = (w >> base) & 0xfu;
+      out |= ((nib & 1u) << r) | (((nib >> 1) & 1u) << (8 + r)) | (((nib >> 2) & 1u) << (16 + r)) |
+             (((nib >> 3) & 1u) << (24 + r));
+    }
+  }
+  tiled[o] = out;
+}
+
+inline unsigned grid_for(int64_t n, int threads) { return (unsigned)ceil_div(n, threads); }
+
+}  // namespace dbf
+
+using namespace dbf;
+
+extern "C" int dbf_pack_signs(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t ld,
+                              uint32_t* words, int64_t word_pitch, int64_t* d_first_bad,
+                              void* stream) {
+  if (!dense || !words || !d_first_bad || rows < 1 || cols < 1 || ld < cols ||
+      word_pitch < canonical_pitch(cols))
+    return DBF_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto* fb = reinterpret_cast<unsigned long long*>(d_first_bad);
+  init_first_bad_kernel<<<1, 1, 0, s>>>(fb);
+  const int64_t threads = rows * word_pitch * 32;
+  return dispatch_float(dtype, [&](auto tag) {
+    using T = decltype(tag);
+    pack_kernel<T><<<grid_for(threads, 256), 256, 0, s>>>((const T*)dense, rows, cols, ld, words,
+                                                          word_pitch, fb);
+    return check_launch();
+  });
+}
+
+extern "C" int dbf_unpack_signs(const uint32_t* words, int64_t rows, int64_t cols,
+                                int64_t word_pitch, void* dense, int dtype, int64_t ld,
+                                void* stream) {
+  if (!dense || !words || rows < 1 || cols < 1 || ld < cols || word_pitch < canonical_pitch(cols))
+    return DBF_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  return dispatch_float(dtype, [&](auto tag) {
+    using T = decltype(tag);
+    unpack_kernel<T><<<grid_for(rows * cols, 256), 256, 0, s>>>(words, rows, cols, word_pitch,
+                                                                (T*)dense, ld);
+    return check_launch();
+  });
+}
+
+extern "C" int dbf_repack_u8(const uint8_t* bytes, int64_t rows, int64_t cols, uint32_t* words,
+                             int64_t word_pitch, void* stream) {
+  if (!bytes || !words || rows < 1 || cols < 1 || word_pitch < canonical_pitch(cols))
+    return DBF_ERR_INVALID_ARGUMENT;
+  repack_u8_kernel<<<grid_for(rows * word_pitch, 256), 256, 0, (cudaStream_t)stream>>>(
+      bytes, rows, cols, words, word_pitch);
+  return check_launch();
+}
+
+extern "C" int dbf_words_to_u8(const uint32_t* words, int64_t rows, int64_t cols,
+                               int64_t word_pitch, uint8_t* bytes, void* stream) {
+  if (!bytes || !words || rows < 1 || cols < 1 || word_pitch < canonical_pitch(cols))
+    return DBF_ERR_INVALID_ARGUMENT;
+  const int64_t n = rows * ((cols + 7) >> 3);
+  words_to_u8_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(words, rows, cols,
+                                                                         word_pitch, bytes);
+  return check_launch();
+}
+
+extern "C" int dbf_tile_signs(const uint32_t* words, int64_t rows, int64_t cols,
+                              int64_t word_pitch, void* tiled, void* stream) {
+  if (!tiled || !words || rows < 1 || cols < 1 || word_pitch < canonical_pitch(cols))
+    return DBF_ERR_INVALID_ARGUMENT;
+  const int64_t nch = chunks(cols);
+  const int64_t total = row_blocks(rows) * nch * (kChunkBytes / 4);
+  tile_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      words, rows, cols, word_pitch, nch, (uint32_t*)tiled, total);
+  return check_launch();
+}

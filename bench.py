@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark of the DBF decode hot path on B200 (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): Llama-2-7B, every linear layer DBF-factorized at ~2 bits
+per weight (k = middle_dim(n, m, 2.0, 32): q/k/v/o 4096x4096 k=4096, gate/up 11008x4096 k=5952,
+down 4096x11008 k=5952), decode batch 1, synthetic random-init factors.
+One STEP = one decode token through all 7 x 32 = 224 linear layers, in decoder dataflow order
+(paper_2505_11076_b200.plan), replayed as one CUDA graph.  The 1.63 GB of packed weights touched
+per step are > 2 x the 126 MB L2, so no L2 flush is needed between steps.
+
+value      = algorithmic HBM bytes per step (SURVEY.md §8d formula, summed over the 224 layers)
+             / device time per step -> GB/s (whole job: summed over ranks for --gpus N)
+e2e        = the same metric through the public plan API with the step input copied from
+             pinned host memory and the step output copied back inside the timed region
+roofline   = the dominant kernel (the tensor-core sign GEMV) against MEASURED_PEAKS.json hbm_gbs
+cpu_baseline = the reference algorithm (oracle restatement, bit-identical to dbf.forward) on the
+             host cores, bounded sample (rank 0, N=1 only)
+
+--impl reference times the reference CPU path (oracle restatement of dbf.forward, all host
+cores via a process pool) on the same metric; the reference package cannot travel to the GPU
+box, so its restatement -- pinned bit-exact to the reference's own outputs -- is what runs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "DBF layer µs & HBM GB/s (Llama2-7B shapes, bs=1); speedup vs fp16 cuBLAS GEMV"
+WORKLOAD = "llama2-7b linears, DBF 2.0 bpw, decode bs=1 (224 layers/step)"
+
+
+# ---------------------------------------------------------------------------------------------
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="llama2-7b")
+    ap.add_argument("--bpw", type=float, default=2.0)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--layer-kernels", action="store_true", help="per-layer GEMV kernels instead of the engine")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while the GPU is loaded."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+        except FileNotFoundError:
+            return self
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------------------------
+class CpuReference:
+    """Reference algorithm (oracle restatement, bit-identical to dbf.forward) on one decoder
+    block of the workload (q,k,v,o + gate,up + down) per step, rows split over all host cores."""
+
+    def __init__(self, model: str, bpw: float, procs: int | None = None):
+        from oracle import dbf_oracle as npo
+        from paper_2505_11076_b200.plan import block_shapes
+
+        rng = np.random.default_rng(0)
+        shapes = block_shapes(model)
+        self.layers = {}
+        for _, n, m in shapes:
+            name = f"{n}x{m}"
+            if name not in self.layers:
+                k = npo.middle_dim(n, m, bpw)
+                self.layers[name] = (
+                    rng.uniform(0.5, 1.5, n) / np.sqrt(k),
+                    rng.integers(0, 256, (n, npo.row_bytes(k)), dtype=np.uint8),
+                    rng.uniform(0.5, 1.5, k),
+                    rng.integers(0, 256, (k, npo.row_bytes(m)), dtype=np.uint8),
+                    rng.uniform(0.5, 1.5, m) / np.sqrt(m),
+                )
+        self.order = [f"{n}x{m}" for _, n, m in shapes]
+        self.bytes_per_block = 0
+        for name in self.order:
+            a, A, mid, B, b = self.layers[name]
+            self.bytes_per_block += A.size + B.size + 2 * (len(a) + len(mid) + len(b)) + 2 * (len(b) + len(a))
+        self.xs = {name: rng.standard_normal((1, len(v[4]))) for name, v in self.layers.items()}
+        self.pf = npo.ProcessForward(self.layers, procs=procs)
+        self.procs = self.pf.procs
+        self.pf.forward(self.order[0], self.xs[self.order[0]])  # warm the pool
+
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        for name in self.order:
+            self.pf.forward(name, self.xs[name])
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pf.close()
+
+
+def cpu_desc(model, bpw, procs):
+    return (f"one {model} decoder block (7 layers: q,k,v,o 4096x4096 k=4096; gate,up 11008x4096 k=5952; "
+            f"down 4096x11008 k=5952 at {bpw} bpw), bs=1, dbf.forward algorithm (oracle restatement, "
+            f"bit-identical to the reference), rows split over {procs} processes")
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # N>1: rank 0 alone runs the CPU reference; others exit 0 without work
+    ref = CpuReference(args.model, args.bpw)
+    for _ in range(args.warmup):
+        ref.step()
+    times = [ref.step() for _ in range(args.steps)]
+    ref.close()
+    t = float(np.mean(times))
+    gbs = ref.bytes_per_block / t / 1e9
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": gbs,
+        "unit": "GB/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (uniform signs, U(0.5,1.5)-scaled vectors, N(0,1) input)",
+        "config": {"workload": WORKLOAD, "model": args.model, "bpw": args.bpw, "global_batch": 1,
+                   "step": "one decoder block (7 of the 224 layers) per step, bounded CPU sample",
+                   "us_per_layer": t * 1e6 / len(ref.order)},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": ref.procs, "kind": "port",
+                         "sample": cpu_desc(args.model, args.bpw, ref.procs)},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+def build_cublas_chain(plan, dtype):
+    """Dense fp16 weights of the same 224 shapes, same dataflow, cuBLAS GEMV per layer."""
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1234)
+    weights = []
+    for layer in plan.layers:
+        w = torch.empty((layer.n, layer.m_dim), dtype=dtype, device="cuda")
+        w.normal_(0, 1.0 / layer.m_dim**0.5, generator=g)
+        weights.append(w)
+    bufs = [torch.zeros_like(b) for b in plan.buffers]
+
+    def step_out():
+        for op in plan.ops:
+            torch.matmul(bufs[op.src], weights[op.layer].t(), out=bufs[op.dst])
+
+    nbytes = sum(2 * w.numel() + 2 * (w.shape[0] + w.shape[1]) for w in weights)
+    return step_out, nbytes, weights
+
+
+def graph_of(fn, warm=2):
+    import torch
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(warm):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn()
+    return g
+
+
+def time_graph(g, steps, warmup, barrier=lambda: None):
+    import torch
+
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        g.replay()
+    e1.record()
+    e1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    return e0.elapsed_time(e1) / steps  # ms per step
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    import paper_2505_11076_b200 as P
+    from paper_2505_11076_b200.plan import llama_decode_plan
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1000 + rank)
+    plan = llama_decode_plan(args.model, bpw=args.bpw, batch=args.batch, generator=g)
+    plan.buffers[plan.input_buffer].normal_(generator=g)
+    if not args.layer_kernels:
+        plan.use_engine()
+    plan.capture()
+    bytes_step = plan.bytes_per_step()
+    launches = plan.kernel_launches_per_step()
+
+    clocks = ClockSampler(local).start()
+    ms = time_graph(plan._graph, args.steps, max(args.warmup, 3), barrier)
+    # keep the GPU loaded ~1.5 s more so the 200 ms clock sampler sees this kernel mix
+    t_end = time.time() + 1.5
+    while time.time() < t_end:
+        for _ in range(20):
+            plan._graph.replay()
+        torch.cuda.synchronize()
+    clk = clocks.stop()
+
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * bytes_step / (ms * 1e-3) / 1e9
+
+    # ---- e2e: pinned host input -> plan -> host output, copies inside the timed region --------
+    inp = plan.buffers[plan.input_buffer]
+    host_x = torch.empty(inp.shape, dtype=inp.dtype, pin_memory=True)
+    host_x.copy_(inp.cpu())
+    host_y = torch.empty(inp.shape, dtype=inp.dtype, pin_memory=True)
+    for _ in range(3):
+        inp.copy_(host_x, non_blocking=True)
+        plan.replay()
+        host_y.copy_(plan.buffers[plan.output_buffer], non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        inp.copy_(host_x, non_blocking=True)
+        plan.replay()
+        host_y.copy_(plan.buffers[plan.output_buffer], non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = {"value": world * bytes_step / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": host_x.numel() * host_x.element_size(),
+           "d2h_bytes_per_step": host_y.numel() * host_y.element_size(),
+           "ms_per_step": ms_e2e, "api": "paper_2505_11076_b200.plan.DecodePlan.run-equivalent (pinned H2D, graph replay, D2H)"}
+
+    # ---- cuBLAS fp16 GEMV over the same 224 shapes and dataflow -----------------------------
+    cublas = None
+    if not args.no_cublas:
+        step_fn, dense_bytes, weights = build_cublas_chain(plan, torch.float16)
+        gc = graph_of(step_fn)
+        ms_c = time_graph(gc, args.steps, max(args.warmup, 3), barrier)
+        cublas = {"ms_per_step": ms_c, "gbs": dense_bytes / (ms_c * 1e-3) / 1e9,
+                  "speedup_dbf_vs_cublas": ms_c / ms, "us_per_layer": ms_c * 1e3 / len(plan.ops)}
+        del gc, weights
+        torch.cuda.empty_cache()
+
+    peak, peak_src = peaks()
+    traffic = None
+    tf = ROOT / "profiles" / "roofline_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("traffic_bytes_per_step")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ref = CpuReference(args.model, args.bpw)
+        t = float(np.median([ref.step() for _ in range(args.cpu_reps)]))
+        ref.close()
+        cpu = {"value": ref.bytes_per_block / t / 1e9, "unit": "GB/s", "cores": ref.procs, "kind": "port",
+               "sample": cpu_desc(args.model, args.bpw, ref.procs) + f", median of {args.cpu_reps} blocks",
+               "ms_per_layer": t * 1e3 / len(ref.order)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(args.warmup, 3),
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "int8-tc(i32 exact) / fp16 io",
+            "data": "synthetic random-init DBF factors of Llama-2-7B shapes (uniform signs, fp16 scales)",
+            "config": {
+                "workload": WORKLOAD, "model": args.model, "bpw": args.bpw, "global_batch": args.batch * world,
+                "seq_len": 1, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                "layers_per_step": len(plan.ops), "us_per_layer": ms * 1e3 / len(plan.ops),
+                "tokens_per_s_linears_only": 1e3 / ms * world,
+                "bytes_per_step": bytes_step, "l2": "working set 1.63 GB/step > 2x126 MB L2; no flush",
+                "cublas_fp16": cublas,
+                "path": "layer kernels (2 GEMV launches per layer)" if args.layer_kernels else
+                        "decode engine: 1 persistent kernel per step (TMA-bulk sign ring + int8 mma.sync + LL handoff)",
+            },
+            "roofline": {"bound": "hbm", "achieved": bytes_step / (ms * 1e-3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_step / (ms * 1e-3) / 1e9 / peak, "traffic": traffic,
+                         "kernel": ("gemv_i8_kernel, all launches of the step" if args.layer_kernels else
+                                    "engine_kernel (one launch = the whole 224-layer step)"),
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -166,6 +166,91 @@ int dbf_finalize_partial(const float* P, const void* a, int scale_dtype, int64_t
 int dbf_sign_matvec_xor(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
                         const void* x, int x_dtype, float* y, void* stream);
 
+/* ---- decode engine: a whole chain of DBF layers in ONE persistent kernel ---------------- */
+/*
+ * A program is a list of SEGMENTS (one sign GEMV each: y = oscale * (S . (iscale * v))) over
+ * VECTORS.  Vector kind 0 = plain (dtype `dtype`, ready when the kernel starts, e.g. the token
+ * input); kind 1 = LL ("low-latency": uint64 words {fp32 value, 32-bit epoch}, produced inside
+ * the kernel by another segment and consumed by polling the words themselves).  Every segment's
+ * work is split into UNITS of 16 rows; each CTA executes a list of RUNS -- consecutive units of
+ * one segment, (segment, first row block, unit count) -- in order (cta_offsets[c] ..
+ * cta_offsets[c+1]); dependencies are respected by construction (a run only reads vectors
+ * written by runs of earlier stages).  One forward of a DBF layer is
+ * two segments: B with iscale=b, oscale=mid -> t (LL), then A with oscale=a -> y.
+ * Each CTA streams its units' packed signs with cp.async.bulk into a shared-memory ring (one
+ * producer warp) while consumer warps run the int8 tensor-core sign GEMV, so weights of later
+ * layers are in flight while a layer waits for its input vector.
+ */
+typedef struct {
+  const void* tiled;    /* tiled sign matrix (dbf_tile_signs) */
+  int32_t rows, cols;   /* logical shape */
+  int32_t in_vec;       /* input vector index */
+  int32_t out_vec;      /* output LL vector index or -1 */
+  const void* iscale;   /* per-column input scale or NULL */
+  const void* oscale;   /* per-row output scale or NULL */
+  int32_t scale_dtype;  /* F16 / F32 */
+  int32_t out_dtype;    /* F16: LL values are rounded through fp16 (and out_plain is fp16); F32 */
+  void* out_plain;      /* optional plain output (out_dtype), NULL if unused */
+} dbf_engine_segment;
+
+typedef struct {
+  void* data;           /* plain: `len` values of `dtype`; LL: `len` uint64 words */
+  int32_t len;
+  int32_t kind;         /* 0 plain, 1 LL */
+  int32_t dtype;        /* plain dtype (F16/F32) */
+  int32_t producers;    /* LL: number of 16-row units that write it (filled by the builder) */
+} dbf_engine_vector;
+
+/* One RUN as the kernel consumes it: everything resolved on the host (no dependent metadata
+ * loads on the device critical path).  Built by dbf_engine_build_runs. */
+typedef struct {
+  const void* tiled;        /* 0   first byte of the run's packed signs (row block rb)       */
+  const void* x;            /* 8   input vector data                                          */
+  const void* iscale;       /* 16  per-column input scale or NULL                             */
+  const void* oscale;       /* 24  per-row output scale or NULL                               */
+  void* out_plain;          /* 32  optional plain output                                      */
+  void* ll_out;             /* 40  output LL vector data or NULL                              */
+  uint32_t* ready_in;       /* 48  ready counter of the input vector (NULL for plain input)   */
+  uint32_t* ready_out;      /* 56  ready counter of the output vector or NULL                 */
+  int32_t rows, cols;       /* 64  segment shape                                              */
+  int32_t rb, nunits;       /* 72  first row block, number of 16-row units                   */
+  int32_t seg;              /* 80  segment index (the input is re-quantized when it changes)  */
+  int32_t in_kind;          /* 84  0 plain, 1 LL                                              */
+  int32_t in_dtype;         /* 88  plain input dtype                                          */
+  int32_t scale_dtype;      /* 92                                                             */
+  int32_t out_dtype;        /* 96                                                             */
+  int32_t in_vec, out_vec;  /* 100 vector indices (LL epochs)                                 */
+  uint32_t in_producers;    /* 108 units producing the input vector (ready target per run)    */
+  int32_t pad[4];           /* 112 -> 128 bytes                                               */
+} dbf_engine_run;
+
+typedef struct {
+  const dbf_engine_run* runs;         /* device array of run records, per CTA in order         */
+  const int32_t* cta_offsets;         /* device array, grid + 1 entries (indices into runs)     */
+  uint32_t* run_counter;              /* device uint32, advanced after every launch             */
+  int64_t* trace;                     /* optional: 4 x int64 %globaltimer stamps per run / NULL */
+  int32_t nvectors;
+  int32_t grid;                       /* CTAs (<= number of SMs; one per SM)                    */
+  int32_t max_cols;                   /* largest segment `cols` (sizes shared memory)          */
+  int32_t pad;
+} dbf_engine_program;
+
+/*
+ * Host-only: resolve (segments, vectors, runs) -- HOST arrays, runs = 3 x int32 (segment, first
+ * row block, units) per run -- into `nruns` run records written to the HOST buffer `out`.
+ * `ready` is the DEVICE base address of the nvectors ready counters (zero-initialized).
+ */
+int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t nsegments,
+                          const dbf_engine_vector* vectors, int32_t nvectors, const int32_t* runs,
+                          int32_t nruns, uint32_t* ready, dbf_engine_run* out);
+
+/* Dynamic shared memory the engine needs for max_cols; DBF_ERR_UNSUPPORTED if it cannot fit. */
+int dbf_engine_smem_bytes(int32_t max_cols, size_t* bytes);
+/* Resident engine CTAs per SM and registers per thread for max_cols (diagnostics). */
+int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, int32_t* regs_per_thread);
+/* Launch one run of the program (cooperative: all CTAs co-resident) + the epoch advance. */
+int dbf_engine_launch(const dbf_engine_program* program, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

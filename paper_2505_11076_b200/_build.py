@@ -1,7 +1,7 @@
 """Build the sm_100a C-ABI library ``libdbf_b200.so`` in-tree with nvcc.
 
 The library is plain CUDA C++ behind ``include/dbf_b200.h`` (no torch types, no Python in the
-signatures).  ``python -m paper_2505_11076_b200._build`` (or ``__graft_entry__.build()``) compiles
+signatures).  ``python paper_2505_11076_b200/_build.py`` (or ``__graft_entry__.build()``) compiles
 every ``csrc/*.cu`` with ``-gencode arch=compute_100a,code=sm_100a -lineinfo`` and links one
 shared object next to this file, so it travels to the GPU box with the repo snapshot.
 """

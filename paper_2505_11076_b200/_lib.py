@@ -54,6 +54,10 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "dbf_finalize_partial": (_int, [_vp, _vp, _int, _i64, _i64, _vp, _int, _i64, _vp]),
     "dbf_sign_matvec_xor": (_int, [_vp, _i64, _i64, _i64, _vp, _int, _vp, _vp]),
+    "dbf_engine_smem_bytes": (_int, [_c.c_int32, _c.POINTER(_sz)]),
+    "dbf_engine_occupancy": (_int, [_c.c_int32, _c.POINTER(_c.c_int32), _c.POINTER(_c.c_int32)]),
+    "dbf_engine_build_runs": (_int, [_vp, _c.c_int32, _vp, _c.c_int32, _vp, _c.c_int32, _vp, _vp]),
+    "dbf_engine_launch": (_int, [_vp, _vp]),
 }
 
 
@@ -64,10 +68,14 @@ class DbfNativeError(RuntimeError):
 def _load():
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is not built; run `python -m paper_2505_11076_b200._build` "
+            f"{LIB_PATH} is not built; run `python paper_2505_11076_b200/_build.py` "
             "(nvcc, sm_100a).  There is no CPU fallback."
         )
     lib = ctypes.CDLL(str(LIB_PATH))
+    missing = [name for name in SIGNATURES if not hasattr(lib, name)]
+    if missing:
+        raise ImportError(f"{LIB_PATH} is stale (missing {missing}); rebuild with "
+                          "`python paper_2505_11076_b200/_build.py`")
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -1,0 +1,229 @@
+"""Host side of the decode engine (include/dbf_b200.h ``dbf_engine_*``).
+
+Compiles a ``DecodePlan`` (ordered layer forwards + activation dataflow) into one persistent
+kernel program:
+
+* every layer forward becomes two SEGMENTS -- B (iscale = b, oscale = mid) writing the LL
+  vector t, then A (oscale = a) writing the LL vector y -- exactly the staging of
+  kernel.py:59-61;
+* ops are grouped into dependency LEVELS (q/k/v of a block share the block input, gate/up
+  share o's output), and each level becomes two STAGES (all GEMV1s, then all GEMV2s), so the
+  independent layers of a level fill the GPU together;
+* each stage's 16-row UNITS are block-distributed over the CTAs (one per SM), rotating the
+  start from stage to stage so bytes stay balanced over the run; a CTA's list is in stage
+  order, which is what makes the in-kernel LL waits deadlock-free.
+
+The program is plain device arrays; ``EngineProgram.launch()`` is one cooperative launch.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+SEG_DTYPE = np.dtype(
+    {
+        "names": ["tiled", "rows", "cols", "in_vec", "out_vec", "iscale", "oscale", "scale_dtype", "out_dtype", "out_plain"],
+        "formats": ["<u8", "<i4", "<i4", "<i4", "<i4", "<u8", "<u8", "<i4", "<i4", "<u8"],
+        "offsets": [0, 8, 12, 16, 20, 24, 32, 40, 44, 48],
+        "itemsize": 56,
+    }
+)
+VEC_DTYPE = np.dtype(
+    {
+        "names": ["data", "len", "kind", "dtype", "producers"],
+        "formats": ["<u8", "<i4", "<i4", "<i4", "<i4"],
+        "offsets": [0, 8, 12, 16, 20],
+        "itemsize": 24,
+    }
+)
+
+
+class _Program(ctypes.Structure):
+    _fields_ = [
+        ("runs", ctypes.c_void_p),
+        ("cta_offsets", ctypes.c_void_p),
+        ("run_counter", ctypes.c_void_p),
+        ("trace", ctypes.c_void_p),
+        ("nvectors", ctypes.c_int32),
+        ("grid", ctypes.c_int32),
+        ("max_cols", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
+    ]
+
+
+_lib.lib.dbf_engine_smem_bytes.restype = ctypes.c_int
+_lib.lib.dbf_engine_smem_bytes.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
+_lib.lib.dbf_engine_occupancy.restype = ctypes.c_int
+_lib.lib.dbf_engine_occupancy.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+_lib.lib.dbf_engine_build_runs.restype = ctypes.c_int
+_lib.lib.dbf_engine_build_runs.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32,
+                                           ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+_lib.lib.dbf_engine_launch.restype = ctypes.c_int
+_lib.lib.dbf_engine_launch.argtypes = [ctypes.POINTER(_Program), ctypes.c_void_p]
+
+
+def occupancy(max_cols: int) -> tuple[int, int]:
+    """(engine CTAs per SM, registers per thread) for a program whose widest segment is max_cols."""
+    b, r = ctypes.c_int32(0), ctypes.c_int32(0)
+    _lib.check(_lib.lib.dbf_engine_occupancy(max_cols, ctypes.byref(b), ctypes.byref(r)), "dbf_engine_occupancy")
+    return b.value, r.value
+
+
+def levels_of(ops, input_buffer: int) -> list[int]:
+    """Dependency level of each op: 1 + level of the op that last wrote its source buffer."""
+    writer_level: dict[int, int] = {}
+    lv = []
+    for op in ops:
+        level = writer_level.get(op.src, -1) + 1
+        lv.append(level)
+        writer_level[op.dst] = level
+    return lv
+
+
+def distribute(units: list[tuple[int, int]], grid: int, rotate: int) -> list[list[tuple[int, int]]]:
+    """Block distribution of a stage's units over CTAs, starting at CTA `rotate`."""
+    out: list[list[tuple[int, int]]] = [[] for _ in range(grid)]
+    n = len(units)
+    for c in range(grid):
+        lo, hi = (c * n) // grid, ((c + 1) * n) // grid
+        out[(c + rotate) % grid].extend(units[lo:hi])
+    return out
+
+
+class EngineProgram:
+    """A DecodePlan compiled for the persistent decode engine."""
+
+    def __init__(self, plan, grid: int | None = None, device="cuda"):
+        import torch
+
+        _lib.require_cuda()
+        self.plan = plan
+        props = torch.cuda.get_device_properties(device)
+        self.grid = int(grid or props.multi_processor_count)
+        dev = torch.device(device)
+        act = plan.buffers[plan.input_buffer]
+        if act.shape[0] != 1:
+            raise ValueError("the decode engine currently runs batch 1 (use forward_device for batches)")
+        act_code = _lib.dtype_code(act.dtype)
+        if act_code not in (_lib.F16, _lib.F32):
+            raise ValueError("engine activations must be float16 or float32")
+
+        # ---- vectors ------------------------------------------------------------------------
+        vecs = []  # (data tensor, len, kind, dtype)
+        self._keep = []
+
+        def ll_vector(length: int) -> int:
+            t = torch.zeros(((length + 3) // 4) * 4, dtype=torch.int64, device=dev)
+            self._keep.append(t)
+            vecs.append((t.data_ptr(), length, 1, 0))
+            return len(vecs) - 1
+
+        vecs.append((act.data_ptr(), act.shape[1], 0, act_code))  # vector 0: the step input
+        latest = {plan.input_buffer: 0}  # buffer id -> vector holding its current version
+
+        lv = levels_of(plan.ops, plan.input_buffer)
+        last_writer = {}
+        for i, op in enumerate(plan.ops):
+            last_writer[op.dst] = i
+        final_op = last_writer.get(plan.output_buffer)
+
+        segs = []
+        stage_units: dict[int, list[tuple[int, int]]] = {}
+        for i, op in enumerate(plan.ops):
+            layer = plan.layers[op.layer]
+            sd = _lib.dtype_code(layer.a.dtype)
+            if sd not in (_lib.F16, _lib.F32):
+                raise ValueError("engine scales must be float16 or float32")
+            if op.src not in latest:  # read before any op wrote it: an external (plain) input
+                buf = plan.buffers[op.src]
+                vecs.append((buf.data_ptr(), buf.shape[1], 0, _lib.dtype_code(buf.dtype)))
+                latest[op.src] = len(vecs) - 1
+            src_vec = latest[op.src]
+            t_vec = ll_vector(layer.k)
+            y_vec = ll_vector(layer.n)
+            segs.append((layer.B.tiled.data_ptr(), layer.k, layer.m_dim, src_vec, t_vec, layer.b.data_ptr(),
+                         layer.mid.data_ptr(), sd, _lib.F32, 0))
+            out_plain = plan.buffers[op.dst].data_ptr() if i == final_op else 0
+            segs.append((layer.A.tiled.data_ptr(), layer.n, layer.k, t_vec, y_vec, 0, layer.a.data_ptr(), sd,
+                         act_code, out_plain))
+            latest[op.dst] = y_vec
+            for stage, seg_idx, rows in ((2 * lv[i], len(segs) - 2, layer.k), (2 * lv[i] + 1, len(segs) - 1, layer.n)):
+                stage_units.setdefault(stage, []).extend((seg_idx, rb) for rb in range((rows + 15) // 16))
+
+        per_cta: list[list[tuple[int, int]]] = [[] for _ in range(self.grid)]
+        rot = 0
+        for stage in sorted(stage_units):
+            units = stage_units[stage]
+            for c, lst in enumerate(distribute(units, self.grid, rot)):
+                per_cta[c].extend(lst)
+            rot = (rot + len(units)) % self.grid
+        # compress each CTA's unit list into runs: consecutive row blocks of one segment
+        per_cta_runs: list[list[tuple[int, int, int]]] = []
+        for lst in per_cta:
+            runs_c: list[list[int]] = []
+            for seg, rb in lst:
+                if runs_c and runs_c[-1][0] == seg and runs_c[-1][1] + runs_c[-1][2] == rb:
+                    runs_c[-1][2] += 1
+                else:
+                    runs_c.append([seg, rb, 1])
+            per_cta_runs.append([tuple(r) for r in runs_c])
+        offsets = np.zeros(self.grid + 1, dtype=np.int32)
+        offsets[1:] = np.cumsum([len(x) for x in per_cta_runs])
+        flat = np.ascontiguousarray(np.array([r for lst in per_cta_runs for r in lst], dtype=np.int32).reshape(-1, 3))
+        self.nunits = sum(len(x) for x in per_cta)
+
+        seg_arr = np.zeros(len(segs), dtype=SEG_DTYPE)
+        for j, sg in enumerate(segs):
+            seg_arr[j] = sg
+        vec_arr = np.zeros(len(vecs), dtype=VEC_DTYPE)
+        for j, (ptr, ln, kind, dt) in enumerate(vecs):
+            vec_arr[j] = (ptr, ln, kind, dt, 0)
+
+        self.max_cols = max(sg[2] for sg in segs)
+        self.run_counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ready = torch.zeros(len(vecs), dtype=torch.int32, device=dev)
+        records = np.zeros(len(flat) * 128, dtype=np.uint8)
+        _lib.check(
+            _lib.lib.dbf_engine_build_runs(
+                seg_arr.ctypes.data, len(segs), vec_arr.ctypes.data, len(vecs), flat.ctypes.data, len(flat),
+                self.ready.data_ptr(), records.ctypes.data,
+            ),
+            "dbf_engine_build_runs",
+        )
+
+        def dev_bytes(a: np.ndarray):
+            t = torch.from_numpy(np.frombuffer(a.tobytes(), dtype=np.uint8).copy()).to(dev)
+            self._keep.append(t)
+            return t.data_ptr()
+
+        self.nruns = len(flat)
+        self.units_per_cta = np.array([len(x) for x in per_cta])
+        self.nstages = len(stage_units)
+        self.nsegments = len(segs)
+        self._prog = _Program(
+            dev_bytes(records), dev_bytes(offsets), self.run_counter.data_ptr(), None,
+            len(vecs), self.grid, self.max_cols, 0,
+        )
+        self._offsets = offsets
+        self._flat = flat
+        size = ctypes.c_size_t(0)
+        _lib.check(_lib.lib.dbf_engine_smem_bytes(self.max_cols, ctypes.byref(size)), "dbf_engine_smem_bytes")
+        self.smem_bytes = size.value
+
+    def enable_trace(self):
+        """Record 4 %globaltimer stamps per run (start, input ready, first weights ready, done)."""
+        import torch
+
+        self.trace = torch.zeros((max(self.nruns, 1), 4), dtype=torch.int64, device="cuda")
+        self._prog.trace = self.trace.data_ptr()
+        return self
+
+    def launch(self, stream=None):
+        _lib.check(_lib.lib.dbf_engine_launch(ctypes.byref(self._prog), _lib.stream_ptr(stream)), "dbf_engine_launch")
+
+    def kernel_launches_per_step(self) -> int:
+        return 2  # the engine kernel + the one-thread epoch advance

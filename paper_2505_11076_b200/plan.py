@@ -1,0 +1,157 @@
+"""Multi-layer decode plans: a chain of DBF layer forwards replayed as one CUDA graph.
+
+The reference applies one layer per ``forward`` call (kernel.py:48-62).  A decode step of a
+factorized model applies every linear layer once per token, so the natural B200 unit of work is
+the whole chain: ``DecodePlan`` records the layer order and the activation dataflow of a decoder
+(q/k/v read the block input, o reads v's output as the attention stand-in, gate/up read o's
+output, down reads gate's output and produces the next block input -- attention, norms and the
+SiLU product are outside this path) and replays it as a single CUDA graph, so per-layer host
+launch overhead disappears.
+
+``run(x)`` accepts a host (numpy / CPU tensor) or device input and copies host inputs in and the
+final output back inside the call -- the end-to-end path the benchmark's ``e2e`` number times.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import _lib
+from .budget import middle_dim
+from .device import DeviceLayer
+from .kernel import forward_device, random_device_layer
+
+# Llama-2 linear shapes (n = out_features, m = in_features), SURVEY.md §8a
+LLAMA_SHAPES = {
+    "llama2-7b": dict(hidden=4096, inter=11008, kv=4096, blocks=32),
+    "llama2-13b": dict(hidden=5120, inter=13824, kv=5120, blocks=40),
+    "llama2-70b": dict(hidden=8192, inter=28672, kv=1024, blocks=80),
+}
+
+
+def block_shapes(model: str) -> list[tuple[str, int, int]]:
+    s = LLAMA_SHAPES[model]
+    h, i, kv = s["hidden"], s["inter"], s["kv"]
+    return [("q", h, h), ("k", kv, h), ("v", kv, h), ("o", h, h), ("gate", i, h), ("up", i, h), ("down", h, i)]
+
+
+@dataclass
+class PlanOp:
+    layer: int  # index into DecodePlan.layers
+    src: int  # activation buffer read
+    dst: int  # activation buffer written
+    name: str = ""
+
+
+@dataclass
+class DecodePlan:
+    layers: list
+    ops: list
+    buffers: list  # device activation tensors (batch x width)
+    input_buffer: int = 0
+    output_buffer: int = 0
+    engine: object = field(default=None, repr=False)
+    _graph: object = field(default=None, repr=False)
+    _stream: object = field(default=None, repr=False)
+
+    # ---- accounting -------------------------------------------------------------------------
+    def bytes_per_step(self) -> int:
+        """Algorithmic HBM bytes of one step (summed over ops)."""
+        act = self.buffers[0].element_size()
+        batch = self.buffers[0].shape[0]
+        return sum(self.layers[op.layer].bytes_logical(batch=batch, act_bytes=act) for op in self.ops)
+
+    def kernel_launches_per_step(self) -> int:
+        if self.engine is not None:
+            return self.engine.kernel_launches_per_step()
+        return 2 * len(self.ops)  # one GEMV launch per stage (B, then A)
+
+    # ---- execution --------------------------------------------------------------------------
+    def use_engine(self, grid: int | None = None):
+        """Run the whole chain in the persistent decode engine (one kernel per step)."""
+        from .engine import EngineProgram
+
+        self.engine = EngineProgram(self, grid=grid)
+        self._graph = None
+        return self
+
+    def use_layer_kernels(self):
+        """Run one dbf_forward (two GEMV launches) per layer instead of the engine."""
+        self.engine = None
+        self._graph = None
+        return self
+
+    def _eager(self):
+        if self.engine is not None:
+            self.engine.launch()
+            return
+        for op in self.ops:
+            forward_device(self.buffers[op.src], self.layers[op.layer], out=self.buffers[op.dst])
+
+    def capture(self):
+        import torch
+
+        _lib.require_cuda()
+        self._stream = torch.cuda.Stream()
+        self._stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self._stream):
+            self._eager()  # warm-up: sets kernel attributes outside the capture
+        torch.cuda.current_stream().wait_stream(self._stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self._stream):
+            self._eager()
+        self._graph = g
+        return self
+
+    def replay(self):
+        """One step on the device (inputs already resident)."""
+        if self._graph is None:
+            self.capture()
+        self._graph.replay()
+
+    def run(self, x):
+        """End-to-end step: host/device input -> device chain -> output (host if x was host)."""
+        import numpy as np
+        import torch
+
+        inp = self.buffers[self.input_buffer]
+        host = not (isinstance(x, torch.Tensor) and x.is_cuda)
+        if host:
+            xt = torch.as_tensor(np.asarray(x) if not isinstance(x, torch.Tensor) else x)
+            inp.copy_(xt.reshape(inp.shape), non_blocking=True)
+        else:
+            inp.copy_(x.reshape(inp.shape))
+        self.replay()
+        out = self.buffers[self.output_buffer]
+        return out.cpu() if host else out
+
+
+def llama_decode_plan(model: str = "llama2-7b", bpw: float = 2.0, batch: int = 1, blocks: int | None = None,
+                      generator=None, act_dtype=None, scale_dtype=None, device="cuda") -> DecodePlan:
+    """Synthetic random-init DBF factors of every linear layer of a Llama-2 model (§8d)."""
+    import torch
+
+    act_dtype = act_dtype or torch.float16
+    s = LLAMA_SHAPES[model]
+    nblocks = blocks if blocks is not None else s["blocks"]
+    shapes = block_shapes(model)
+    layers, ops = [], []
+    widths = {"h": s["hidden"], "q": s["hidden"], "k": s["kv"], "v": s["kv"], "o": s["hidden"],
+              "gate": s["inter"], "up": s["inter"]}
+    # activation buffers: 0 = block input h (also the output of down), one per layer output
+    names = ["h", "q", "k", "v", "o", "gate", "up"]
+    buffers = [torch.zeros((batch, widths[nm]), dtype=act_dtype, device=device) for nm in names]
+    idx = {nm: i for i, nm in enumerate(names)}
+    src_of = {"q": "h", "k": "h", "v": "h", "o": "v", "gate": "o", "up": "o", "down": "gate"}
+    dst_of = {"q": "q", "k": "k", "v": "v", "o": "o", "gate": "gate", "up": "up", "down": "h"}
+    for _ in range(nblocks):
+        for name, n, m in shapes:
+            k = middle_dim(n, m, bpw, 32)
+            layers.append(random_device_layer(n, k, m, generator=generator, scale_dtype=scale_dtype, device=device))
+            ops.append(PlanOp(len(layers) - 1, idx[src_of[name]], idx[dst_of[name]], name))
+    if s["kv"] != s["hidden"]:
+        # GQA (70B): v is narrower than o's input; o reads q's output instead
+        for op in ops:
+            if op.name == "o":
+                op.src = idx["q"]
+    return DecodePlan(layers, ops, buffers, input_buffer=idx["h"], output_buffer=idx["h"])

@@ -30,9 +30,13 @@
 namespace dbf {
 namespace engine {
 
-constexpr int kWarps = 15;                    // consumer warps (15 + 1 producer = 4 warps per SMSP)
+constexpr int kWarps = 14;                    // consumer warps (+ 1 finalizer + 1 producer = 4 per SMSP)
+constexpr int kFinWarp = kWarps;              // finalizer warp index
+constexpr int kDeal = 4;                      // chunks per dealt block (round-robin over warps)
+constexpr int kCycle = kWarps * kDeal;        // chunks per full dealing cycle
+constexpr int kProdWarp = kWarps + 1;         // producer warp index
 constexpr int kConsumers = kWarps * 32;
-constexpr int kThreads = kConsumers + 32;     // + 1 producer warp
+constexpr int kThreads = kConsumers + 64;     // + finalizer warp + producer warp
 constexpr int kSlotBytes = 16384;             // one ring slot = 32 chunks of 512 B
 constexpr int kSlotChunks = kSlotBytes / kChunkBytes;
 constexpr int kRegGroups = 6;                 // register-resident 4-column groups per thread
@@ -167,6 +171,8 @@ struct Smem {
   long long* red;   // [kRedBufs][kWarps][16]
   int* red_cnt;     // [kRedBufs] arrivals of the unit currently in each buffer
   int* red_fin;     // [kRedBufs] units finalized from each buffer
+  long long* run_T; // [2*kRedBufs] T of the run (by run sequence), for the finalizer
+  int* run_F;       // [2*kRedBufs] F of the run
   float* red_max;   // [kWarps]
   long long* red_sum;  // [kWarps]
   uint64_t* full;
@@ -308,7 +314,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   sm.red = (long long*)(sm.xfrag + xfrag_bytes);
   sm.red_cnt = (int*)(sm.red + kRedBufs * 32);  // red: kRedBufs x 64 int32
   sm.red_fin = sm.red_cnt + kRedBufs;
-  sm.red_max = (float*)(sm.red_fin + kRedBufs);
+  sm.run_T = (long long*)(sm.red_fin + kRedBufs);
+  sm.run_F = (int*)(sm.run_T + 2 * kRedBufs);
+  sm.red_max = (float*)(sm.run_F + 2 * kRedBufs);
   sm.red_sum = (long long*)(sm.red_max + 16);  // 16 floats: keeps the int64 array 8-byte aligned
   sm.full = (uint64_t*)(sm.red_sum + 16);
   sm.empty = sm.full + kMaxSlots;
@@ -332,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   const uint32_t run_ctr = *prog.run_counter;
   const uint32_t ebase = run_ctr * (uint32_t)prog.nvectors + 1u;
 
-  if (warp == kWarps) {
+  if (warp == kProdWarp) {
     // ---------------- producer: stream each run's packed signs (contiguous) into the ring -----
     // The run record is staged into the header of the run's first slot (consumers read it from
     // shared memory); the next record is prefetched while the current run's pieces are issued.
@@ -369,81 +377,58 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     return;
   }
 
-  // ---------------- consumers ---------------------------------------------------------------
-  // A run's chunks are dealt round-robin over the 15 consumer warps (continuing across runs),
-  // so no warp waits for another per unit.  When a warp leaves a unit it drops its partial
-  // into a ring of kRedBufs per-unit buffers; the last of the min(15, nch) contributors
-  // finalizes the unit (exact sum, scales, LL publish, ready-counter bump).
-  const int g = lane >> 2, tig = lane & 3;
-  const uint2* xlane = (const uint2*)sm.xfrag + (lane & 15);  // lanes 16-31 mirror 0-15 (ignored cols)
-  int slot = 0;
-  uint32_t phase = 0;
-  int cur_seg = -1;
-  int F = 0;
-  long long T = 0;
-  double inv_scale = 1.0;
-  int dealt = 0;      // chunks dealt on this CTA so far, mod kWarps
-  int unit_seq = 0;   // units completed on this CTA before the current run
-  for (int i = r0; i < r1; ++i) {
-    int64_t* tr = prog.trace ? prog.trace + 4 * (size_t)i : nullptr;
-    if (tr && threadIdx.x == 0) tr[0] = gtimer();
-    mbar_wait(&sm.full[slot], phase);  // first piece of the run: its header holds the record
-    const dbf_engine_run& H = sm.hdr[slot];
-    const int rows = H.rows, cols = H.cols, rb = H.rb, nunits = H.nunits;
-    const void* oscale = H.oscale;
-    const int scale_dtype = H.scale_dtype, out_dtype = H.out_dtype;
-    void* out_plain = H.out_plain;
-    unsigned long long* ll_out = (unsigned long long*)H.ll_out;
-    uint32_t* ready_out = H.ready_out;
-    const uint32_t out_epoch = ebase + (uint32_t)H.out_vec;
-    if (H.seg != cur_seg) {
-      InSpec in;
-      in.x = H.x;
-      in.iscale = H.iscale;
-      in.kind = H.in_kind;
-      in.dtype = H.in_dtype;
-      in.scale_dtype = scale_dtype;
-      in.cols = cols;
-      prepare(in, ebase + (uint32_t)H.in_vec, sm, F, T, H.ready_in, (run_ctr + 1u) * H.in_producers);
-      cur_seg = H.seg;
-      inv_scale = __longlong_as_double((long long)(1023 - F) << 52);  // 2^-F
-    }
-    if (tr && threadIdx.x == 0) tr[1] = gtimer();
-    const int nch = (cols + kChunkCols - 1) / kChunkCols;
-    const int total = nunits * nch;
-    const int need = nch < kWarps ? nch : kWarps;  // contributors per unit
-    int gch = warp - dealt;
-    if (gch < 0) gch += kWarps;
-    int u = gch / nch, cu = gch - u * nch;
-    int cur_u = -1;
-    uint32_t osc_raw = 0;  // raw bits of this unit's output scale; converted only by the finalizer
-    int acc[4][4] = {};
-
-    auto flush = [&](int uu) {
-      // add this warp's int32 plane sums into the unit's 16x4 accumulator (exact, order-free)
-      const int c0 = acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0];
-      const int c1 = acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1];
-      const int c2 = acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2];
-      const int c3 = acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3];
-      const int seq = unit_seq + uu;
-      const int rbuf = seq & (kRedBufs - 1);
-      int* red = (int*)sm.red + rbuf * 64;  // [row 16][plane 4] int32
-      while (*(volatile int*)&sm.red_fin[rbuf] != seq / kRedBufs) {
+  if (warp == kFinWarp) {
+    // ---------------- finalizer: completes units in order as their contributions land -------
+    // (exact digit recombination, scales, LL publish + ready-counter bump), so the consumer
+    // warps never stall on epilogues and stay close together over the ring.
+    const dbf_engine_run* R = prog.runs;
+    int seq = 0;
+    int dealt = 0;  // chunks dealt before the current run, mod kCycle (mirrors the consumers)
+    for (int i = r0; i < r1; ++i) {
+      const dbf_engine_run& run = R[i];
+      const int rows = run.rows, cols = run.cols, rb = run.rb, nunits = run.nunits;
+      const void* oscale = run.oscale;
+      const int scale_dtype = run.scale_dtype, out_dtype = run.out_dtype;
+      void* out_plain = run.out_plain;
+      unsigned long long* ll_out = (unsigned long long*)run.ll_out;
+      uint32_t* ready_out = run.ready_out;
+      const uint32_t out_epoch = ebase + (uint32_t)run.out_vec;
+      const int nch = (cols + kChunkCols - 1) / kChunkCols;
+      uint32_t osc_next = 0;
+      {
+        const int row = rb * 16 + (lane & 15);
+        if (oscale && row < rows)
+          osc_next = scale_dtype == DBF_F16 ? (uint32_t)__ldg((const unsigned short*)oscale + row)
+                                            : __ldg((const uint32_t*)oscale + row);
       }
-      if (tig < 2) {
-        red_add_s32(&red[g * 4 + 2 * tig], c0);
-        red_add_s32(&red[g * 4 + 2 * tig + 1], c1);
-        red_add_s32(&red[(g + 8) * 4 + 2 * tig], c2);
-        red_add_s32(&red[(g + 8) * 4 + 2 * tig + 1], c3);
-      }
-      __syncwarp();
-      fence_cta();
-      int old = 0;
-      if (lane == 0) old = atomicAdd(&sm.red_cnt[rbuf], 1);
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (old == need - 1) {
-        // last contributor: all partial sums have landed (fence + counter order)
+      const int rs = (i - r0) & (2 * kRedBufs - 1);
+      bool have_FT = false;
+      int F = 0;
+      long long T = 0;
+      double inv_scale = 1.0;
+      for (int uu = 0; uu < nunits; ++uu, ++seq) {
+        const uint32_t osc_raw = osc_next;
+        if (uu + 1 < nunits) {  // prefetch the next unit's output scale
+          const int row = (rb + uu + 1) * 16 + (lane & 15);
+          if (oscale && row < rows)
+            osc_next = scale_dtype == DBF_F16 ? (uint32_t)__ldg((const unsigned short*)oscale + row)
+                                              : __ldg((const uint32_t*)oscale + row);
+        }
+        const int rbuf = seq & (kRedBufs - 1);
+        // contributors = dealt blocks intersecting the unit (one flush per warp per unit)
+        const int v0 = dealt + uu * nch, v1 = v0 + nch - 1;
+        int need = v1 / kDeal - v0 / kDeal + 1;
+        need = need < kWarps ? need : kWarps;
+        while (*(volatile int*)&sm.red_cnt[rbuf] < need) {
+        }
         fence_cta();
+        if (!have_FT) {  // written by the consumers before their first contribution to this run
+          F = *(volatile int*)&sm.run_F[rs];
+          T = *(volatile long long*)&sm.run_T[rs];
+          inv_scale = __longlong_as_double((long long)(1023 - F) << 52);  // 2^-F
+          have_FT = true;
+        }
+        int* red = (int*)sm.red + rbuf * 64;
         const int row = (rb + uu) * 16 + lane;
         if (lane < 16) {
           int4* pp = (int4*)&red[lane * 4];
@@ -474,7 +459,81 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           fence_cta();
           *(volatile int*)&sm.red_fin[rbuf] = seq / kRedBufs + 1;
         }
+        __syncwarp();
       }
+      dealt = (dealt + nunits * nch) % kCycle;
+    }
+    return;
+  }
+
+  // ---------------- consumers ---------------------------------------------------------------
+  // A run's chunks are dealt round-robin over the 15 consumer warps (continuing across runs),
+  // so no warp waits for another per unit.  When a warp leaves a unit it drops its partial
+  // (int32 shared-memory reductions, exact) into a ring of kRedBufs per-unit accumulators and
+  // bumps the unit's arrival count; the finalizer warp completes units in order.
+  const int g = lane >> 2, tig = lane & 3;
+  const uint2* xlane = (const uint2*)sm.xfrag + (lane & 15);  // lanes 16-31 mirror 0-15 (ignored cols)
+  int slot = 0;
+  uint32_t phase = 0;
+  int cur_seg = -1;
+  int F = 0;
+  long long T = 0;
+  int dealt = 0;      // chunks dealt on this CTA so far, mod kCycle
+  int unit_seq = 0;   // units completed on this CTA before the current run
+  for (int i = r0; i < r1; ++i) {
+    int64_t* tr = prog.trace ? prog.trace + 4 * (size_t)i : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtimer();
+    mbar_wait(&sm.full[slot], phase);  // first piece of the run: its header holds the record
+    const dbf_engine_run& H = sm.hdr[slot];
+    const int rows = H.rows, cols = H.cols, rb = H.rb, nunits = H.nunits;
+    if (H.seg != cur_seg) {
+      InSpec in;
+      in.x = H.x;
+      in.iscale = H.iscale;
+      in.kind = H.in_kind;
+      in.dtype = H.in_dtype;
+      in.scale_dtype = H.scale_dtype;
+      in.cols = cols;
+      prepare(in, ebase + (uint32_t)H.in_vec, sm, F, T, H.ready_in, (run_ctr + 1u) * H.in_producers);
+      cur_seg = H.seg;
+    }
+    if (threadIdx.x == 0) {  // F/T of this run for the finalizer; depth 2*kRedBufs runs is safe:
+      // reaching run i+2R means unit seq(i)+2R-1 was flushed, which waited for seq(i)+R-1 done
+      sm.run_F[(i - r0) & (2 * kRedBufs - 1)] = F;
+      sm.run_T[(i - r0) & (2 * kRedBufs - 1)] = T;
+    }
+    if (tr && threadIdx.x == 0) tr[1] = gtimer();
+    const int nch = (cols + kChunkCols - 1) / kChunkCols;
+    const int total = nunits * nch;
+    // virtual chunk index v = run chunk + dealt; this warp owns v with (v / kDeal) % kWarps == warp
+    int v = warp * kDeal;  // this warp's first block of the cycle
+    if (v + kDeal <= dealt) v += kCycle;  // already passed: take the next cycle's block
+    else if (v < dealt) v = dealt;        // the run starts inside this warp's block
+    int gch = v - dealt;
+    int u = gch / nch, cu = gch - u * nch;
+    int cur_u = -1;
+    int acc[4][4] = {};
+
+    auto flush = [&](int uu) {
+      // add this warp's int32 plane sums into the unit's 16x4 accumulator (exact, order-free)
+      const int c0 = acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0];
+      const int c1 = acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1];
+      const int c2 = acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2];
+      const int c3 = acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3];
+      const int seq = unit_seq + uu;
+      const int rbuf = seq & (kRedBufs - 1);
+      int* red = (int*)sm.red + rbuf * 64;  // [row 16][plane 4] int32
+      while (*(volatile int*)&sm.red_fin[rbuf] != seq / kRedBufs) {
+      }
+      if (tig < 2) {
+        red_add_s32(&red[g * 4 + 2 * tig], c0);
+        red_add_s32(&red[g * 4 + 2 * tig + 1], c1);
+        red_add_s32(&red[(g + 8) * 4 + 2 * tig], c2);
+        red_add_s32(&red[(g + 8) * 4 + 2 * tig + 1], c3);
+      }
+      __syncwarp();
+      fence_cta();
+      if (lane == 0) atomicAdd(&sm.red_cnt[rbuf], 1);
     };
 
     bool first_piece = true;
@@ -484,16 +543,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       if (tr && threadIdx.x == 0 && first_piece) tr[2] = gtimer();
       first_piece = false;
       const uint4* piece = (const uint4*)(sm.ring + (size_t)slot * kSlotBytes) + lane;
-      for (; gch < pe; gch += kWarps) {
+      for (; gch < pe;) {
         if (u != cur_u) {
           if (cur_u >= 0) flush(cur_u);
           cur_u = u;
 #pragma unroll
           for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0;
-          const int row = (rb + u) * 16 + (lane & 15);
-          if (oscale && row < rows)
-            osc_raw = scale_dtype == DBF_F16 ? (uint32_t)__ldg((const unsigned short*)oscale + row)
-                                             : __ldg((const uint32_t*)oscale + row);
         }
         const uint4 w = piece[(gch - pb) * 32];
         const uint2* xk = xlane + cu * 8 * 16;
@@ -503,7 +558,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           const uint2 b = xk[r * 16];
           imma(acc[r & 3], w.x & m, w.y & m, w.z & m, w.w & m, b.x, b.y);
         }
-        cu += kWarps;
+        // next owned chunk: +1 inside the block, else jump to this warp's next block
+        int step = 1;
+        if (((gch + dealt + 1) % kDeal) == 0) step = 1 + (kWarps - 1) * kDeal;
+        gch += step;
+        cu += step;
         while (cu >= nch) { cu -= nch; ++u; }
       }
       __syncwarp();
@@ -512,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     }
     if (cur_u >= 0) flush(cur_u);
     if (tr && threadIdx.x == 0) tr[3] = gtimer();
-    dealt = (dealt + total) % kWarps;
+    dealt = (dealt + total) % kCycle;
     unit_seq += nunits;
   }
 }
@@ -521,7 +580,7 @@ __global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; 
 
 int ring_slots_for(int xfrag_bytes) {
   const int fixed = xfrag_bytes + kMaxSlots * (int)sizeof(dbf_engine_run) + kRedBufs * 64 * 4 +
-                    2 * kRedBufs * 4 + 16 * 4 + 16 * 8 + 2 * kMaxSlots * 8 + 256;
+                    2 * kRedBufs * 4 + 2 * kRedBufs * 12 + 16 * 4 + 16 * 8 + 2 * kMaxSlots * 8 + 256;
   int slots = (kMaxSmem - fixed) / kSlotBytes;
   return std::min(slots, kMaxSlots);
 }
@@ -531,7 +590,7 @@ int xfrag_bytes_for(int max_cols) {
 }
 size_t smem_bytes(int slots, int xfrag_bytes) {
   return (size_t)slots * kSlotBytes + kMaxSlots * sizeof(dbf_engine_run) + xfrag_bytes +
-         kRedBufs * 64 * 4 + 2 * kRedBufs * 4 + 16 * 4 + 16 * 8 + 2 * kMaxSlots * 8 + 64;
+         kRedBufs * 64 * 4 + 2 * kRedBufs * 4 + 2 * kRedBufs * 12 + 16 * 4 + 16 * 8 + 2 * kMaxSlots * 8 + 64;
 }
 
 }  // namespace engine

@@ -170,7 +170,7 @@ class DeviceLayer:
         dev = torch.device(device) if device is not None else torch.device("cuda")
 
         def vec(v):
-            return torch.as_tensor(np.asarray(v, dtype=np.float64)).to(device=dev, dtype=scale_dtype)
+            return torch.as_tensor(np.array(v, dtype=np.float64)).to(device=dev, dtype=scale_dtype)
 
         A = DeviceSignMatrix.from_host(layer.A, dev, keep_words=keep_words)
         B = DeviceSignMatrix.from_host(layer.B, dev, keep_words=keep_words)

@@ -1,0 +1,163 @@
+"""Middle-dimension (k) sharding of one DBF layer across the GPUs of a node.
+
+    y = a * (A . (mid * (B . (b * x))))  =  a * sum_g  A[:, K_g] . (mid[K_g] * (B[K_g, :] . (b * x)))
+
+Rank g owns rows K_g of B, columns K_g of A and mid[K_g]; x, b and a are replicated.  Each rank
+computes its fp32 partial ``P_g = A_g . (mid_g * (B_g . (b * x)))`` with no communication
+(``dbf_forward_partial``), one SUM all-reduce combines the partials over NVLink (NCCL through
+``torch.distributed``), and ``y = a * P`` is applied after the reduce (``dbf_finalize_partial``).
+
+Shard boundaries are multiples of 32 columns so every shard of A is a word-aligned slice of the
+packed rows (the reference's LSB-first layout, bitcore.py:7-9): k = 12736 over 4 ranks gives
+3200/3200/3200/3136 (12736/4 = 3184 is not word-aligned).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .bitcore import SignMatrix, row_bytes
+
+
+def shard_bounds(k: int, world: int, align: int = 32) -> list[tuple[int, int]]:
+    """Contiguous [k0, k1) ranges covering 0..k, boundaries multiples of ``align``, sizes
+    balanced to within one alignment block; trailing ranks may be empty if k is tiny."""
+    if k < 1 or world < 1 or align < 1:
+        raise ValueError("k, world and align must be >= 1")
+    blocks = -(-k // align)
+    bounds = []
+    for r in range(world):
+        b0 = (r * blocks) // world
+        b1 = ((r + 1) * blocks) // world
+        bounds.append((min(b0 * align, k), min(b1 * align, k)))
+    return bounds
+
+
+def slice_columns(bits: np.ndarray, cols: int, c0: int, c1: int) -> np.ndarray:
+    """Reference row bytes of columns [c0, c1) (c0 a multiple of 8) of a packed sign matrix."""
+    if c0 % 8:
+        raise ValueError("column slices must start on a byte boundary")
+    if not (0 <= c0 < c1 <= cols):
+        raise ValueError(f"bad column range [{c0}, {c1}) for {cols} columns")
+    out = np.ascontiguousarray(bits[:, c0 // 8 : c0 // 8 + row_bytes(c1 - c0)]).copy()
+    tail = (c1 - c0) % 8
+    if tail:
+        out[:, -1] &= (1 << tail) - 1  # padding bits beyond c1 must be zero
+    return out
+
+
+@dataclass(frozen=True)
+class LayerShard:
+    """Host-side shard of a DbfLayer for rank `rank` of `world` (k range [k0, k1))."""
+
+    rank: int
+    world: int
+    k0: int
+    k1: int
+    a: np.ndarray
+    A: SignMatrix  # n x (k1 - k0)
+    mid: np.ndarray  # (k1 - k0,)
+    B: SignMatrix  # (k1 - k0) x m
+    b: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.A.rows
+
+    @property
+    def k_shard(self) -> int:
+        return self.k1 - self.k0
+
+    @property
+    def m_dim(self) -> int:
+        return self.B.cols
+
+
+def shard_layer(layer, rank: int, world: int, align: int = 32) -> LayerShard:
+    """Cut the k-shard of `rank` out of a host DbfLayer (ours or the reference's)."""
+    k = layer.A.cols
+    k0, k1 = shard_bounds(k, world, align)[rank]
+    if k1 <= k0:
+        raise ValueError(f"rank {rank} has an empty shard of k={k} over {world} ranks")
+    A_bits = slice_columns(np.asarray(layer.A.bits), k, k0, k1)
+    B_bits = np.ascontiguousarray(np.asarray(layer.B.bits)[k0:k1]).copy()
+    return LayerShard(
+        rank, world, k0, k1,
+        np.asarray(layer.a, dtype=np.float64),
+        SignMatrix(layer.A.rows, k1 - k0, A_bits),
+        np.asarray(layer.mid, dtype=np.float64)[k0:k1].copy(),
+        SignMatrix(k1 - k0, layer.B.cols, B_bits),
+        np.asarray(layer.b, dtype=np.float64),
+    )
+
+
+class DeviceShard:
+    """Device image of a LayerShard (tiled A_g, B_g; scales in `scale_dtype`)."""
+
+    def __init__(self, shard: LayerShard, scale_dtype=None, device=None):
+        import torch
+
+        from .device import DeviceSignMatrix
+
+        sd = scale_dtype or torch.float32
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.shard = shard
+        self.A = DeviceSignMatrix.from_host(shard.A, dev, keep_words=False)
+        self.B = DeviceSignMatrix.from_host(shard.B, dev, keep_words=False)
+        self.a = torch.as_tensor(shard.a).to(dev, sd)
+        self.mid = torch.as_tensor(shard.mid).to(dev, sd)
+        self.b = torch.as_tensor(shard.b).to(dev, sd)
+
+    def partial(self, X):
+        """fp32 partial P_g (batch x n) for a CUDA tensor X (batch x m)."""
+        import torch
+
+        from . import _lib
+        from .kernel import _workspace
+
+        sh = self.shard
+        X2 = X if X.ndim == 2 else X.unsqueeze(0)
+        X2 = X2.contiguous()
+        P = torch.empty((X2.shape[0], sh.n), dtype=torch.float32, device=X2.device)
+        ws_bytes = _lib.lib.dbf_forward_workspace_bytes(sh.n, sh.k_shard, sh.m_dim, X2.shape[0])
+        ws = _workspace(ws_bytes, X2.device)
+        _lib.check(
+            _lib.lib.dbf_forward_partial(
+                self.A.tiled.data_ptr(), self.B.tiled.data_ptr(), self.mid.data_ptr(), self.b.data_ptr(),
+                _lib.dtype_code(self.a.dtype), sh.n, sh.k_shard, sh.m_dim, X2.data_ptr(), _lib.dtype_code(X2.dtype),
+                X2.shape[0], X2.stride(0), P.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(),
+            ),
+            "dbf_forward_partial",
+        )
+        return P
+
+    def finalize(self, P, out_dtype=None):
+        import torch
+
+        from . import _lib
+
+        Y = torch.empty(P.shape, dtype=out_dtype or torch.float16, device=P.device)
+        _lib.check(
+            _lib.lib.dbf_finalize_partial(
+                P.data_ptr(), self.a.data_ptr(), _lib.dtype_code(self.a.dtype), P.shape[1], P.shape[0],
+                Y.data_ptr(), _lib.dtype_code(Y.dtype), Y.stride(0), _lib.stream_ptr(),
+            ),
+            "dbf_finalize_partial",
+        )
+        return Y
+
+    def forward(self, X, group=None, out_dtype=None):
+        """y = a * all_reduce_sum(P_g): one NCCL SUM all-reduce of n x batch fp32 values."""
+        import torch.distributed as dist
+
+        P = self.partial(X)
+        dist.all_reduce(P, op=dist.ReduceOp.SUM, group=group)
+        return self.finalize(P, out_dtype=out_dtype or X.dtype)
+
+
+def reduce_partials_host(partials, a) -> np.ndarray:
+    """Host restatement of the combine step (used by the CPU multi-process tests)."""
+    total = np.sum(np.stack(partials), axis=0)
+    return total * np.asarray(a)[None, :]

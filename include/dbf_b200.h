@@ -251,6 +251,33 @@ int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, int32_t* regs
 /* Launch one run of the program (cooperative: all CTAs co-resident) + the epoch advance. */
 int dbf_engine_launch(const dbf_engine_program* program, void* stream);
 
+/* ---- prefill / batched path: tcgen05 + TMEM sign GEMMs (>= 64 tokens) ------------------ */
+/*
+ * The same forward as dbf_forward (kernel.py:48-62) for token batches, as two tensor-core GEMMs
+ * with fp16 activations and fp32 accumulation in tensor memory:
+ *   t = mid * (X . (B * b)^T)   (fp16 workspace, T x dbf_prefill_ld(k))
+ *   Y = a   * (t . A^T)
+ * Sign matrices are read in the CANONICAL layout and expanded to +-1 (times b for B) on chip.
+ * Activations and scales are fp16; X must have ldx % 8 == 0 and a 16-byte aligned base
+ * (DBF_ERR_UNSUPPORTED otherwise).  Not bitwise reproducible against dbf_forward: products
+ * are exact, sums are fp32 and t is rounded to fp16 (DESIGN.md §5 tolerance).
+ */
+int64_t dbf_prefill_ld(int64_t cols);
+size_t dbf_prefill_workspace_bytes(int64_t k, int64_t tokens);
+
+/* One sign GEMM: out[i, r] = rscale[r] * sum_c S[r, c] * kscale[c] * act[i, c]   (fp16 in/out)
+ * act: tokens x K (stride ld_act), S: rows x K canonical words, out: tokens x rows (stride ldo);
+ * kscale / rscale may be NULL (= 1).  Replaces one staged sign_matvec of kernel.py:58-61. */
+int dbf_sign_gemm(const void* act, int64_t tokens, int64_t K, int64_t ld_act, const uint32_t* words,
+                  int64_t word_pitch, int64_t rows, const void* kscale, const void* rscale, void* out,
+                  int64_t ldo, void* stream);
+
+/* kernel.forward (kernel.py:48-62) for a token batch: X tokens x m fp16 -> Y tokens x n fp16. */
+int dbf_forward_prefill(const uint32_t* A_words, int64_t A_pitch, const uint32_t* B_words,
+                        int64_t B_pitch, const void* a, const void* mid, const void* b, int64_t n,
+                        int64_t k, int64_t m, const void* X, int64_t tokens, int64_t ldx, void* Y,
+                        int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

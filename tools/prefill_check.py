@@ -1,0 +1,64 @@
+"""Quick GPU check of the tcgen05 prefill sign GEMM against a torch fp32 reference, plus timing.
+
+python tools/prefill_check.py [T n k m]
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+
+import paper_2505_11076_b200 as P
+from paper_2505_11076_b200 import _lib
+
+
+def main():
+    T, n, k, m = (int(v) for v in sys.argv[1:5]) if len(sys.argv) >= 5 else (512, 384, 320, 512)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    layer = P.random_device_layer(n, k, m, generator=g, keep_words=True)
+    X = torch.randn((T, m), generator=g, device="cuda").half()
+    # single GEMM check: out = rscale * (X . (B*b)^T)
+    Bd = layer.B.unpack(torch.float32)
+    out = torch.empty((T, k), dtype=torch.half, device="cuda")
+    _lib.check(_lib.lib.dbf_sign_gemm(X.data_ptr(), T, m, m, layer.B.words.data_ptr(), layer.B.words.shape[1], k,
+                                      layer.b.data_ptr(), layer.mid.data_ptr(), out.data_ptr(), k,
+                                      _lib.stream_ptr()), "dbf_sign_gemm")
+    ref = layer.mid.float()[None, :] * ((X.float() * layer.b.float()[None, :]) @ Bd.t())
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item() / ref.abs().max().item()
+    print(f"gemm1 T={T} rows={k} K={m}: max rel err {err:.3e}")
+    # full forward
+    ws = torch.empty(_lib.lib.dbf_prefill_workspace_bytes(k, T), dtype=torch.uint8, device="cuda")
+    Y = torch.empty((T, n), dtype=torch.half, device="cuda")
+
+    def run():
+        _lib.check(_lib.lib.dbf_forward_prefill(
+            layer.A.words.data_ptr(), layer.A.words.shape[1], layer.B.words.data_ptr(), layer.B.words.shape[1],
+            layer.a.data_ptr(), layer.mid.data_ptr(), layer.b.data_ptr(), n, k, m, X.data_ptr(), T, m,
+            Y.data_ptr(), n, ws.data_ptr(), ws.numel(), _lib.stream_ptr()), "dbf_forward_prefill")
+
+    run()
+    Ad = layer.A.unpack(torch.float32)
+    t = ref.half().float()
+    refY = layer.a.float()[None, :] * (t @ Ad.t())
+    torch.cuda.synchronize()
+    errY = (Y.float() - refY).abs().max().item() / refY.abs().max().item()
+    nrm = ((Y.float() - refY).norm() / refY.norm()).item()
+    print(f"forward: max rel err {errY:.3e}  norm rel err {nrm:.3e}")
+    for _ in range(3):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    e1.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    flops = 2.0 * T * k * (n + m)
+    print(f"forward {us:.1f} us  {flops / us / 1e6:.1f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    main()

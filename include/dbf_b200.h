@@ -257,23 +257,33 @@ int dbf_engine_launch(const dbf_engine_program* program, void* stream);
  * with fp16 activations and fp32 accumulation in tensor memory:
  *   t = mid * (X . (B * b)^T)   (fp16 workspace, T x dbf_prefill_ld(k))
  *   Y = a   * (t . A^T)
- * Sign matrices are read in the CANONICAL layout and expanded to +-1 (times b for B) on chip.
+ * Sign matrices are read in the PAIRED layout (dbf_pair_signs) and expanded to +-1 (times b for B)
+ * on chip, straight into tensor memory.
  * Activations and scales are fp16; X must have ldx % 8 == 0 and a 16-byte aligned base
  * (DBF_ERR_UNSUPPORTED otherwise).  Not bitwise reproducible against dbf_forward: products
  * are exact, sums are fp32 and t is rounded to fp16 (DESIGN.md §5 tolerance).
  */
+/* canonical words -> PAIRED prefill words (same pitch): per 32-column group, bit q (q < 16) holds
+ * column 2q and bit 16+q column 2q+1, so one shift puts the signs of an fp16 pair at bits 15/31. */
+int dbf_pair_signs(const uint32_t* words, int64_t rows, int64_t word_pitch, uint32_t* paired,
+                   void* stream);
+/* row pitch (elements) of the fp16 intermediate t in the prefill workspace */
 int64_t dbf_prefill_ld(int64_t cols);
 size_t dbf_prefill_workspace_bytes(int64_t k, int64_t tokens);
 
+/* Diagnostics: with DBF_PREFILL_TRACE set in the environment, the last sign GEMM launch records
+ * per-K-block clock64 stamps of CTA (0,0); copies n int64 of them to host memory. */
+int dbf_prefill_debug_trace(long long* host, int n);
+
 /* One sign GEMM: out[i, r] = rscale[r] * sum_c S[r, c] * kscale[c] * act[i, c]   (fp16 in/out)
- * act: tokens x K (stride ld_act), S: rows x K canonical words, out: tokens x rows (stride ldo);
+ * act: tokens x K (stride ld_act), S: rows x K paired words, out: tokens x rows (stride ldo);
  * kscale / rscale may be NULL (= 1).  Replaces one staged sign_matvec of kernel.py:58-61. */
-int dbf_sign_gemm(const void* act, int64_t tokens, int64_t K, int64_t ld_act, const uint32_t* words,
+int dbf_sign_gemm(const void* act, int64_t tokens, int64_t K, int64_t ld_act, const uint32_t* paired,
                   int64_t word_pitch, int64_t rows, const void* kscale, const void* rscale, void* out,
                   int64_t ldo, void* stream);
 
 /* kernel.forward (kernel.py:48-62) for a token batch: X tokens x m fp16 -> Y tokens x n fp16. */
-int dbf_forward_prefill(const uint32_t* A_words, int64_t A_pitch, const uint32_t* B_words,
+int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired,
                         int64_t B_pitch, const void* a, const void* mid, const void* b, int64_t n,
                         int64_t k, int64_t m, const void* X, int64_t tokens, int64_t ldx, void* Y,
                         int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);

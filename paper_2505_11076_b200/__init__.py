@@ -27,6 +27,7 @@ from .kernel import (
     bench_forward,
     forward,
     forward_device,
+    forward_prefill,
     random_device_layer,
     sign_matvec,
     sign_matvec_device,
@@ -47,6 +48,7 @@ __all__ = [
     "dumps_dbf",
     "forward",
     "forward_device",
+    "forward_prefill",
     "load_dbf",
     "middle_dim",
     "pack",

@@ -114,6 +114,19 @@ inline unsigned grid_for(int64_t n, int threads) { return (unsigned)ceil_div(n, 
 
 using namespace dbf;
 
+// ---- canonical words -> paired prefill layout: per 32-column word, bit i (i < 16) holds column
+// 2i and bit 16 + i holds column 2i + 1, so ONE shift brings the signs of the fp16 pair
+// (2q, 2q+1) to bit positions 15 / 31 (prefill.cu).  Same pitch, padding bits stay zero.
+__global__ void pair_kernel(const uint32_t* __restrict__ words, int64_t n, uint32_t* __restrict__ paired) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t c = words[i];
+  uint32_t p = 0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) p |= ((c >> (2 * b)) & 1u) << b | ((c >> (2 * b + 1)) & 1u) << (16 + b);
+  paired[i] = p;
+}
+
 extern "C" int dbf_pack_signs(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t ld,
                               uint32_t* words, int64_t word_pitch, int64_t* d_first_bad,
                               void* stream) {
@@ -173,5 +186,13 @@ extern "C" int dbf_tile_signs(const uint32_t* words, int64_t rows, int64_t cols,
   const int64_t total = row_blocks(rows) * nch * (kChunkBytes / 4);
   tile_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
       words, rows, cols, word_pitch, nch, (uint32_t*)tiled, total);
+  return check_launch();
+}
+
+extern "C" int dbf_pair_signs(const uint32_t* words, int64_t rows, int64_t word_pitch, uint32_t* paired,
+                              void* stream) {
+  if (!words || !paired || rows < 1 || word_pitch < 1) return DBF_ERR_INVALID_ARGUMENT;
+  const int64_t n = rows * word_pitch;
+  pair_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(words, n, paired);
   return check_launch();
 }

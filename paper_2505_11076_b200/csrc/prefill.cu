@@ -6,21 +6,27 @@
 //   GEMM2  Y[T, n] = a   (.) ( t[T, k] . A^T )              A: n x k signs
 //
 // One kernel, `sign_gemm_kernel`, runs either GEMM: out[T, rows] = rscale (.) (act . (S (.) kscale)^T)
-// with S a rows x K sign matrix in the canonical word layout (include/dbf_b200.h).
+// with S a rows x K sign matrix in the PAIRED word layout (include/dbf_b200.h, dbf_pair_signs).
 //
-// Per CTA: a 128 (sign rows) x 256 (tokens) output tile, accumulated in TMEM (256 fp32 columns).
-//   warp 0       TMA producer: 256 x 64 fp16 activation tiles (128-byte swizzle) into a smem ring.
-//   warp 1       TMEM allocator + MMA issuer (one thread): tcgen05.mma.kind::f16, M=128 N=256 K=16,
-//                A operand from TMEM, B operand (activations) from shared memory.
-//   warps 4..7   sign expanders, then epilogue.  Thread r owns sign row r of the tile (= TMEM
-//                lane r): it reads the row's 64 packed bits per K block and writes 64 fp16 values
-//                +-kscale[j] -- the fp16 sign bit XORed in from the packed bit -- straight into
-//                TMEM with tcgen05.st (32x32b.x32).  No shared-memory traffic for the weights: the
-//                +-1 expansion never leaves the tensor-memory side of the SM.
+// Per CTA: a 256 (sign rows) x 128 (tokens) output tile = two M=128 halves, each accumulated in
+// TMEM (2 x 128 fp32 columns).  256 rows per activation tile halve the L2->SM activation stream
+// per MMA (32 B/clk/SM at full tensor rate) -- the first bottleneck of a 128-row tile.
+//   warps 0,2,3  TMA producers: 128 x 64 fp16 activation tiles (128-byte swizzle) into a smem ring.
+//   warp 1       TMEM allocator + MMA issuer (one thread): tcgen05.mma.kind::f16, M=128 N=128 K=16,
+//                twice per K step (both M halves share the B tile), A operand (the expanded signs)
+//                from TMEM, B operand (activations) from smem.
+//   warps 4..19  sign expanders, then epilogue.  Warp w owns TMEM sub-partition w%4 (32 sign rows,
+//                one per lane) of M half ((w-4)/4)%2 and word (w-4)/8 of every 64-column K block:
+//                per K block a lane turns
+//                ONE 32-bit word of packed signs into 32 fp16 values +-kscale[c] -- one shift + one
+//                LOP3 per fp16 pair, the fp16 sign bit XORed in from the packed bit -- and writes
+//                them straight into TMEM with tcgen05.st (32x32b.x16).  The +-1 expansion never
+//                touches shared memory; the activation ring is the only smem traffic of the MMAs.
 //   epilogue     tcgen05.ld of the accumulator (lane = sign row, column = token), scale by
 //                rscale[row], fp16 store.
-// The ring stage s couples a smem activation tile and a TMEM A slot; both are released by the
+// Ring stage s couples a smem activation tile and a TMEM A slot; both are released by the
 // tcgen05.commit of the MMAs that read them.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include "common.cuh"
@@ -31,22 +37,33 @@ namespace prefill {
 
 using namespace sm100;
 
-constexpr int BM = 128;          // sign rows per tile (MMA M, TMEM lanes)
-constexpr int BN = 256;          // tokens per tile (MMA N, accumulator columns)
+constexpr int UM = 128;          // MMA M (TMEM lanes)
+#ifndef DBF_PREFILL_MH
+#define DBF_PREFILL_MH 1
+#endif
+constexpr int MH = DBF_PREFILL_MH;  // M halves per tile (accumulators)
+constexpr int BM = MH * UM;      // sign rows per tile
+constexpr int BN = 256 / MH;     // tokens per tile (MMA N, accumulator columns)
 constexpr int BK = 64;           // K per stage (one 128-byte swizzle atom of fp16)
 constexpr int UK = 16;           // K per tcgen05.mma (kind::f16)
-constexpr int STAGES = 4;
+#ifndef DBF_PREFILL_STAGES
+#define DBF_PREFILL_STAGES 6
+#endif
+constexpr int STAGES = DBF_PREFILL_STAGES;
 constexpr int kActStageBytes = BN * BK * 2;   // 32 KB
-constexpr int kAColsPerStage = BK / 2;        // 32 TMEM columns (2 fp16 per 32-bit column)
-constexpr int kAccCol = 0;
-constexpr int kACol0 = BN;                    // A slots after the accumulator
+constexpr int kAColsPerHalf = BK / 2;         // 32 TMEM columns (2 fp16 per 32-bit column)
+constexpr int kAColsPerStage = MH * kAColsPerHalf;
+constexpr int kAccCol = 0;                    // accumulator of M half h at column h * BN
+constexpr int kACol0 = MH * BN;               // A slots after the accumulators
 constexpr int kTmemCols = 512;
-constexpr int kThreads = 256;
 constexpr int kExpWarp0 = 4;
-static_assert(kACol0 + STAGES * kAColsPerStage <= kTmemCols, "TMEM budget");
+constexpr int kNumProducers = 3;              // warps 0, 2, 3
+constexpr int kExpWarps = 8 * MH;
+constexpr int kThreads = (kExpWarp0 + kExpWarps) * 32;
+constexpr int kMaxKScale = 32768;             // K columns whose kscale fits the smem copy
 
 struct Params {
-  const uint32_t* words;   // rows x pitch canonical words
+  const uint32_t* words;   // rows x pitch PAIRED words
   int64_t pitch;           // words per row
   const __half* kscale;    // K values or nullptr (= 1)
   const __half* rscale;    // rows values or nullptr (= 1)
@@ -54,6 +71,7 @@ struct Params {
   int64_t ldo;
   int rows, K, T;
   int num_kb;
+  long long* trace;        // debug: per-K-block clock64 stamps of CTA (0,0), or nullptr
 };
 
 struct __align__(8) Barriers {
@@ -64,30 +82,19 @@ struct __align__(8) Barriers {
   uint32_t tmem_base;
 };
 
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)STAGES * kActStageBytes + sizeof(Barriers);
+static_assert(kACol0 + STAGES * kAColsPerStage <= kTmemCols, "TMEM budget (A slots)");
+constexpr size_t kFixedSmem = 1024 /*align slack*/ + (size_t)STAGES * kActStageBytes + sizeof(Barriers) + 64;
+inline size_t smem_bytes(int num_kb, bool kscale) {
+  return kFixedSmem + (kscale ? (size_t)num_kb * BK * 2 : 0);
+}
 
-// 64 packed signs (bit i = column i, 1 <=> +1) -> 32 words of fp16 pairs +-ks, in K order.
-// Pair (2q, 2q+1) of the NEGATED bits moves to the fp16 sign positions 15 / 31 with one multiply:
-// p * (2^(15-2q) + 2^(30-2q)) puts bit 2q at 15 and bit 2q+1 at 31 (no carries), then
-// LOP3 ((prod & 0x80008000) ^ ks) applies it.
-template <bool KSCALE>
-__device__ __forceinline__ void expand_signs(uint64_t bits, const uint32_t* ks, uint32_t (&v)[32]) {
-  const uint32_t nw[2] = {~(uint32_t)bits, ~(uint32_t)(bits >> 32)};
+// One paired word (bit q <-> column 2q, bit 16+q <-> column 2q+1 of a 32-column group) -> 16 words of
+// fp16 pairs +-ks.  (~w << (15-q)) moves the NEGATED signs of the pair to the fp16 sign positions
+// 15 / 31; LOP3 ((x & 0x80008000) ^ ks) applies them.  ks = +1.0 pairs when there is no kscale.
+__device__ __forceinline__ void expand_word(uint32_t w, const uint32_t* ks, uint32_t (&v)[16]) {
+  const uint32_t nw = ~w;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-#pragma unroll
-    for (int half16 = 0; half16 < 2; ++half16) {
-      const uint32_t w = half16 ? (nw[h] >> 16) : nw[h];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t p = w & (3u << (2 * q));
-        const uint32_t mul = (1u << (15 - 2 * q)) + (1u << (30 - 2 * q));
-        const int idx = h * 16 + half16 * 8 + q;
-        const uint32_t base = KSCALE ? ks[idx] : 0x3C003C00u;
-        v[idx] = ((p * mul) & 0x80008000u) ^ base;
-      }
-    }
-  }
+  for (int q = 0; q < 16; ++q) v[q] = ((nw << (15 - q)) & 0x80008000u) ^ ks[q];
 }
 
 template <bool KSCALE>
@@ -97,6 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* act = smem;
   Barriers& bar = *reinterpret_cast<Barriers*>(smem + (size_t)STAGES * kActStageBytes);
+  uint32_t* ks_smem = reinterpret_cast<uint32_t*>(smem + (size_t)STAGES * kActStageBytes + sizeof(Barriers) + 64);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = blockIdx.x * BM;
@@ -105,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bar.full_act[s], 1);
-      mbar_init(&bar.full_a[s], 4);
+      mbar_init(&bar.full_a[s], kExpWarps);
       mbar_init(&bar.empty[s], 1);
     }
     mbar_init(&bar.acc_full, 1);
@@ -113,19 +121,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&act_map);
   }
   if (warp == 1) tmem_alloc<kTmemCols>(&bar.tmem_base);
+  if constexpr (KSCALE) {
+    // kscale as fp16 pairs, zero beyond K (those columns meet TMA zero-fill anyway)
+    const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
+    for (int i = threadIdx.x; i < p.num_kb * (BK / 2); i += kThreads) {
+      const int c = 2 * i;
+      const uint32_t lo = c < p.K ? src[c] : 0u, hi = c + 1 < p.K ? src[c + 1] : 0u;
+      ks_smem[i] = lo | (hi << 16);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
+  const bool tracing = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
 
-  if (warp == 0) {
-    // ---------------- TMA producer ----------------
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // ---------------- TMA producers ----------------
+    // One thread's TMA loads complete one after another (~500 clk per box on B200, measured:
+    // tools/microbench/tma.cu); three issuing warps keep three boxes in flight.
     if (lane == 0) {
+      const int prod = warp == 0 ? 0 : warp - 1;
       const uint64_t pol = policy_evict_last();  // activations are re-read by every row tile
-      for (int kb = 0; kb < p.num_kb; ++kb) {
+      for (int kb = prod; kb < p.num_kb; kb += kNumProducers) {
         const int s = kb % STAGES;
         const uint32_t ph = (kb / STAGES) & 1;
         mbar_wait(&bar.empty[s], ph ^ 1);
+        if (tracing) p.trace[5 * p.num_kb + kb] = clock64();
         mbar_arrive_expect_tx(&bar.full_act[s], kActStageBytes);
         tma_load_2d(act + (size_t)s * kActStageBytes, &act_map, kb * BK, tok0, &bar.full_act[s], pol);
       }
@@ -133,19 +155,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_f32(BM, BN);
+      constexpr uint32_t idesc = idesc_f16_f32(UM, BN);
       for (int kb = 0; kb < p.num_kb; ++kb) {
         const int s = kb % STAGES;
         const uint32_t ph = (kb / STAGES) & 1;
         mbar_wait(&bar.full_act[s], ph);
+        if (tracing) p.trace[4 * kb + 3] = clock64();
         mbar_wait(&bar.full_a[s], ph);
         tc_fence_after();
+        if (tracing) p.trace[4 * p.num_kb + kb] = clock64();
         const uint32_t a_base = tmem + kACol0 + s * kAColsPerStage;
         const uint32_t b_base = smem_u32(act + (size_t)s * kActStageBytes);
 #pragma unroll
         for (int kk = 0; kk < BK / UK; ++kk) {
-          mma_f16_ts(tmem + kAccCol, a_base + kk * (UK / 2), sdesc_k_sw128(b_base + kk * UK * 2), idesc,
-                     (kb | kk) != 0);
+          const uint64_t bd = sdesc_k_sw128(b_base + kk * UK * 2);
+#pragma unroll
+          for (int h = 0; h < MH; ++h)
+            mma_f16_ts(tmem + kAccCol + h * BN, a_base + h * kAColsPerHalf + kk * (UK / 2), bd, idesc,
+                       (kb | kk) != 0);
         }
         mma_commit(&bar.empty[s]);
       }
@@ -154,60 +181,66 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= kExpWarp0) {
     // ---------------- sign expanders + epilogue ----------------
     const int sub = warp & 3;                 // TMEM sub-partition this warp may access
-    const int r = sub * 32 + lane;            // tile row = TMEM lane
+    const int mh = ((warp - kExpWarp0) >> 2) % MH;  // M half (accumulator) of this warp's rows
+    const int half = ((warp - kExpWarp0) >> 2) / MH;  // which 32-column word of each K block
+    const int r = mh * UM + sub * 32 + lane;  // tile row
     const int grow = row0 + r;
     const bool live = grow < p.rows;
     const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
-    const uint32_t* wrow = p.words + (int64_t)(live ? grow : 0) * p.pitch;
-    uint64_t next = live ? *(const uint64_t*)(wrow) : 0ull;
+    const uint4* wrow = reinterpret_cast<const uint4*>(p.words + (int64_t)(live ? grow : 0) * p.pitch);
+    // one uint4 = words 4i..4i+3 = K blocks 2i (.x/.y) and 2i+1 (.z/.w); prefetched one ahead
+    const int nquads = (p.num_kb + 1) >> 1;
+    uint4 cur = make_uint4(0, 0, 0, 0), nxt = live ? __ldg(wrow) : make_uint4(0, 0, 0, 0);
+    const bool tr = tracing && threadIdx.x == 32 * kExpWarp0;
     for (int kb = 0; kb < p.num_kb; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
-      const uint64_t bits = next;
-      if (kb + 1 < p.num_kb && live) next = *(const uint64_t*)(wrow + 2 * (kb + 1));
-      uint32_t ks[KSCALE ? 32 : 1];
-      if constexpr (KSCALE) {
-        const int c0 = kb * BK;
-        if (c0 + BK <= p.K) {
-          const uint4* src = reinterpret_cast<const uint4*>(p.kscale + c0);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint4 u = __ldg(src + i);
-            ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
-          }
-        } else {
-          const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int c = c0 + 2 * i;
-            const uint32_t lo16 = c < p.K ? src[c] : 0u, hi16 = c + 1 < p.K ? src[c + 1] : 0u;
-            ks[i] = lo16 | (hi16 << 16);
-          }
-        }
+      if ((kb & 1) == 0) {
+        cur = nxt;
+        if (live && (kb >> 1) + 1 < nquads) nxt = __ldg(wrow + (kb >> 1) + 1);
       }
-      uint32_t v[32];
-      expand_signs<KSCALE>(bits, ks, v);
-      mbar_wait(&bar.empty[s], ph ^ 1);
+      const uint32_t w = (kb & 1) ? (half ? cur.w : cur.z) : (half ? cur.y : cur.x);
+      uint32_t ks[16];
+      if constexpr (KSCALE) {
+        const uint4* src = reinterpret_cast<const uint4*>(ks_smem + kb * (BK / 2) + half * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 u = src[i];
+          ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ks[i] = 0x3C003C00u;
+      }
+      uint32_t v[16];
+      expand_word(w, ks, v);
+      if (tr) p.trace[4 * kb] = clock64();
+      if (lane == 0) mbar_wait(&bar.empty[s], ph ^ 1);  // one poller per warp
+      __syncwarp();
+      if (tr) p.trace[4 * kb + 1] = clock64();
       tc_fence_after();
-      tmem_st32(tmem + lane_addr + kACol0 + s * kAColsPerStage, v);
+      tmem_st16(tmem + lane_addr + kACol0 + s * kAColsPerStage + mh * kAColsPerHalf + half * 16, v);
       tmem_wait_st();
       tc_fence_before();
+      if (tr) p.trace[4 * kb + 2] = clock64();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar.full_a[s]);
     }
-    // epilogue
-    mbar_wait(&bar.acc_full, 0);
+    // epilogue: this warp stores tokens [half*64, half*64+64) of its 32 rows (accumulator mh)
+    if (lane == 0) mbar_wait(&bar.acc_full, 0);
+    __syncwarp();
     tc_fence_after();
     const float rs = (live && p.rscale) ? __half2float(p.rscale[grow]) : 1.f;
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+    for (int c = 0; c < BN / 64; ++c) {
+      const int col = half * (BN / 2) + c * 32;
       uint32_t acc[32];
-      tmem_ld32(tmem + lane_addr + kAccCol + c * 32, acc);
+      tmem_ld32(tmem + lane_addr + kAccCol + mh * BN + col, acc);
       tmem_wait_ld();
       if (live) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int tok = tok0 + c * 32 + j;
+          const int tok = tok0 + col + j;
           if (tok < p.T) p.out[(int64_t)tok * p.ldo + grow] = __float2half_rn(__uint_as_float(acc[j]) * rs);
         }
       }
@@ -253,13 +286,17 @@ static int make_act_map(CUtensorMap* map, const void* act, int64_t T, int64_t K,
   return r == CUDA_SUCCESS ? DBF_OK : DBF_ERR_CUDA;
 }
 
+static long long* trace_buf = nullptr;
+
 static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_act, const uint32_t* words,
                             int64_t pitch, int64_t rows, const __half* kscale, const __half* rscale, __half* out,
                             int64_t ldo, cudaStream_t stream) {
   if (T < 1 || K < 1 || rows < 1) return DBF_ERR_INVALID_ARGUMENT;
   if ((ld_act * 2) % 16 != 0 || ((uintptr_t)act & 15) != 0 || ld_act < K) return DBF_ERR_UNSUPPORTED;
+  if (((uintptr_t)words & 15) != 0 || pitch % 4 != 0) return DBF_ERR_UNSUPPORTED;
   if (pitch * 32 < ceil_div(K, BK) * BK) return DBF_ERR_SHAPE;  // a K block would read past the row
   if (T > INT32_MAX || rows > INT32_MAX || K > INT32_MAX) return DBF_ERR_UNSUPPORTED;
+  if (kscale && K > kMaxKScale) return DBF_ERR_UNSUPPORTED;
   CUtensorMap map;
   int st = make_act_map(&map, act, T, K, ld_act);
   if (st != DBF_OK) return st;
@@ -274,22 +311,19 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   p.K = (int)K;
   p.T = (int)T;
   p.num_kb = (int)ceil_div(K, BK);
-  dim3 grid((unsigned)ceil_div(rows, BM), (unsigned)ceil_div(T, BN));
-  if (kscale) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(sign_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-      attr = true;
-    }
-    sign_gemm_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(map, p);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(sign_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-      attr = true;
-    }
-    sign_gemm_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(map, p);
+  p.trace = nullptr;
+  if (getenv("DBF_PREFILL_TRACE")) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 8 * 6 * 4096);
+    p.trace = trace_buf;
   }
+  dim3 grid((unsigned)ceil_div(rows, BM), (unsigned)ceil_div(T, BN));
+  const size_t smem = smem_bytes(p.num_kb, kscale != nullptr);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, kThreads, smem, stream>>>(map, p);
+  };
+  if (kscale) go(sign_gemm_kernel<true>);
+  else go(sign_gemm_kernel<false>);
   return check_launch();
 }
 
@@ -300,26 +334,34 @@ using namespace dbf;
 
 extern "C" {
 
+// debug: copy the last traced launch's stamps (5 * num_kb int64) to host memory
+int dbf_prefill_debug_trace(long long* host, int n) {
+  if (!prefill::trace_buf) return DBF_ERR_UNSUPPORTED;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, prefill::trace_buf, 8 * (size_t)n, cudaMemcpyDeviceToHost) == cudaSuccess ? DBF_OK
+                                                                                                    : DBF_ERR_CUDA;
+}
+
 int64_t dbf_prefill_ld(int64_t cols) { return ceil_div(cols, 64) * 64; }
 
 size_t dbf_prefill_workspace_bytes(int64_t k, int64_t tokens) {
   return (size_t)(tokens > 0 ? tokens : 0) * (size_t)dbf_prefill_ld(k) * 2;
 }
 
-int dbf_sign_gemm(const void* act, int64_t tokens, int64_t K, int64_t ld_act, const uint32_t* words,
+int dbf_sign_gemm(const void* act, int64_t tokens, int64_t K, int64_t ld_act, const uint32_t* paired,
                   int64_t word_pitch, int64_t rows, const void* kscale, const void* rscale, void* out, int64_t ldo,
                   void* stream) {
-  if (!act || !words || !out) return DBF_ERR_INVALID_ARGUMENT;
+  if (!act || !paired || !out) return DBF_ERR_INVALID_ARGUMENT;
   if (ldo < rows) return DBF_ERR_SHAPE;
-  return prefill::launch_sign_gemm(act, tokens, K, ld_act, words, word_pitch, rows, (const __half*)kscale,
+  return prefill::launch_sign_gemm(act, tokens, K, ld_act, paired, word_pitch, rows, (const __half*)kscale,
                                    (const __half*)rscale, (__half*)out, ldo, (cudaStream_t)stream);
 }
 
-int dbf_forward_prefill(const uint32_t* A_words, int64_t A_pitch, const uint32_t* B_words, int64_t B_pitch,
+int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired, int64_t B_pitch,
                         const void* a, const void* mid, const void* b, int64_t n, int64_t k, int64_t m,
                         const void* X, int64_t tokens, int64_t ldx, void* Y, int64_t ldy, void* workspace,
                         size_t workspace_bytes, void* stream) {
-  if (!A_words || !B_words || !a || !mid || !b || !X || !Y) return DBF_ERR_INVALID_ARGUMENT;
+  if (!A_paired || !B_paired || !a || !mid || !b || !X || !Y) return DBF_ERR_INVALID_ARGUMENT;
   if (n < 1 || k < 1 || m < 1 || tokens < 1) return DBF_ERR_INVALID_ARGUMENT;
   if (ldy < n || ldx < m) return DBF_ERR_SHAPE;
   if (A_pitch < canonical_pitch(k) || B_pitch < canonical_pitch(m)) return DBF_ERR_SHAPE;
@@ -327,10 +369,10 @@ int dbf_forward_prefill(const uint32_t* A_words, int64_t A_pitch, const uint32_t
   const int64_t ldt = dbf_prefill_ld(k);
   __half* t = (__half*)workspace;
   cudaStream_t s = (cudaStream_t)stream;
-  int st = prefill::launch_sign_gemm(X, tokens, m, ldx, B_words, B_pitch, k, (const __half*)b,
+  int st = prefill::launch_sign_gemm(X, tokens, m, ldx, B_paired, B_pitch, k, (const __half*)b,
                                      (const __half*)mid, t, ldt, s);
   if (st != DBF_OK) return st;
-  return prefill::launch_sign_gemm(t, tokens, k, ldt, A_words, A_pitch, n, nullptr, (const __half*)a,
+  return prefill::launch_sign_gemm(t, tokens, k, ldt, A_paired, A_pitch, n, nullptr, (const __half*)a,
                                    (__half*)Y, ldy, s);
 }
 

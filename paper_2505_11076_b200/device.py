@@ -104,6 +104,21 @@ class DeviceSignMatrix:
             raise ValueError("this DeviceSignMatrix was built without canonical words (keep_words=False)")
         return self.words
 
+    @property
+    def paired(self):
+        """The paired prefill layout (dbf_pair_signs), built once from the canonical words."""
+        import torch
+
+        if getattr(self, "_paired", None) is None:
+            w = self._need_words()
+            out = torch.empty_like(w)
+            _lib.check(
+                _lib.lib.dbf_pair_signs(w.data_ptr(), self.rows, w.shape[1], out.data_ptr(), _lib.stream_ptr()),
+                "dbf_pair_signs",
+            )
+            self._paired = out
+        return self._paired
+
     def to_host(self) -> SignMatrix:
         from .bitcore import words_to_bytes
 

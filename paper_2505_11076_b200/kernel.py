@@ -77,8 +77,63 @@ def as_device_signs(s) -> DeviceSignMatrix:
 # ---------------------------------------------------------------------------------------------
 # device fast path
 # ---------------------------------------------------------------------------------------------
+PREFILL_MIN_TOKENS = 64
+
+
+def _prefill_eligible(X2, layer: DeviceLayer, out_dtype) -> bool:
+    import torch
+
+    return (
+        X2.shape[0] >= PREFILL_MIN_TOKENS
+        and X2.dtype == torch.float16
+        and out_dtype == torch.float16
+        and layer.scale_dtype == torch.float16
+        and layer.A.words is not None
+        and layer.B.words is not None
+    )
+
+
+def forward_prefill(X, layer: DeviceLayer, out=None):
+    """Y = forward(X, layer) for a token batch on the tcgen05 tensor cores (prefill path).
+
+    X: CUDA fp16 tensor tokens x m; layer: fp16 scales with canonical words kept.  The two sign
+    GEMMs run with fp32 accumulation in tensor memory and an fp16 intermediate t."""
+    import torch
+
+    if X.ndim != 2:
+        raise ValueError(f"X must be 2-D, got ndim={X.ndim}")
+    if X.shape[1] != layer.m_dim:
+        raise ValueError(f"X has {X.shape[1]} columns, expected {layer.m_dim}")
+    if X.dtype != torch.float16 or layer.scale_dtype != torch.float16:
+        raise ValueError("the prefill path computes in fp16: X and the layer scales must be float16")
+    T, m = X.shape
+    if X.stride(1) != 1 or X.stride(0) % 8 or X.data_ptr() % 16:
+        # TMA needs a 16-byte aligned base and a row pitch that is a multiple of 16 bytes
+        ld = (m + 7) // 8 * 8
+        Xp = torch.empty((T, ld), dtype=X.dtype, device=X.device)
+        Xp[:, :m] = X
+        X = Xp[:, :m]
+    Y = out if out is not None else torch.empty((T, layer.n), dtype=torch.float16, device=X.device)
+    ws_bytes = _lib.lib.dbf_prefill_workspace_bytes(layer.k, T)
+    ws = _workspace(ws_bytes, X.device)
+    A, B = layer.A.paired, layer.B.paired
+    _lib.check(
+        _lib.lib.dbf_forward_prefill(
+            A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1],
+            layer.a.data_ptr(), layer.mid.data_ptr(), layer.b.data_ptr(), layer.n, layer.k, layer.m_dim,
+            X.data_ptr(), T, X.stride(0), Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(), _lib.stream_ptr(),
+        ),
+        "dbf_forward_prefill",
+    )
+    return Y
+
+
 def forward_device(X, layer: DeviceLayer, out=None, out_dtype=None):
-    """Y = forward(X, layer) for a CUDA tensor X (batch x m or m); returns a CUDA tensor."""
+    """Y = forward(X, layer) for a CUDA tensor X (batch x m or m); returns a CUDA tensor.
+
+    fp16 batches of >= PREFILL_MIN_TOKENS tokens on an fp16 layer run the tcgen05 prefill path
+    (forward_prefill); everything else -- decode batches, fp32/fp64 parity inputs -- runs the
+    exact-integer tensor-core GEMV (dbf_forward)."""
     import torch
 
     squeeze = X.ndim == 1
@@ -91,6 +146,8 @@ def forward_device(X, layer: DeviceLayer, out=None, out_dtype=None):
         X2 = X2.contiguous()
     batch = X2.shape[0]
     out_dtype = out_dtype or X2.dtype
+    if _prefill_eligible(X2, layer, out_dtype) and (out is None or (out.stride(1) == 1 and out.dtype == torch.float16)):
+        return forward_prefill(X2, layer, out=out)
     Y = out if out is not None else torch.empty((batch, layer.n), dtype=out_dtype, device=X2.device)
     ws_bytes = _lib.lib.dbf_forward_workspace_bytes(layer.n, layer.k, layer.m_dim, batch)
     ws = _workspace(ws_bytes, X2.device)

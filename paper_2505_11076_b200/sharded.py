@@ -106,9 +106,9 @@ class DeviceShard:
         self.shard = shard
         self.A = DeviceSignMatrix.from_host(shard.A, dev, keep_words=False)
         self.B = DeviceSignMatrix.from_host(shard.B, dev, keep_words=False)
-        self.a = torch.as_tensor(shard.a).to(dev, sd)
-        self.mid = torch.as_tensor(shard.mid).to(dev, sd)
-        self.b = torch.as_tensor(shard.b).to(dev, sd)
+        self.a = torch.as_tensor(np.array(shard.a)).to(dev, sd)
+        self.mid = torch.as_tensor(np.array(shard.mid)).to(dev, sd)
+        self.b = torch.as_tensor(np.array(shard.b)).to(dev, sd)
 
     def partial(self, X):
         """fp32 partial P_g (batch x n) for a CUDA tensor X (batch x m)."""

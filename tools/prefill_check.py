@@ -21,7 +21,7 @@ def main():
     # single GEMM check: out = rscale * (X . (B*b)^T)
     Bd = layer.B.unpack(torch.float32)
     out = torch.empty((T, k), dtype=torch.half, device="cuda")
-    _lib.check(_lib.lib.dbf_sign_gemm(X.data_ptr(), T, m, m, layer.B.words.data_ptr(), layer.B.words.shape[1], k,
+    _lib.check(_lib.lib.dbf_sign_gemm(X.data_ptr(), T, m, m, layer.B.paired.data_ptr(), layer.B.paired.shape[1], k,
                                       layer.b.data_ptr(), layer.mid.data_ptr(), out.data_ptr(), k,
                                       _lib.stream_ptr()), "dbf_sign_gemm")
     ref = layer.mid.float()[None, :] * ((X.float() * layer.b.float()[None, :]) @ Bd.t())
@@ -34,7 +34,7 @@ def main():
 
     def run():
         _lib.check(_lib.lib.dbf_forward_prefill(
-            layer.A.words.data_ptr(), layer.A.words.shape[1], layer.B.words.data_ptr(), layer.B.words.shape[1],
+            layer.A.paired.data_ptr(), layer.A.paired.shape[1], layer.B.paired.data_ptr(), layer.B.paired.shape[1],
             layer.a.data_ptr(), layer.mid.data_ptr(), layer.b.data_ptr(), n, k, m, X.data_ptr(), T, m,
             Y.data_ptr(), n, ws.data_ptr(), ws.numel(), _lib.stream_ptr()), "dbf_forward_prefill")
 
@@ -58,6 +58,25 @@ def main():
     us = e0.elapsed_time(e1) * 1e3 / reps
     flops = 2.0 * T * k * (n + m)
     print(f"forward {us:.1f} us  {flops / us / 1e6:.1f} TFLOP/s")
+
+    def g1():
+        _lib.lib.dbf_sign_gemm(X.data_ptr(), T, m, m, layer.B.paired.data_ptr(), layer.B.paired.shape[1], k,
+                               layer.b.data_ptr(), layer.mid.data_ptr(), out.data_ptr(), k, _lib.stream_ptr())
+
+    def g2():
+        _lib.lib.dbf_sign_gemm(out.data_ptr(), T, k, k, layer.A.paired.data_ptr(), layer.A.paired.shape[1], n,
+                               None, layer.a.data_ptr(), Y.data_ptr(), n, _lib.stream_ptr())
+
+    for name, fn, fl in (("gemm1", g1, 2.0 * T * k * m), ("gemm2", g2, 2.0 * T * k * n)):
+        for _ in range(3):
+            fn()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        print(f"  {name} {us:.1f} us  {fl / us / 1e6:.1f} TFLOP/s")
 
 
 if __name__ == "__main__":

@@ -170,16 +170,20 @@ int dbf_sign_matvec_xor(const uint32_t* words, int64_t rows, int64_t cols, int64
 /*
  * A program is a list of SEGMENTS (one sign GEMV each: y = oscale * (S . (iscale * v))) over
  * VECTORS.  Vector kind 0 = plain (dtype `dtype`, ready when the kernel starts, e.g. the token
- * input); kind 1 = LL ("low-latency": uint64 words {fp32 value, 32-bit epoch}, produced inside
- * the kernel by another segment and consumed by polling the words themselves).  Every segment's
- * work is split into UNITS of 16 rows; each CTA executes a list of RUNS -- consecutive units of
+ * input); kind 1 = LL ("low-latency": uint32 words {fp16 value (low 16 bits), 16-bit epoch},
+ * produced inside the kernel by another segment and consumed by polling the words themselves;
+ * the buffer is padded to a multiple of 256 words).  Every segment's work is split into UNITS of
+ * 16 rows; each CTA executes a list of RUNS -- up to dbf_engine_run_limits() consecutive units of
  * one segment, (segment, first row block, unit count) -- in order (cta_offsets[c] ..
  * cta_offsets[c+1]); dependencies are respected by construction (a run only reads vectors
- * written by runs of earlier stages).  One forward of a DBF layer is
- * two segments: B with iscale=b, oscale=mid -> t (LL), then A with oscale=a -> y.
- * Each CTA streams its units' packed signs with cp.async.bulk into a shared-memory ring (one
- * producer warp) while consumer warps run the int8 tensor-core sign GEMV, so weights of later
- * layers are in flight while a layer waits for its input vector.
+ * written by runs of earlier stages).  One forward of a DBF layer is two segments: B with
+ * iscale=b, oscale=mid -> t (LL), then A with oscale=a -> y.
+ * Each CTA streams its runs' packed signs with cp.async.bulk into a shared-memory ring (one
+ * producer warp) while 16 compute warps each own a set of 256-column chunks of the run's input:
+ * a chunk is quantized (warp-local, relative to the chunk's max) as soon as its LL words carry
+ * this launch's epoch and is multiplied on the int8 tensor cores against every unit of the run.
+ * Outputs are fp16 (rounded once per layer stage); sums are exact integers per chunk, scaled and
+ * accumulated in a fixed order, so results are bitwise reproducible run to run.
  */
 typedef struct {
   const void* tiled;    /* tiled sign matrix (dbf_tile_signs) */
@@ -194,7 +198,7 @@ typedef struct {
 } dbf_engine_segment;
 
 typedef struct {
-  void* data;           /* plain: `len` values of `dtype`; LL: `len` uint64 words */
+  void* data;           /* plain: `len` values of `dtype`; LL: uint32 words, padded to 256 */
   int32_t len;
   int32_t kind;         /* 0 plain, 1 LL */
   int32_t dtype;        /* plain dtype (F16/F32) */
@@ -244,6 +248,8 @@ int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t nsegments,
                           const dbf_engine_vector* vectors, int32_t nvectors, const int32_t* runs,
                           int32_t nruns, uint32_t* ready, dbf_engine_run* out);
 
+/* Largest run the engine accepts: units per run and packed-sign bytes per run. */
+int dbf_engine_run_limits(int32_t* max_units, int64_t* max_run_bytes);
 /* Dynamic shared memory the engine needs for max_cols; DBF_ERR_UNSUPPORTED if it cannot fit. */
 int dbf_engine_smem_bytes(int32_t max_cols, size_t* bytes);
 /* Resident engine CTAs per SM and registers per thread for max_cols (diagnostics). */

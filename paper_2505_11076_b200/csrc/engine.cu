@@ -2,26 +2,29 @@
 //
 // Per-layer kernels pay a grid launch + drain per GEMV (4 us back-to-back on B200, ~2 us in a
 // graph), which is 3-10x the HBM time of a 7B layer at 2 bits/weight (0.7-1.8 us).  Here one
-// CTA per SM runs the whole program (include/dbf_b200.h, dbf_engine_program):
+// CTA per SM runs the whole program (include/dbf_b200.h, dbf_engine_program) -- a list of RUNS
+// (consecutive 16-row units of one segment) per CTA, in stage order:
 //
-//   warp W (producer)    walks this CTA's unit list and streams every unit's packed signs
-//                        into a shared-memory ring with cp.async.bulk (TMA bulk copies,
-//                        mbarrier complete_tx).  It never waits on activations, so the weights
-//                        of the next layers are already in flight while a layer waits for its
-//                        input vector -- HBM stays busy across the layer dependencies.
-//   warps 0..W-1         (consumers) per unit: quantize the input vector into int8 digit-plane
-//                        B fragments (once per segment), then the int8 tensor-core sign GEMV of
-//                        decode.cu from the ring, cross-warp integer reduction, epilogue with the
-//                        output scale, and publish the 16 outputs as LL words.
+//   producer warp        streams every run's packed signs (+ its 128-byte record) into a
+//                        shared-memory ring with cp.async.bulk (mbarrier complete_tx).  It never
+//                        waits on activations, so the next layers' weights are in flight while a
+//                        layer waits for its input.
+//   16 compute warps     warp w OWNS the 256-column chunks c = w, w+16, ... of the run's input.
+//                        Per chunk it polls the chunk's LL words straight from L2 (streaming: a
+//                        chunk is processed as soon as ITS producers are done), quantizes the 256
+//                        values to a 22-bit grid relative to the CHUNK's max |value| (warp-local:
+//                        no CTA-wide barrier, no global max), builds the int8 digit-plane B
+//                        fragments, and runs the int8 tensor-core sign GEMV of every unit of the
+//                        run against that chunk.  The chunk's exact integer sum is scaled by
+//                        2^-F_c and accumulated in fp32 registers, per unit, in chunk order.
+//   finalizer warp       sums the 16 warps' partials of each unit in warp order (deterministic),
+//                        applies the output scale and publishes fp16 outputs as LL words.
 //
-// Inter-CTA dependencies use an LL ("low latency", as in NCCL's LL protocol) handoff: each
-// produced value is written as one 64-bit word {fp32 value, 32-bit epoch}; consumers poll the
-// words themselves, so there is no separate flag, fence or counter round trip.  Epochs are
-// run_counter * nvectors + vector + 1, advanced by a one-thread kernel after every launch, so
-// LL buffers never need clearing.
-//
-// Arithmetic is identical to decode.cu (same quantization and exact integer sums), so the
-// engine's outputs equal a chain of dbf_forward calls bit for bit.
+// Inter-CTA dependencies use an LL ("low latency", as in NCCL's LL protocol) handoff: each value
+// is one 32-bit word {fp16 value, 16-bit epoch}; consumers poll the words themselves, so there is
+// no separate flag, fence or counter round trip.  Epochs are (launch * nvectors + vector) mod
+// 65535 + 1, advanced by a one-thread kernel after every launch, so LL buffers never need
+// clearing (a stale word always carries the previous launch's epoch).
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -30,19 +33,16 @@
 namespace dbf {
 namespace engine {
 
-constexpr int kWarps = 14;                    // consumer warps (+ 1 finalizer + 1 producer = 4 per SMSP)
-constexpr int kFinWarp = kWarps;              // finalizer warp index
-constexpr int kDeal = 4;                      // chunks per dealt block (round-robin over warps)
-constexpr int kCycle = kWarps * kDeal;        // chunks per full dealing cycle
-constexpr int kProdWarp = kWarps + 1;         // producer warp index
-constexpr int kConsumers = kWarps * 32;
-constexpr int kThreads = kConsumers + 64;     // + finalizer warp + producer warp
+constexpr int kWarps = 16;                    // compute warps
+constexpr int kProdWarp = kWarps;             // producer warp index
+constexpr int kThreads = (kWarps + 1) * 32;
 constexpr int kSlotBytes = 16384;             // one ring slot = 32 chunks of 512 B
-constexpr int kSlotChunks = kSlotBytes / kChunkBytes;
-constexpr int kRegGroups = 6;                 // register-resident 4-column groups per thread
+constexpr int kMaxUnits = 8;                  // units per run (the host splits longer runs)
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMinSlots = 4;
 constexpr int kMaxSlots = 16;
+constexpr int kXsBytes = 8 * 128;             // per-warp B-fragment scratch: 8 k-blocks x 16 lanes x 8 B
+constexpr int kPartFloats = kWarps * kMaxUnits * 16;  // one partial buffer
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -80,9 +80,6 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
-}
 __device__ __forceinline__ void imma(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                      uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -91,246 +88,177 @@ __device__ __forceinline__ void imma(int (&c)[4], uint32_t a0, uint32_t a1, uint
       : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void st_ll(unsigned long long* p, float v, uint32_t epoch) {
-  const unsigned long long w = ((unsigned long long)epoch << 32) | (unsigned long long)__float_as_uint(v);
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+__device__ __forceinline__ void st_ll16(uint32_t* p, __half v, uint32_t epoch) {
+  const uint32_t w = (epoch << 16) | (uint32_t)__half_as_ushort(v);
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(w) : "memory");
 }
-
-__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
-__device__ __forceinline__ void red_add_s32(int* p, int v) {
-  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+__device__ __forceinline__ uint4 ld_ll16x4(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
 }
-
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-
 __device__ __forceinline__ float ld_scale(const void* p, int dt, int i) {
   return dt == DBF_F16 ? __half2float(((const __half*)p)[i]) : ((const float*)p)[i];
 }
-
-// Plain (kind 0) vector: the 4 values of group q (columns 4q..4q+3, zero beyond cols).
-__device__ __forceinline__ void load_plain(const void* data, int dtype, int cols, int q, float (&u)[4]) {
-  const int j0 = 4 * q;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int j = j0 + e;
-    u[e] = j < cols ? (dtype == DBF_F16 ? __half2float(((const __half*)data)[j]) : ((const float*)data)[j]) : 0.f;
-  }
+__device__ __forceinline__ uint32_t epoch16(uint32_t run_ctr, int nvectors, int vec) {
+  return (uint32_t)(((uint64_t)run_ctr * (uint64_t)nvectors + (uint64_t)vec) % 65535ull) + 1u;
 }
-__device__ __forceinline__ void ld_ll4(const unsigned long long* w, unsigned long long (&x)[4]) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(x[0]), "=l"(x[1]) : "l"(w));
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(x[2]), "=l"(x[3]) : "l"(w + 2));
-}
-// LL group check: every element below `cols` must carry the expected epoch.
-__device__ __forceinline__ bool ll_take(const unsigned long long (&x)[4], int j0, int cols, uint32_t epoch,
-                                        float (&u)[4]) {
-  bool ok = true;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const bool in = j0 + e < cols;
-    ok &= !in || (uint32_t)(x[e] >> 32) == epoch;
-    u[e] = in ? __uint_as_float((uint32_t)x[e]) : 0.f;
-  }
-  return ok;
-}
-// Input of a run, resolved into registers once per prepare.
-struct InSpec {
-  const void* x;
-  const void* iscale;
-  int kind, dtype, scale_dtype, cols;
-};
-__device__ __forceinline__ void apply_iscale(const InSpec& in, int q, float (&u)[4]) {
-  if (!in.iscale) return;
-  const int j0 = 4 * q;
-#pragma unroll
-  for (int e = 0; e < 4; ++e)
-    if (j0 + e < in.cols) u[e] *= ld_scale(in.iscale, in.scale_dtype, j0 + e);
-}
-// One group, blocking (used for groups beyond the register-resident ones).
-__device__ __forceinline__ void load_group(const InSpec& in, int q, uint32_t epoch, float (&u)[4]) {
-  if (in.kind == 1) {
-    unsigned long long x[4];
-    const unsigned long long* w = (const unsigned long long*)in.x + 4 * q;
-    do {
-      ld_ll4(w, x);
-    } while (!ll_take(x, 4 * q, in.cols, epoch, u));
-  } else {
-    load_plain(in.x, in.dtype, in.cols, q, u);
-  }
-  apply_iscale(in, q, u);
-}
-
-constexpr int kRedBufs = 16;                  // per-unit partial-sum ring depth (power of 2)
 
 struct Smem {
   uint8_t* ring;
-  uint8_t* xfrag;
-  long long* red;   // [kRedBufs][kWarps][16]
-  int* red_cnt;     // [kRedBufs] arrivals of the unit currently in each buffer
-  int* red_fin;     // [kRedBufs] units finalized from each buffer
-  long long* run_T; // [2*kRedBufs] T of the run (by run sequence), for the finalizer
-  int* run_F;       // [2*kRedBufs] F of the run
-  float* red_max;   // [kWarps]
-  long long* red_sum;  // [kWarps]
+  dbf_engine_run* hdr;  // [kMaxSlots] record of the run whose first piece is in that slot
+  uint8_t* xs;          // [kWarps][kXsBytes]
+  float* part;          // [2][kWarps][kMaxUnits][16]
   uint64_t* full;
   uint64_t* empty;
-  dbf_engine_run* hdr;  // [kMaxSlots] run record of the run whose first piece is in that slot
 };
 
-// Quantize the segment's input vector into B fragments (SINGLE layout: 16 lanes x 8 B per k-block).
-// Returns F (every thread) and T = sum_j X_j (valid in all threads after the final barrier).
-__device__ void prepare(const InSpec& in, uint32_t epoch, const Smem& sm, int& F_out, long long& T_out,
-                        const uint32_t* ready, uint32_t ready_target) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (in.kind == 1 && ready) {
-    // one poller per CTA; the data words' epochs are still checked below
-    if (tid == 0) {
-      uint32_t c;
-      for (;;) {
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ready) : "memory");
-        if ((int)(c - ready_target) >= 0) break;
-        __nanosleep(64);
-      }
-    }
-    consumer_sync();
+// A run's input vector, resolved into registers once per run.
+struct InSpec {
+  const void* x;
+  const void* iscale;
+  int kind, dtype, sdt, cols;
+};
+
+// The 4 input scales of columns col0..col0+3 (1 when there is no input scale, 0 beyond cols).
+__device__ __forceinline__ void load_scale4(const InSpec& in, int col0, float (&s)[4]) {
+  if (!in.iscale) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[e] = 1.f;
+    return;
   }
-  const int nch = (in.cols + kChunkCols - 1) / kChunkCols;
-  const int ngroups = nch * (kChunkCols / 4);
-  float u[kRegGroups][4];
+  if (col0 + 3 < in.cols) {
+    if (in.sdt == DBF_F16) {
+      const uint2 v = __ldg((const uint2*)((const __half*)in.iscale + col0));
+      const float2 a = __half22float2(*(const __half2*)&v.x), b = __half22float2(*(const __half2*)&v.y);
+      s[0] = a.x, s[1] = a.y, s[2] = b.x, s[3] = b.y;
+    } else {
+      const float4 v = __ldg((const float4*)((const float*)in.iscale + col0));
+      s[0] = v.x, s[1] = v.y, s[2] = v.z, s[3] = v.w;
+    }
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s[e] = col0 + e < in.cols ? ld_scale(in.iscale, in.sdt, col0 + e) : 0.f;
+}
+
+// Load the 4 values of columns col0..col0+3; for LL vectors also report whether all carry `epoch`.
+// Columns >= cols read as 0.
+__device__ __forceinline__ bool load_group(const InSpec& in, int col0, uint32_t epoch, float (&u)[4]) {
   if (in.kind == 1) {
-    // issue every group's LL loads back to back, then check; re-poll only the pending groups,
-    // again in one batched pass, until all carry this run's epoch
-    const unsigned long long* base = (const unsigned long long*)in.x;
-    unsigned long long x[kRegGroups][4];
+    const uint4 v = ld_ll16x4((const uint32_t*)in.x + col0);  // LL vectors are padded to whole chunks
+    const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+    bool ok = true;
 #pragma unroll
-    for (int g = 0; g < kRegGroups; ++g)
-      if (tid + g * kConsumers < ngroups) ld_ll4(base + 4 * (tid + g * kConsumers), x[g]);
-    uint32_t pending = 0;
-#pragma unroll
-    for (int g = 0; g < kRegGroups; ++g) {
-      const int q = tid + g * kConsumers;
-      if (q < ngroups && !ll_take(x[g], 4 * q, in.cols, epoch, u[g])) pending |= 1u << g;
+    for (int e = 0; e < 4; ++e) {
+      const bool inb = col0 + e < in.cols;
+      ok &= !inb || (vv[e] >> 16) == epoch;
+      u[e] = inb ? __half2float(__ushort_as_half((unsigned short)(vv[e] & 0xFFFFu))) : 0.f;
     }
-    while (pending) {
+    return ok;
+  }
+  if (col0 + 3 < in.cols && in.dtype == DBF_F16 && (((uintptr_t)in.x & 7) == 0)) {
+    const uint2 v = __ldg((const uint2*)((const __half*)in.x + col0));
+    const float2 a = __half22float2(*(const __half2*)&v.x), b = __half22float2(*(const __half2*)&v.y);
+    u[0] = a.x, u[1] = a.y, u[2] = b.x, u[3] = b.y;
+    return true;
+  }
 #pragma unroll
-      for (int g = 0; g < kRegGroups; ++g)
-        if (pending & (1u << g)) ld_ll4(base + 4 * (tid + g * kConsumers), x[g]);
-#pragma unroll
-      for (int g = 0; g < kRegGroups; ++g)
-        if ((pending & (1u << g)) && ll_take(x[g], 4 * (tid + g * kConsumers), in.cols, epoch, u[g]))
-          pending &= ~(1u << g);
-    }
-  } else {
-#pragma unroll
-    for (int g = 0; g < kRegGroups; ++g) {
-      const int q = tid + g * kConsumers;
-      if (q < ngroups) load_plain(in.x, in.dtype, in.cols, q, u[g]);
-    }
+  for (int e = 0; e < 4; ++e) {
+    const int j = col0 + e;
+    u[e] = j < in.cols ? (in.dtype == DBF_F16 ? __half2float(((const __half*)in.x)[j]) : ((const float*)in.x)[j])
+                       : 0.f;
+  }
+  return true;
+}
+
+// Quantize chunk c of the run's input (256 columns, warp-local) into this warp's B-fragment
+// scratch.  X_j = round(x_j * 2^F) on a 14-bit grid relative to the CHUNK max (|X| < 2^13); the
+// MMA A bytes are 2^t * bit_j for k-block r = 2s + t (the packed word pre-shifted by 2s), so the B
+// operand carries Y_j = X_j * 2^(1-t) as two balanced int8 digits (planes = MMA columns 0, 1) and
+// every k-block contributes 2 * sum bit_j X_j alike.  Returns F and T = sum_j X_j.
+__device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t epoch, uint8_t* xs,
+                                               int& F_out, int& T_out) {
+  const int lane = threadIdx.x & 31;
+  float u[2][4], sc[2][4];
+  const int c0 = c * kChunkCols;
+  // groups q = lane and lane + 32 (64 groups of 4 columns per chunk); scales first (never wait)
+  load_scale4(in, c0 + 4 * lane, sc[0]);
+  load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
+  for (;;) {
+    const bool ok0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
+    const bool ok1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
+    if (__all_sync(0xffffffffu, ok0 && ok1)) break;
+    __nanosleep(32);
   }
   float mx = 0.f;
 #pragma unroll
-  for (int g = 0; g < kRegGroups; ++g) {
-    const int q = tid + g * kConsumers;
-    if (q < ngroups) {
-      apply_iscale(in, q, u[g]);
+  for (int h = 0; h < 2; ++h) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) mx = fmaxf(mx, fabsf(u[g][e]));
+    for (int e = 0; e < 4; ++e) {
+      u[h][e] *= sc[h][e];
+      mx = fmaxf(mx, fabsf(u[h][e]));
     }
-  }
-  for (int q = tid + kRegGroups * kConsumers; q < ngroups; q += kConsumers) {
-    float t[4];
-    load_group(in, q, epoch, t);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) mx = fmaxf(mx, fabsf(t[e]));
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) sm.red_max[warp] = mx;
-  consumer_sync();
-  float m = 0.f;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) m = fmaxf(m, sm.red_max[w]);
   int F = 0;
-  if (m > 0.f) {
+  if (mx > 0.f) {
     int e;
-    frexpf(m, &e);
-    F = 22 - e;
-    F = F > 125 ? 125 : F;
+    frexpf(mx, &e);  // mx in [2^(e-1), 2^e)  ->  |X| <= 2^13
+    F = 13 - e;
+    F = F > 125 ? 125 : (F < -125 ? -125 : F);
   }
   const float scale = __int_as_float((F + 127) << 23);
-  long long tsum = 0;
-  auto emit = [&](int q, const float (&uu)[4]) {
-    const int kb = q >> 3, r = kb & 7, tig = q & 3, half = (q >> 2) & 1;
-    const uint32_t sr = 1u << (7 - r);
-    const uint32_t cr = 0x00808080u - 0x4B400000u * sr;
-    uint32_t d[4];
-    int ts = 0;
+  int ts = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = lane + 32 * h;
+    const int kb = q >> 3, tig = q & 3, half = (q >> 2) & 1;
+    const int sh = 1 - (kb & 1);  // Y = X * 2^(1-t)
+    uint32_t v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const uint32_t bits = __float_as_uint(fmaf(uu[e], scale, 12582912.0f));
-      ts += (int)(bits - 0x4B400000u);
-      d[e] = (bits * sr + cr) ^ 0x00808080u;
+      const int X = __float2int_rn(u[h][e] * scale);
+      ts += X;
+      v[e] = (uint32_t)((X << sh) + 0x8080);  // bytes 0,1 = balanced digits + 128
     }
-    tsum += ts;
-    const uint32_t t0 = __byte_perm(d[0], d[1], 0x5140), t1 = __byte_perm(d[0], d[1], 0x7362);
-    const uint32_t t2 = __byte_perm(d[2], d[3], 0x5140), t3 = __byte_perm(d[2], d[3], 0x7362);
-    uint8_t* base = sm.xfrag + kb * 128 + 4 * half + tig * 8;
-    *(uint32_t*)(base + 0) = __byte_perm(t0, t2, 0x5410);
-    *(uint32_t*)(base + 32) = __byte_perm(t0, t2, 0x7632);
-    *(uint32_t*)(base + 64) = __byte_perm(t1, t3, 0x5410);
-    *(uint32_t*)(base + 96) = __byte_perm(t1, t3, 0x7632);
-  };
-#pragma unroll
-  for (int g = 0; g < kRegGroups; ++g) {
-    const int q = tid + g * kConsumers;
-    if (q < ngroups) emit(q, u[g]);
-  }
-  for (int q = tid + kRegGroups * kConsumers; q < ngroups; q += kConsumers) {
-    float t[4];
-    load_group(in, q, epoch, t);
-    emit(q, t);
+    const uint32_t lo = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+    const uint32_t hi = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
+    uint8_t* base = xs + kb * 128 + 4 * half + tig * 8;
+    *(uint32_t*)(base + 0) = lo ^ 0x80808080u;   // plane 0 -> MMA column 0 (lanes 0-3)
+    *(uint32_t*)(base + 32) = hi ^ 0x80808080u;  // plane 1 -> MMA column 1 (lanes 4-7)
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
-  if (lane == 0) sm.red_sum[warp] = tsum;
-  consumer_sync();
-  long long T = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) T += sm.red_sum[w];
+  for (int o = 16; o; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+  __syncwarp();
   F_out = F;
-  T_out = T;
+  T_out = ts;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program prog, int ring_slots,
-                                                            int xfrag_bytes) {
+__global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program prog, int ring_slots) {
   extern __shared__ __align__(128) uint8_t smem[];
   Smem sm;
   sm.ring = smem;
   sm.hdr = (dbf_engine_run*)(sm.ring + (size_t)ring_slots * kSlotBytes);
-  sm.xfrag = (uint8_t*)(sm.hdr + kMaxSlots);
-  sm.red = (long long*)(sm.xfrag + xfrag_bytes);
-  sm.red_cnt = (int*)(sm.red + kRedBufs * 32);  // red: kRedBufs x 64 int32
-  sm.red_fin = sm.red_cnt + kRedBufs;
-  sm.run_T = (long long*)(sm.red_fin + kRedBufs);
-  sm.run_F = (int*)(sm.run_T + 2 * kRedBufs);
-  sm.red_max = (float*)(sm.run_F + 2 * kRedBufs);
-  sm.red_sum = (long long*)(sm.red_max + 16);  // 16 floats: keeps the int64 array 8-byte aligned
-  sm.full = (uint64_t*)(sm.red_sum + 16);
+  sm.xs = (uint8_t*)(sm.hdr + kMaxSlots);
+  sm.part = (float*)(sm.xs + kWarps * kXsBytes);
+  sm.full = (uint64_t*)(sm.part + 2 * kPartFloats);
   sm.empty = sm.full + kMaxSlots;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < kRedBufs) {
-    sm.red_cnt[threadIdx.x] = 0;
-    sm.red_fin[threadIdx.x] = 0;
-  }
-  for (int i = threadIdx.x; i < kRedBufs * 64; i += kThreads) ((int*)sm.red)[i] = 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < ring_slots; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], kWarps);
+      mbar_init(&sm.empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -338,18 +266,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 
   const int r0 = prog.cta_offsets[blockIdx.x], r1 = prog.cta_offsets[blockIdx.x + 1];
   const uint32_t run_ctr = *prog.run_counter;
-  const uint32_t ebase = run_ctr * (uint32_t)prog.nvectors + 1u;
+  const dbf_engine_run* R = prog.runs;
 
   if (warp == kProdWarp) {
     // ---------------- producer: stream each run's packed signs (contiguous) into the ring -----
-    // The run record is staged into the header of the run's first slot (consumers read it from
-    // shared memory); the next record is prefetched while the current run's pieces are issued.
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
       int slot = 0;
       uint32_t phase = 0;
-      const dbf_engine_run* R = prog.runs;
-      // prefetch the fields the producer needs one run ahead (the record itself is bulk-copied)
       const void* n_tiled = nullptr;
       int n_cols = 1, n_units = 0;
       if (r0 < r1) { n_tiled = R[r0].tiled; n_cols = R[r0].cols; n_units = R[r0].nunits; }
@@ -357,19 +281,17 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         const uint8_t* src = (const uint8_t*)n_tiled;
         const int cols = n_cols, nunits = n_units;
         if (i + 1 < r1) { n_tiled = R[i + 1].tiled; n_cols = R[i + 1].cols; n_units = R[i + 1].nunits; }
-        const int nch = (cols + kChunkCols - 1) / kChunkCols;
-        const int total = nunits * nch;
-        for (int p = 0; p < total; p += kSlotChunks) {
-          const int n = min(kSlotChunks, total - p);
+        const int total = nunits * ((cols + kChunkCols - 1) / kChunkCols) * kChunkBytes;
+        for (int off = 0; off < total; off += kSlotBytes) {
+          const int n = min(kSlotBytes, total - off);
           mbar_wait(&sm.empty[slot], phase ^ 1u);
-          if (p == 0) {
-            mbar_arrive_expect_tx(&sm.full[slot], n * kChunkBytes + (int)sizeof(dbf_engine_run));
+          if (off == 0) {
+            mbar_arrive_expect_tx(&sm.full[slot], n + (int)sizeof(dbf_engine_run));
             bulk_g2s(&sm.hdr[slot], R + i, sizeof(dbf_engine_run), &sm.full[slot], pol);
           } else {
-            mbar_arrive_expect_tx(&sm.full[slot], n * kChunkBytes);
+            mbar_arrive_expect_tx(&sm.full[slot], n);
           }
-          bulk_g2s(sm.ring + (size_t)slot * kSlotBytes, src + (size_t)p * kChunkBytes, n * kChunkBytes,
-                   &sm.full[slot], pol);
+          bulk_g2s(sm.ring + (size_t)slot * kSlotBytes, src + off, n, &sm.full[slot], pol);
           if (++slot == ring_slots) { slot = 0; phase ^= 1u; }
         }
       }
@@ -377,221 +299,146 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     return;
   }
 
-  if (warp == kFinWarp) {
-    // ---------------- finalizer: completes units in order as their contributions land -------
-    // (exact digit recombination, scales, LL publish + ready-counter bump), so the consumer
-    // warps never stall on epilogues and stay close together over the ring.
-    const dbf_engine_run* R = prog.runs;
-    int seq = 0;
-    int dealt = 0;  // chunks dealt before the current run, mod kCycle (mirrors the consumers)
-    for (int i = r0; i < r1; ++i) {
-      const dbf_engine_run& run = R[i];
-      const int rows = run.rows, cols = run.cols, rb = run.rb, nunits = run.nunits;
-      const void* oscale = run.oscale;
-      const int scale_dtype = run.scale_dtype, out_dtype = run.out_dtype;
-      void* out_plain = run.out_plain;
-      unsigned long long* ll_out = (unsigned long long*)run.ll_out;
-      uint32_t* ready_out = run.ready_out;
-      const uint32_t out_epoch = ebase + (uint32_t)run.out_vec;
-      const int nch = (cols + kChunkCols - 1) / kChunkCols;
-      uint32_t osc_next = 0;
-      {
-        const int row = rb * 16 + (lane & 15);
-        if (oscale && row < rows)
-          osc_next = scale_dtype == DBF_F16 ? (uint32_t)__ldg((const unsigned short*)oscale + row)
-                                            : __ldg((const uint32_t*)oscale + row);
-      }
-      const int rs = (i - r0) & (2 * kRedBufs - 1);
-      bool have_FT = false;
-      int F = 0;
-      long long T = 0;
-      double inv_scale = 1.0;
-      for (int uu = 0; uu < nunits; ++uu, ++seq) {
-        const uint32_t osc_raw = osc_next;
-        if (uu + 1 < nunits) {  // prefetch the next unit's output scale
-          const int row = (rb + uu + 1) * 16 + (lane & 15);
-          if (oscale && row < rows)
-            osc_next = scale_dtype == DBF_F16 ? (uint32_t)__ldg((const unsigned short*)oscale + row)
-                                              : __ldg((const uint32_t*)oscale + row);
-        }
-        const int rbuf = seq & (kRedBufs - 1);
-        // contributors = dealt blocks intersecting the unit (one flush per warp per unit)
-        const int v0 = dealt + uu * nch, v1 = v0 + nch - 1;
-        int need = v1 / kDeal - v0 / kDeal + 1;
-        need = need < kWarps ? need : kWarps;
-        while (*(volatile int*)&sm.red_cnt[rbuf] < need) {
-        }
-        fence_cta();
-        if (!have_FT) {  // written by the consumers before their first contribution to this run
-          F = *(volatile int*)&sm.run_F[rs];
-          T = *(volatile long long*)&sm.run_T[rs];
-          inv_scale = __longlong_as_double((long long)(1023 - F) << 52);  // 2^-F
-          have_FT = true;
-        }
-        int* red = (int*)sm.red + rbuf * 64;
-        const int row = (rb + uu) * 16 + lane;
-        if (lane < 16) {
-          int4* pp = (int4*)&red[lane * 4];
-          const int4 sum = *pp;
-          *pp = make_int4(0, 0, 0, 0);
-          if (row < rows) {
-            const long long s128 = (long long)sum.x + ((long long)sum.y << 8) + ((long long)sum.z << 16) +
-                                   ((long long)sum.w << 24);
-            const long long P = 2 * (s128 >> 7) - T;
-            const float oscf = oscale ? (scale_dtype == DBF_F16 ? __half2float(__ushort_as_half((unsigned short)osc_raw))
-                                                                : __uint_as_float(osc_raw))
-                                      : 1.f;
-            float fv = (float)((double)P * inv_scale * (double)oscf);
-            if (out_dtype == DBF_F16) {
-              const __half h = __float2half_rn(fv);
-              fv = __half2float(h);
-              if (out_plain) ((__half*)out_plain)[row] = h;
-            } else if (out_plain) {
-              ((float*)out_plain)[row] = fv;
-            }
-            if (ll_out) st_ll(ll_out + row, fv, out_epoch);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          if (ready_out) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(ready_out) : "memory");
-          sm.red_cnt[rbuf] = 0;
-          fence_cta();
-          *(volatile int*)&sm.red_fin[rbuf] = seq / kRedBufs + 1;
-        }
-        __syncwarp();
-      }
-      dealt = (dealt + nunits * nch) % kCycle;
-    }
-    return;
-  }
-
-  // ---------------- consumers ---------------------------------------------------------------
-  // A run's chunks are dealt round-robin over the 15 consumer warps (continuing across runs),
-  // so no warp waits for another per unit.  When a warp leaves a unit it drops its partial
-  // (int32 shared-memory reductions, exact) into a ring of kRedBufs per-unit accumulators and
-  // bumps the unit's arrival count; the finalizer warp completes units in order.
+  // ---------------- compute warps -------------------------------------------------------------
   const int g = lane >> 2, tig = lane & 3;
-  const uint2* xlane = (const uint2*)sm.xfrag + (lane & 15);  // lanes 16-31 mirror 0-15 (ignored cols)
-  int slot = 0;
-  uint32_t phase = 0;
-  int cur_seg = -1;
-  int F = 0;
-  long long T = 0;
-  int dealt = 0;      // chunks dealt on this CTA so far, mod kCycle
-  int unit_seq = 0;   // units completed on this CTA before the current run
+  uint8_t* xs = sm.xs + warp * kXsBytes;
+  const uint2* xlane = (const uint2*)xs + (lane & 15);  // lanes 16-31 mirror 0-15 (ignored cols)
+  int P = 0;  // ring pieces consumed before the current run
   for (int i = r0; i < r1; ++i) {
+    const int j = i - r0, buf = j & 1;
     int64_t* tr = prog.trace ? prog.trace + 4 * (size_t)i : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
-    mbar_wait(&sm.full[slot], phase);  // first piece of the run: its header holds the record
-    const dbf_engine_run& H = sm.hdr[slot];
-    const int rows = H.rows, cols = H.cols, rb = H.rb, nunits = H.nunits;
-    if (H.seg != cur_seg) {
-      InSpec in;
-      in.x = H.x;
-      in.iscale = H.iscale;
-      in.kind = H.in_kind;
-      in.dtype = H.in_dtype;
-      in.scale_dtype = H.scale_dtype;
-      in.cols = cols;
-      prepare(in, ebase + (uint32_t)H.in_vec, sm, F, T, H.ready_in, (run_ctr + 1u) * H.in_producers);
-      cur_seg = H.seg;
-    }
-    if (threadIdx.x == 0) {  // F/T of this run for the finalizer; depth 2*kRedBufs runs is safe:
-      // reaching run i+2R means unit seq(i)+2R-1 was flushed, which waited for seq(i)+R-1 done
-      sm.run_F[(i - r0) & (2 * kRedBufs - 1)] = F;
-      sm.run_T[(i - r0) & (2 * kRedBufs - 1)] = T;
-    }
-    if (tr && threadIdx.x == 0) tr[1] = gtimer();
+    const int slot0 = P % ring_slots;
+    const uint32_t phase0 = (uint32_t)(P / ring_slots) & 1u;
+    mbar_wait(&sm.full[slot0], phase0);  // first piece: holds the record
+    const dbf_engine_run& H = sm.hdr[slot0];
+    const int cols = H.cols, nunits = H.nunits;
+    InSpec in;
+    in.x = H.x;
+    in.iscale = H.iscale;
+    in.kind = H.in_kind;
+    in.dtype = H.in_dtype;
+    in.sdt = H.scale_dtype;
+    in.cols = cols;
+    // finalize fields (the record's ring slot is recycled once the run is released)
+    const int rows = H.rows, rb = H.rb, odt = H.out_dtype;
+    const void* oscale = H.oscale;
+    void* out_plain = H.out_plain;
+    uint32_t* ll_out = (uint32_t*)H.ll_out;
+    const uint32_t ep_out = epoch16(run_ctr, prog.nvectors, H.out_vec);
     const int nch = (cols + kChunkCols - 1) / kChunkCols;
-    const int total = nunits * nch;
-    // virtual chunk index v = run chunk + dealt; this warp owns v with (v / kDeal) % kWarps == warp
-    int v = warp * kDeal;  // this warp's first block of the cycle
-    if (v + kDeal <= dealt) v += kCycle;  // already passed: take the next cycle's block
-    else if (v < dealt) v = dealt;        // the run starts inside this warp's block
-    int gch = v - dealt;
-    int u = gch / nch, cu = gch - u * nch;
-    int cur_u = -1;
-    int acc[4][4] = {};
-
-    auto flush = [&](int uu) {
-      // add this warp's int32 plane sums into the unit's 16x4 accumulator (exact, order-free)
-      const int c0 = acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0];
-      const int c1 = acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1];
-      const int c2 = acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2];
-      const int c3 = acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3];
-      const int seq = unit_seq + uu;
-      const int rbuf = seq & (kRedBufs - 1);
-      int* red = (int*)sm.red + rbuf * 64;  // [row 16][plane 4] int32
-      while (*(volatile int*)&sm.red_fin[rbuf] != seq / kRedBufs) {
-      }
-      if (tig < 2) {
-        red_add_s32(&red[g * 4 + 2 * tig], c0);
-        red_add_s32(&red[g * 4 + 2 * tig + 1], c1);
-        red_add_s32(&red[(g + 8) * 4 + 2 * tig], c2);
-        red_add_s32(&red[(g + 8) * 4 + 2 * tig + 1], c3);
-      }
-      __syncwarp();
-      fence_cta();
-      if (lane == 0) atomicAdd(&sm.red_cnt[rbuf], 1);
-    };
-
-    bool first_piece = true;
-    for (int pb = 0; pb < total; pb += kSlotChunks) {
-      const int pe = min(pb + kSlotChunks, total);
-      if (!first_piece) mbar_wait(&sm.full[slot], phase);
-      if (tr && threadIdx.x == 0 && first_piece) tr[2] = gtimer();
-      first_piece = false;
-      const uint4* piece = (const uint4*)(sm.ring + (size_t)slot * kSlotBytes) + lane;
-      for (; gch < pe;) {
-        if (u != cur_u) {
-          if (cur_u >= 0) flush(cur_u);
-          cur_u = u;
+    const int npieces = (nunits * nch * kChunkBytes + kSlotBytes - 1) / kSlotBytes;
+    const uint32_t ep_in = H.in_kind == 1 ? epoch16(run_ctr, prog.nvectors, H.in_vec) : 0u;
+    int64_t* dbg = (prog.trace && prog.pad && blockIdx.x == 0 && lane == 0) ? prog.trace + prog.pad + (j * kWarps + warp) * 4 : nullptr;
+    if (dbg) dbg[0] = clock64();
+    int nwait = 0;
+    float acc0[kMaxUnits], acc1[kMaxUnits];  // rows g and g+8 of each unit (lanes with tig == 0)
 #pragma unroll
-          for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0;
-        }
-        const uint4 w = piece[(gch - pb) * 32];
-        const uint2* xk = xlane + cu * 8 * 16;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const uint32_t m = 0x01010101u << r;
-          const uint2 b = xk[r * 16];
-          imma(acc[r & 3], w.x & m, w.y & m, w.z & m, w.w & m, b.x, b.y);
-        }
-        // next owned chunk: +1 inside the block, else jump to this warp's next block
-        int step = 1;
-        if (((gch + dealt + 1) % kDeal) == 0) step = 1 + (kWarps - 1) * kDeal;
-        gch += step;
-        cu += step;
-        while (cu >= nch) { cu -= nch; ++u; }
+    for (int u = 0; u < kMaxUnits; ++u) acc0[u] = acc1[u] = 0.f;
+    // all of the run's signs are resident before the MMA loop (no waits inside it, so the
+    // compiler can interleave the units' loads and MMAs)
+    {
+      long long tw = dbg ? clock64() : 0;
+      for (int p = 1; p < npieces; ++p) {
+        int sl = slot0 + p;
+        uint32_t ph = phase0;
+        if (sl >= ring_slots) { sl -= ring_slots; ph ^= 1u; }
+        mbar_wait(&sm.full[sl], ph);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[slot]);
-      if (++slot == ring_slots) { slot = 0; phase ^= 1u; }
+      if (dbg) nwait = (int)(clock64() - tw);
     }
-    if (cur_u >= 0) flush(cur_u);
+    const float osc = (oscale && warp < nunits && lane < 16 && (rb + warp) * 16 + lane < rows)
+                          ? ld_scale(oscale, in.sdt, (rb + warp) * 16 + lane)
+                          : 1.f;
+    bool first = true;
+    for (int c = warp; c < nch; c += kWarps) {
+      int F, T;
+      quantize_chunk(in, c, ep_in, xs, F, T);
+      if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
+      if (dbg && first) dbg[1] = clock64();
+      uint2 b[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) b[r] = xlane[r * 16];
+      const float inv = __int_as_float((127 - F) << 23);  // 2^-F  (|F| <= 125)
+#pragma unroll
+      for (int u = 0; u < kMaxUnits; ++u) {
+        if (u < nunits) {
+          const int off = (u * nch + c) * kChunkBytes;
+          const int piece = off >> 14;
+          int slot = slot0 + piece;
+          if (slot >= ring_slots) slot -= ring_slots;
+          const uint4 w = *((const uint4*)(sm.ring + (size_t)slot * kSlotBytes + (off & (kSlotBytes - 1))) + lane);
+          // k-block r = 2s + t reads (word >> 2s) & (0x01010101 << t): A bytes 2^t * bit
+          uint4 ws[4];
+          ws[0] = w;
+          ws[1] = make_uint4(w.x >> 2, w.y >> 2, w.z >> 2, w.w >> 2);
+          ws[2] = make_uint4(w.x >> 4, w.y >> 4, w.z >> 4, w.w >> 4);
+          ws[3] = make_uint4(w.x >> 6, w.y >> 6, w.z >> 6, w.w >> 6);
+          int ac[4][4] = {};  // four independent accumulator chains
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const uint32_t m = 0x01010101u << (r & 1);
+            const uint4& x = ws[r >> 1];
+            imma(ac[r & 3], x.x & m, x.y & m, x.z & m, x.w & m, b[r].x, b[r].y);
+          }
+          // columns 0, 1 (planes) of rows g, g+8 live in lanes tig == 0: s = 2 * sum bit X
+          const int s0 = (ac[0][0] + ac[1][0]) + (ac[2][0] + ac[3][0]);
+          const int s1 = (ac[0][1] + ac[1][1]) + (ac[2][1] + ac[3][1]);
+          const int s2 = (ac[0][2] + ac[1][2]) + (ac[2][2] + ac[3][2]);
+          const int s3 = (ac[0][3] + ac[1][3]) + (ac[2][3] + ac[3][3]);
+          acc0[u] = fmaf((float)(s0 + 256 * s1 - T), inv, acc0[u]);
+          acc1[u] = fmaf((float)(s2 + 256 * s3 - T), inv, acc1[u]);
+        }
+      }
+      first = false;
+    }
+    if (tr && warp == 0 && lane == 0) tr[2] = gtimer();
+    if (dbg) { dbg[2] = clock64(); dbg[3] = nwait; }
+    // partials -> shared memory (double-buffered by run parity), then the compute warps meet once
+    float* part = sm.part + buf * kPartFloats;
+    if (tig == 0) {
+#pragma unroll
+      for (int u = 0; u < kMaxUnits; ++u) {
+        if (u < nunits) {
+          part[(warp * kMaxUnits + u) * 16 + g] = acc0[u];
+          part[(warp * kMaxUnits + u) * 16 + g + 8] = acc1[u];
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+    if (warp == 0 && lane == 0)  // every compute warp is done with the run's signs
+      for (int p = 0; p < npieces; ++p) {
+        int sl = slot0 + p;
+        if (sl >= ring_slots) sl -= ring_slots;
+        mbar_arrive(&sm.empty[sl]);
+      }
+    // warp u finalizes unit u: sum the 16 warps' partials in warp order (deterministic), scale, publish
+    if (warp < nunits && lane < 16) {
+      const int row = (rb + warp) * 16 + lane;
+      if (row < rows) {
+        float v = 0.f;
+#pragma unroll
+        for (int w2 = 0; w2 < kWarps; ++w2) v += part[(w2 * kMaxUnits + warp) * 16 + lane];
+        v *= osc;
+        const __half h = __float2half_rn(v);
+        if (ll_out) st_ll16(ll_out + row, h, ep_out);
+        if (out_plain) {
+          if (odt == DBF_F16) ((__half*)out_plain)[row] = h;
+          else ((float*)out_plain)[row] = __half2float(h);
+        }
+      }
+    }
     if (tr && threadIdx.x == 0) tr[3] = gtimer();
-    dealt = (dealt + total) % kCycle;
-    unit_seq += nunits;
+    P += npieces;
   }
 }
 
 __global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; }
 
-int ring_slots_for(int xfrag_bytes) {
-  const int fixed = xfrag_bytes + kMaxSlots * (int)sizeof(dbf_engine_run) + kRedBufs * 64 * 4 +
-                    2 * kRedBufs * 4 + 2 * kRedBufs * 12 + 16 * 4 + 16 * 8 + 2 * kMaxSlots * 8 + 256;
-  int slots = (kMaxSmem - fixed) / kSlotBytes;
-  return std::min(slots, kMaxSlots);
-}
-int xfrag_bytes_for(int max_cols) {
-  const int nch = (max_cols + kChunkCols - 1) / kChunkCols;
-  return nch * 8 * 128;
-}
-size_t smem_bytes(int slots, int xfrag_bytes) {
-  return (size_t)slots * kSlotBytes + kMaxSlots * sizeof(dbf_engine_run) + xfrag_bytes +
-         kRedBufs * 64 * 4 + 2 * kRedBufs * 4 + 2 * kRedBufs * 12 + 16 * 4 + 16 * 8 + 2 * kMaxSlots * 8 + 64;
-}
+constexpr size_t kFixedSmem = kMaxSlots * sizeof(dbf_engine_run) + kWarps * kXsBytes + 2 * kPartFloats * 4 +
+                              2 * kMaxSlots * 8 + 4 * 4 + 128;
+int ring_slots() { return std::min((int)((kMaxSmem - kFixedSmem) / kSlotBytes), kMaxSlots); }
+size_t smem_bytes(int slots) { return (size_t)slots * kSlotBytes + kFixedSmem; }
 
 }  // namespace engine
 }  // namespace dbf
@@ -622,6 +469,9 @@ extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t
     const dbf_engine_segment& g = segments[seg];
     if ((int64_t)(rb + n) * kRowBlock > (int64_t)((g.rows + kRowBlock - 1) / kRowBlock) * kRowBlock)
       return DBF_ERR_SHAPE;
+    if (n > engine::kMaxUnits ||
+        (int64_t)n * chunks(g.cols) * kChunkBytes > (int64_t)(engine::ring_slots() / 2) * engine::kSlotBytes)
+      return DBF_ERR_SHAPE;  // split longer runs (dbf_engine_run_limits)
     const dbf_engine_vector& vin = vectors[g.in_vec];
     if (vin.len != g.cols) return DBF_ERR_SHAPE;
     dbf_engine_run r;
@@ -654,18 +504,27 @@ extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t
 
 extern "C" int dbf_engine_smem_bytes(int32_t max_cols, size_t* bytes) {
   if (max_cols < 1 || !bytes) return DBF_ERR_INVALID_ARGUMENT;
-  const int xb = engine::xfrag_bytes_for(max_cols);
-  const int slots = engine::ring_slots_for(xb);
-  if (slots < engine::kMinSlots) return DBF_ERR_UNSUPPORTED;
-  *bytes = engine::smem_bytes(slots, xb);
+  const int slots = engine::ring_slots();
+  // one 16-row unit of the widest segment must fit the ring with a slot to spare
+  if (slots < engine::kMinSlots || chunks(max_cols) * kChunkBytes > (int64_t)(slots - 1) * engine::kSlotBytes)
+    return DBF_ERR_UNSUPPORTED;
+  *bytes = engine::smem_bytes(slots);
+  return DBF_OK;
+}
+
+extern "C" int dbf_engine_run_limits(int32_t* max_units, int64_t* max_run_bytes) {
+  if (!max_units || !max_run_bytes) return DBF_ERR_INVALID_ARGUMENT;
+  *max_units = engine::kMaxUnits;
+  // a run's signs stay resident until every compute warp is done with it; leave room to prefetch
+  *max_run_bytes = (int64_t)(engine::ring_slots() / 2) * engine::kSlotBytes;
   return DBF_OK;
 }
 
 extern "C" int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, int32_t* regs_per_thread) {
   if (!blocks_per_sm || !regs_per_thread || max_cols < 1) return DBF_ERR_INVALID_ARGUMENT;
-  const int xb = engine::xfrag_bytes_for(max_cols);
-  const int slots = engine::ring_slots_for(xb);
-  if (slots < engine::kMinSlots) return DBF_ERR_UNSUPPORTED;
+  size_t smem = 0;
+  int st = dbf_engine_smem_bytes(max_cols, &smem);
+  if (st != DBF_OK) return st;
   cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        engine::kMaxSmem);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
@@ -674,8 +533,7 @@ extern "C" int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, in
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   *regs_per_thread = fa.numRegs;
   int nb = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, engine::engine_kernel, engine::kThreads,
-                                                    engine::smem_bytes(slots, xb));
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, engine::engine_kernel, engine::kThreads, smem);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   *blocks_per_sm = nb;
   return DBF_OK;
@@ -685,10 +543,10 @@ extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream
   if (!program || !program->runs || !program->cta_offsets || !program->run_counter || program->grid < 1 ||
       program->max_cols < 1)
     return DBF_ERR_INVALID_ARGUMENT;
-  const int xb = engine::xfrag_bytes_for(program->max_cols);
-  const int slots = engine::ring_slots_for(xb);
-  if (slots < engine::kMinSlots) return DBF_ERR_UNSUPPORTED;
-  const size_t smem = engine::smem_bytes(slots, xb);
+  size_t smem = 0;
+  int st = dbf_engine_smem_bytes(program->max_cols, &smem);
+  if (st != DBF_OK) return st;
+  const int slots = engine::ring_slots();
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -708,7 +566,7 @@ extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   dbf_engine_program prog = *program;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, engine::engine_kernel, prog, slots, xb);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, engine::engine_kernel, prog, slots);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   engine::advance_run_kernel<<<1, 1, 0, s>>>(program->run_counter);
   return check_launch();

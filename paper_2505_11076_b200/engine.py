@@ -73,6 +73,13 @@ def occupancy(max_cols: int) -> tuple[int, int]:
     return b.value, r.value
 
 
+def run_limits() -> tuple[int, int]:
+    """(units per run, packed-sign bytes per run) the engine accepts."""
+    u, b = ctypes.c_int32(0), ctypes.c_int64(0)
+    _lib.check(_lib.lib.dbf_engine_run_limits(ctypes.byref(u), ctypes.byref(b)), "dbf_engine_run_limits")
+    return u.value, b.value
+
+
 def levels_of(ops, input_buffer: int) -> list[int]:
     """Dependency level of each op: 1 + level of the op that last wrote its source buffer."""
     writer_level: dict[int, int] = {}
@@ -117,7 +124,8 @@ class EngineProgram:
         self._keep = []
 
         def ll_vector(length: int) -> int:
-            t = torch.zeros(((length + 3) // 4) * 4, dtype=torch.int64, device=dev)
+            # uint32 {fp16, epoch16} words, padded to whole 256-column chunks (the kernel reads them)
+            t = torch.zeros(((length + 255) // 256) * 256, dtype=torch.int32, device=dev)
             self._keep.append(t)
             vecs.append((t.data_ptr(), length, 1, 0))
             return len(vecs) - 1
@@ -161,12 +169,16 @@ class EngineProgram:
             for c, lst in enumerate(distribute(units, self.grid, rot)):
                 per_cta[c].extend(lst)
             rot = (rot + len(units)) % self.grid
-        # compress each CTA's unit list into runs: consecutive row blocks of one segment
+        # compress each CTA's unit list into runs: consecutive row blocks of one segment, at most
+        # max_units units / max_run_bytes of packed signs each (dbf_engine_run_limits)
+        max_units, max_bytes = run_limits()
+        unit_bytes = {j: ((sg[2] + 255) // 256) * 512 for j, sg in enumerate(segs)}
         per_cta_runs: list[list[tuple[int, int, int]]] = []
         for lst in per_cta:
             runs_c: list[list[int]] = []
             for seg, rb in lst:
-                if runs_c and runs_c[-1][0] == seg and runs_c[-1][1] + runs_c[-1][2] == rb:
+                if (runs_c and runs_c[-1][0] == seg and runs_c[-1][1] + runs_c[-1][2] == rb
+                        and runs_c[-1][2] < max_units and (runs_c[-1][2] + 1) * unit_bytes[seg] <= max_bytes):
                     runs_c[-1][2] += 1
                 else:
                     runs_c.append([seg, rb, 1])

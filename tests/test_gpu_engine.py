@@ -1,5 +1,7 @@
-"""Decode engine (one persistent kernel per step) == the per-layer kernel chain, bit for bit,
-and == the oracle within the fp16 tolerance."""
+"""Decode engine (one persistent kernel per step): parity with the per-layer kernel chain and the
+oracle within the fp16 tolerance, and bitwise determinism -- across replays, graph capture and
+grid sizes (every unit's sum is exact per chunk and combined in a fixed order, independent of
+how units are spread over CTAs)."""
 
 import numpy as np
 import pytest
@@ -11,6 +13,8 @@ from paper_2505_11076_b200.plan import llama_decode_plan  # noqa: E402
 import oracle  # noqa: E402
 from conftest import rel_max, rel_norm  # noqa: E402
 
+TOL = 1e-2  # fp16 activations: max|err|/max|ref| and ||err||/||ref||
+
 
 def _run(plan, x):
     import torch
@@ -21,8 +25,13 @@ def _run(plan, x):
     return plan.buffers[plan.output_buffer].clone()
 
 
-@pytest.mark.parametrize("blocks,grid", [(1, 148), (2, 148), (1, 7), (3, 64)])
-def test_engine_equals_layer_chain(blocks, grid):
+def _close(out, ref):
+    o, r = out.double().cpu().numpy(), ref.double().cpu().numpy()
+    return rel_max(o, r) <= TOL and rel_norm(o, r) <= TOL, (rel_max(o, r), rel_norm(o, r))
+
+
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_engine_matches_layer_chain_and_is_grid_independent(blocks):
     import torch
 
     g = torch.Generator(device="cuda")
@@ -30,40 +39,42 @@ def test_engine_equals_layer_chain(blocks, grid):
     plan = llama_decode_plan("llama2-7b", bpw=2.0, blocks=blocks, generator=g)
     x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
     ref = _run(plan.use_layer_kernels(), x)
-    out = _run(plan.use_engine(grid=grid), x)
-    assert torch.equal(out, ref)
-    # replays reuse LL buffers through the epoch counter
+    out = _run(plan.use_engine(grid=148), x)
+    ok, err = _close(out, ref)
+    assert ok, err
+    for grid in (7, 64):
+        assert torch.equal(_run(plan.use_engine(grid=grid), x), out)
+    # replays reuse the LL buffers through the epoch counter
+    plan.use_engine(grid=148)
     for _ in range(3):
-        assert torch.equal(_run(plan, x), ref)
+        assert torch.equal(_run(plan, x), out)
 
 
-def test_engine_graph_replay_and_intermediate_parity():
+def test_engine_graph_replay_is_deterministic():
     import torch
 
     g = torch.Generator(device="cuda")
     g.manual_seed(5)
     plan = llama_decode_plan("llama2-7b", bpw=1.0, blocks=2, generator=g).use_engine()
     x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
-    plan.buffers[plan.input_buffer].copy_(x)
+    eager = _run(plan, x)
     plan.capture()
-    outs = []
     for _ in range(3):
         plan.buffers[plan.input_buffer].copy_(x)
         plan.replay()
         torch.cuda.synchronize()
-        outs.append(plan.buffers[plan.output_buffer].clone())
-    ref = _run(plan.use_layer_kernels(), x)
-    for o in outs:
-        assert torch.equal(o, ref)
+        assert torch.equal(plan.buffers[plan.output_buffer], eager)
+    ok, err = _close(eager, _run(plan.use_layer_kernels(), x))
+    assert ok, err
 
 
-def test_engine_single_layer_vs_oracle():
+@pytest.mark.parametrize("n,k,m", [(11008, 5952, 4096), (4096, 5952, 11008), (1000, 300, 777)])
+def test_engine_single_layer_vs_oracle(n, k, m):
     import torch
     from paper_2505_11076_b200.plan import DecodePlan, PlanOp
 
     g = torch.Generator(device="cuda")
     g.manual_seed(3)
-    n, k, m = 11008, 5952, 4096
     layer = P.random_device_layer(n, k, m, generator=g, keep_words=True)
     bufs = [torch.randn((1, m), generator=g, device="cuda").half(), torch.zeros((1, n), device="cuda").half()]
     plan = DecodePlan([layer], [PlanOp(0, 0, 1, "gate")], bufs, input_buffer=0, output_buffer=1).use_engine()
@@ -71,4 +82,4 @@ def test_engine_single_layer_vs_oracle():
     y = bufs[1].float().cpu().numpy()
     ref = oracle.c_forward(bufs[0].double().cpu().numpy(), layer.a.double().cpu().numpy(), layer.A.to_host().bits,
                            layer.mid.double().cpu().numpy(), layer.B.to_host().bits, layer.b.double().cpu().numpy())
-    assert rel_max(y, ref) <= 1e-2 and rel_norm(y, ref) <= 1e-2
+    assert rel_max(y, ref) <= TOL and rel_norm(y, ref) <= TOL, (rel_max(y, ref), rel_norm(y, ref))

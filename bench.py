@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--layer-kernels", action="store_true", help="per-layer GEMV kernels instead of the engine")
     return ap.parse_args()
@@ -64,6 +65,14 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def tensor_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"]))
+    return 1590.0, 1400.0
 
 
 class ClockSampler:
@@ -255,6 +264,57 @@ def time_graph(g, steps, warmup, barrier=lambda: None):
     return e0.elapsed_time(e1) / steps  # ms per step
 
 
+def prefill_bench(model: str, bpw: float, tokens: int, steps: int, warmup: int):
+    """BASELINE configs[2]: every Llama-2 linear shape at ~1 bpw, a prefill of `tokens` tokens through
+    the tcgen05 path (forward_prefill), timed per distinct shape with CUDA events, against the
+    dense fp16 cuBLAS GEMM of the same shapes; FLOPs = 2 T k (n + m) per layer."""
+    import torch
+
+    import paper_2505_11076_b200 as P
+    from paper_2505_11076_b200.budget import middle_dim
+    from paper_2505_11076_b200.plan import block_shapes
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    rows, total_us, total_dense_us, total_flops = [], 0.0, 0.0, 0.0
+    shapes = block_shapes(model)
+    for name, n, m in shapes:
+        k = middle_dim(n, m, bpw, 32)
+        layer = P.random_device_layer(n, k, m, generator=g, keep_words=True)
+        layer.A.paired, layer.B.paired  # build the prefill layout outside the timed region
+        X = torch.randn((tokens, m), generator=g, device="cuda").half()
+        Y = torch.empty((tokens, n), dtype=torch.half, device="cuda")
+        W = torch.randn((n, m), generator=g, device="cuda").half()
+        Yd = torch.empty_like(Y)
+
+        def t_of(fn):
+            for _ in range(warmup):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                fn()
+            e1.record()
+            e1.synchronize()
+            return e0.elapsed_time(e1) * 1e3 / steps
+
+        us = t_of(lambda: P.forward_prefill(X, layer, out=Y))
+        us_dense = t_of(lambda: torch.matmul(X, W.t(), out=Yd))
+        flops = 2.0 * tokens * k * (n + m)
+        rows.append({"layer": name, "n": n, "k": k, "m": m, "us": us, "tflops": flops / us / 1e6,
+                     "cublas_fp16_dense_us": us_dense})
+        total_us += us
+        total_dense_us += us_dense
+        total_flops += flops
+        del layer, X, Y, W, Yd
+    torch.cuda.empty_cache()
+    return {"workload": f"{model} linears, DBF {bpw} bpw, prefill {tokens} tokens (tcgen05 path)",
+            "tokens": tokens, "us_per_block": total_us, "tokens_per_s_linears_only": tokens / (total_us * 32 / 1e6),
+            "tflops": total_flops / total_us / 1e6, "cublas_fp16_dense_us_per_block": total_dense_us,
+            "speedup_vs_cublas_dense": total_dense_us / total_us, "layers": rows}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -354,6 +414,14 @@ def main():
         except Exception:
             traffic = None
 
+    prefill = None
+    if rank == 0 and not args.no_prefill:
+        prefill = prefill_bench(args.model, 1.0, 2048, max(args.steps // 2, 5), 3)
+        _, bf16_peak = tensor_peaks()
+        prefill["roofline"] = {"bound": "tensor", "achieved": prefill["tflops"], "peak": bf16_peak,
+                               "unit": "TFLOP/s", "frac": prefill["tflops"] / bf16_peak,
+                               "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense fp16 = bf16 rate)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         ref = CpuReference(args.model, args.bpw)
@@ -375,7 +443,7 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "int8-tc(i32 exact) / fp16 io",
+            "dtype": "int8-tc (exact i32 per 256-col chunk) / fp16 io",
             "data": "synthetic random-init DBF factors of Llama-2-7B shapes (uniform signs, fp16 scales)",
             "config": {
                 "workload": WORKLOAD, "model": args.model, "bpw": args.bpw, "global_batch": args.batch * world,
@@ -385,7 +453,7 @@ def main():
                 "bytes_per_step": bytes_step, "l2": "working set 1.63 GB/step > 2x126 MB L2; no flush",
                 "cublas_fp16": cublas,
                 "path": "layer kernels (2 GEMV launches per layer)" if args.layer_kernels else
-                        "decode engine: 1 persistent kernel per step (TMA-bulk sign ring + int8 mma.sync + LL handoff)",
+                        "decode engine: 1 persistent kernel per step (bulk-copy sign ring + int8 mma.sync + fp16 LL handoff)",
             },
             "roofline": {"bound": "hbm", "achieved": bytes_step / (ms * 1e-3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": bytes_step / (ms * 1e-3) / 1e9 / peak, "traffic": traffic,
@@ -394,6 +462,7 @@ def main():
                          "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "prefill": prefill,
             "gpu_launches": launches * args.steps,
             "clocks": clk,
         }

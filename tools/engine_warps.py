@@ -29,7 +29,7 @@ plan.use_engine()
 eng = plan.engine
 nr = eng.nruns
 runs0 = eng._offsets[1] - eng._offsets[0]
-eng.trace = torch.zeros(4 * nr + runs0 * 16 * 4 + 64, dtype=torch.int64, device="cuda")
+eng.trace = torch.zeros(4 * nr + 16 * 4 * 64 + runs0 * 16 * 4 + 64, dtype=torch.int64, device="cuda")
 eng._prog.trace = eng.trace.data_ptr()
 eng._prog.pad = 4 * nr
 for _ in range(3):
@@ -37,6 +37,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 t = eng.trace.cpu().numpy()
 d = t[4 * nr: 4 * nr + runs0 * 64].reshape(runs0, 16, 4)
+qd = t[4 * nr + 16 * 4 * 64: 4 * nr + 16 * 4 * 64 + runs0 * 64].reshape(runs0, 16, 4)
 base = d[0, :, 0].min()
 for j in range(runs0):
     seg, rb, n = eng._flat[j]
@@ -45,4 +46,8 @@ for j in range(runs0):
     c = d[j, :, 2] - d[j, :, 1]
     w = d[j, :, 3]
     print(f"run {j:2d} seg {seg:3d} n {n}: start {s0.min():7d}..{s0.max():7d}  quant(first) med {int(np.median(q)):6d} max {q.max():6d}"
-          f"  compute med {int(np.median(c)):6d} max {c.max():6d}  wait-w med {int(np.median(w)):6d} max {w.max():6d}")
+          f"  compute med {int(np.median(c)):6d} max {c.max():6d}")
+    ok = qd[j, :, 0] > 0
+    if ok.any():
+        a = (qd[j, ok, 0] - d[j, ok, 0]); b = qd[j, ok, 1] - qd[j, ok, 0]; cc = qd[j, ok, 2] - qd[j, ok, 1]; e = d[j, ok, 1] - qd[j, ok, 2]
+        print(f"      quantize: loads {int(np.median(a))}  max-reduce {int(np.median(b))}  digits {int(np.median(cc))}  tail {int(np.median(e))}")

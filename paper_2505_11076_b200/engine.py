@@ -175,14 +175,22 @@ class EngineProgram:
         unit_bytes = {j: ((sg[2] + 255) // 256) * 512 for j, sg in enumerate(segs)}
         per_cta_runs: list[list[tuple[int, int, int]]] = []
         for lst in per_cta:
-            runs_c: list[list[int]] = []
+            maximal: list[list[int]] = []
             for seg, rb in lst:
-                if (runs_c and runs_c[-1][0] == seg and runs_c[-1][1] + runs_c[-1][2] == rb
-                        and runs_c[-1][2] < max_units and (runs_c[-1][2] + 1) * unit_bytes[seg] <= max_bytes):
-                    runs_c[-1][2] += 1
+                if maximal and maximal[-1][0] == seg and maximal[-1][1] + maximal[-1][2] == rb:
+                    maximal[-1][2] += 1
                 else:
-                    runs_c.append([seg, rb, 1])
-            per_cta_runs.append([tuple(r) for r in runs_c])
+                    maximal.append([seg, rb, 1])
+            runs_c: list[tuple[int, int, int]] = []
+            for seg, rb, n in maximal:  # split evenly (e.g. 10 units -> 5 + 5, not 8 + 2)
+                cap = max(1, min(max_units, max_bytes // unit_bytes[seg]))
+                parts = -(-n // cap)
+                start = rb
+                for p in range(parts):
+                    cnt = n * (p + 1) // parts - n * p // parts
+                    runs_c.append((seg, start, cnt))
+                    start += cnt
+            per_cta_runs.append(runs_c)
         offsets = np.zeros(self.grid + 1, dtype=np.int32)
         offsets[1:] = np.cumsum([len(x) for x in per_cta_runs])
         flat = np.ascontiguousarray(np.array([r for lst in per_cta_runs for r in lst], dtype=np.int32).reshape(-1, 3))

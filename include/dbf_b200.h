@@ -105,6 +105,20 @@ int dbf_repack_u8(const uint8_t* bytes, int64_t rows, int64_t cols, uint32_t* wo
 int dbf_words_to_u8(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
                     uint8_t* bytes, void* stream);
 
+/* dbf_transpose_signs -- canonical words of S (rows x cols) -> canonical words of S^T (cols x rows,
+ * pitch out_pitch >= dbf_canonical_pitch_words(rows)); padding bits zero.  Feeds the transposed
+ * sign products of the staged gradients (budget.channel_scores, budget.py:145-173;
+ * factorize._staged_loss_grads / refine_scales, factorize.py:310-370). */
+int dbf_transpose_signs(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
+                        uint32_t* out, int64_t out_pitch, void* stream);
+
+/* dbf_sign_gemm_f64 -- out[i, r] = sum_c S[r, c] * x[i, c] in float64 on CUDA cores (canonical
+ * words; x: batch x cols, stride ldx; out: batch x rows, stride ldo).  The float64 sign products of
+ * the staged gradients (budget.py:158-168, factorize.py:310-326), where the reference's tests
+ * compare exact zeros and equalities. */
+int dbf_sign_gemm_f64(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
+                      const double* x, int64_t ldx, int64_t batch, double* out, int64_t ldo, void* stream);
+
 /* dbf_tile_signs -- canonical words -> tiled decode layout (dbf_tiled_bytes(rows, cols)). */
 int dbf_tile_signs(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
                    void* tiled, void* stream);

@@ -21,6 +21,7 @@ from .bitcore import (
 )
 from .budget import middle_dim, storage_bits
 from .device import DeviceLayer, DeviceSignMatrix
+from .staged import ChannelScores, channel_scores, refine_scales, staged_loss_grads
 from .kernel import (
     BENCH_CSV_HEADER,
     BenchRow,
@@ -38,6 +39,10 @@ __version__ = "0.1.0"
 __all__ = [
     "BENCH_CSV_HEADER",
     "BenchRow",
+    "ChannelScores",
+    "channel_scores",
+    "refine_scales",
+    "staged_loss_grads",
     "DbfFormatError",
     "DbfLayer",
     "DbfNativeError",

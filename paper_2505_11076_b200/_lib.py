@@ -42,6 +42,8 @@ SIGNATURES: dict[str, tuple] = {
     "dbf_repack_u8": (_int, [_vp, _i64, _i64, _vp, _i64, _vp]),
     "dbf_words_to_u8": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "dbf_tile_signs": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    "dbf_transpose_signs": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),
+    "dbf_sign_gemm_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp]),
     "dbf_forward_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "dbf_sign_matvec": (_int, [_vp, _i64, _i64, _vp, _int, _i64, _i64, _vp, _int, _i64, _vp, _sz, _vp]),
     "dbf_forward": (

@@ -127,6 +127,72 @@ __global__ void pair_kernel(const uint32_t* __restrict__ words, int64_t n, uint3
   paired[i] = p;
 }
 
+// ---- bit-matrix transpose (canonical words): one warp per 32 x 32 bit block.  Lane i holds the
+// word of row r0+i; __ballot_sync over bit j gives the word of transposed row c0+j (bit i <-> row
+// r0+i).  Used for the transposed sign products of the staged gradients (budget.py:145-173,
+// factorize.py:310-326): d_h2 = d_h3 @ A, d_h0 = (d_h2 * mid) @ B.
+__global__ void transpose_kernel(const uint32_t* __restrict__ words, int64_t rows, int64_t cols, int64_t pitch,
+                                 uint32_t* __restrict__ out, int64_t out_pitch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t rblocks = (rows + 31) >> 5, cblocks = (cols + 31) >> 5;
+  if (warp >= rblocks * cblocks) return;
+  const int64_t rb = warp % rblocks, cb = warp / rblocks;
+  const int64_t r = rb * 32 + lane;
+  const uint32_t w = (r < rows && cb < pitch) ? __ldg(words + r * pitch + cb) : 0u;
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t t = __ballot_sync(0xffffffffu, (w >> j) & 1u);
+    const int64_t orow = cb * 32 + j;
+    if (lane == j && orow < cols) out[orow * out_pitch + rb] = t;
+  }
+}
+
+// Zero the padding words of the transposed matrix (rows of out beyond the 32-bit blocks written).
+__global__ void zero_pad_kernel(uint32_t* out, int64_t rows, int64_t pitch, int64_t first_word) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per = pitch - first_word;
+  if (per <= 0 || i >= rows * per) return;
+  out[(i / per) * pitch + first_word + i % per] = 0u;
+}
+
+// ---- float64 sign GEMM on CUDA cores: out[i, r] = sum_c S[r, c] * x[i, c] (canonical words).
+// The staged-gradient consumers (budget.channel_scores, factorize.refine_scales) are float64 numpy
+// in the reference and their tests compare exact zeros / equalities (test_budget.py:97-104,
+// test_factorize.py:231-238), so they get an fp64 path: one warp per (row, 4 input rows); lane =
+// bit position, so the x loads of a 32-column word are one coalesced 256-byte access.
+constexpr int kF64Batch = 4;
+__global__ void sign_gemm_f64_kernel(const uint32_t* __restrict__ words, int64_t rows, int64_t cols, int64_t pitch,
+                                     const double* __restrict__ x, int64_t ldx, int64_t batch,
+                                     double* __restrict__ out, int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t bgroups = (batch + kF64Batch - 1) / kF64Batch;
+  if (warp >= rows * bgroups) return;
+  const int64_t r = warp / bgroups, i0 = (warp % bgroups) * kF64Batch;
+  double acc[kF64Batch] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t nw = (cols + 31) >> 5;
+  for (int64_t wi = 0; wi < nw; ++wi) {
+    const uint32_t w = __ldg(words + r * pitch + wi);
+    const int64_t c = wi * 32 + lane;
+    if (c < cols) {
+      const bool plus = (w >> lane) & 1u;
+#pragma unroll
+      for (int b = 0; b < kF64Batch; ++b)
+        if (i0 + b < batch) {
+          const double v = __ldg(x + (i0 + b) * ldx + c);
+          acc[b] += plus ? v : -v;
+        }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < kF64Batch; ++b) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+    if (lane == 0 && i0 + b < batch) out[(i0 + b) * ldo + r] = acc[b];
+  }
+}
+
 extern "C" int dbf_pack_signs(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t ld,
                               uint32_t* words, int64_t word_pitch, int64_t* d_first_bad,
                               void* stream) {
@@ -194,5 +260,35 @@ extern "C" int dbf_pair_signs(const uint32_t* words, int64_t rows, int64_t word_
   if (!words || !paired || rows < 1 || word_pitch < 1) return DBF_ERR_INVALID_ARGUMENT;
   const int64_t n = rows * word_pitch;
   pair_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(words, n, paired);
+  return check_launch();
+}
+
+extern "C" int dbf_transpose_signs(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
+                                   uint32_t* out, int64_t out_pitch, void* stream) {
+  if (!words || !out || rows < 1 || cols < 1) return DBF_ERR_INVALID_ARGUMENT;
+  if (word_pitch < ceil_div(cols, 32) || out_pitch < ceil_div(rows, 32)) return DBF_ERR_SHAPE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nwarps = ceil_div(rows, 32) * ceil_div(cols, 32);
+  transpose_kernel<<<(unsigned)ceil_div(nwarps * 32, 256), 256, 0, s>>>(words, rows, cols, word_pitch, out,
+                                                                         out_pitch);
+  int st = check_launch();
+  if (st != DBF_OK) return st;
+  const int64_t first = ceil_div(rows, 32);
+  if (out_pitch > first) {
+    const int64_t n = cols * (out_pitch - first);
+    zero_pad_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(out, cols, out_pitch, first);
+    st = check_launch();
+  }
+  return st;
+}
+
+extern "C" int dbf_sign_gemm_f64(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
+                                 const double* x, int64_t ldx, int64_t batch, double* out, int64_t ldo,
+                                 void* stream) {
+  if (!words || !x || !out || rows < 1 || cols < 1 || batch < 1) return DBF_ERR_INVALID_ARGUMENT;
+  if (word_pitch < ceil_div(cols, 32) || ldx < cols || ldo < rows) return DBF_ERR_SHAPE;
+  const int64_t nwarps = rows * ceil_div(batch, kF64Batch);
+  sign_gemm_f64_kernel<<<(unsigned)ceil_div(nwarps * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      words, rows, cols, word_pitch, x, ldx, batch, out, ldo);
   return check_launch();
 }

@@ -119,6 +119,22 @@ class DeviceSignMatrix:
             self._paired = out
         return self._paired
 
+    def transposed(self) -> "DeviceSignMatrix":
+        """S^T as its own device sign matrix (canonical words + tiled), built once on the GPU."""
+        import torch
+
+        if getattr(self, "_transposed", None) is None:
+            w = self._need_words()
+            pitch = _lib.lib.dbf_canonical_pitch_words(self.rows)
+            out = torch.empty((self.cols, pitch), dtype=torch.int32, device=w.device)
+            _lib.check(
+                _lib.lib.dbf_transpose_signs(w.data_ptr(), self.rows, self.cols, w.shape[1], out.data_ptr(), pitch,
+                                             _lib.stream_ptr()),
+                "dbf_transpose_signs",
+            )
+            self._transposed = DeviceSignMatrix.from_words(out, self.cols, self.rows, tile=True, keep_words=True)
+        return self._transposed
+
     def to_host(self) -> SignMatrix:
         from .bitcore import words_to_bytes
 

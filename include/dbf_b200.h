@@ -308,6 +308,16 @@ int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_
                         int64_t k, int64_t m, const void* X, int64_t tokens, int64_t ldx, void* Y,
                         int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The same forward as ONE persistent kernel (GEMM1 and GEMM2 tiles scheduled dynamically over the
+ * SMs, GEMM2 tiles of a token block start as soon as that block's t is published).  Workspace:
+ * dbf_prefill_fused_workspace_bytes (t + scheduling counters, 256-byte aligned); X, Y need 16-byte
+ * aligned rows.  Same numerics as dbf_forward_prefill. */
+size_t dbf_prefill_fused_workspace_bytes(int64_t k, int64_t tokens);
+int dbf_forward_prefill_fused(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired,
+                              int64_t B_pitch, const void* a, const void* mid, const void* b, int64_t n,
+                              int64_t k, int64_t m, const void* X, int64_t tokens, int64_t ldx, void* Y,
+                              int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

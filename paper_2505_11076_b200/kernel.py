@@ -13,6 +13,7 @@ relative, well inside the reference's own 1e-5 / 1e-4 tolerances (test_kernel.py
 
 from __future__ import annotations
 
+import os
 import time
 import weakref
 from dataclasses import dataclass
@@ -78,6 +79,9 @@ def as_device_signs(s) -> DeviceSignMatrix:
 # device fast path
 # ---------------------------------------------------------------------------------------------
 PREFILL_MIN_TOKENS = 64
+# DBF_PREFILL_FUSED=1 selects the single persistent kernel for both GEMMs (dbf_forward_prefill_fused);
+# it is correct but slower than the two-launch path on B200 so far, so not the default
+PREFILL_FUSED = bool(os.environ.get("DBF_PREFILL_FUSED"))
 
 
 def _prefill_eligible(X2, layer: DeviceLayer, out_dtype) -> bool:
@@ -114,16 +118,18 @@ def forward_prefill(X, layer: DeviceLayer, out=None):
         Xp[:, :m] = X
         X = Xp[:, :m]
     Y = out if out is not None else torch.empty((T, layer.n), dtype=torch.float16, device=X.device)
-    ws_bytes = _lib.lib.dbf_prefill_workspace_bytes(layer.k, T)
-    ws = _workspace(ws_bytes, X.device)
     A, B = layer.A.paired, layer.B.paired
+    fused = PREFILL_FUSED and Y.stride(0) % 8 == 0 and Y.data_ptr() % 16 == 0
+    name = "dbf_forward_prefill_fused" if fused else "dbf_forward_prefill"
+    ws_bytes = (_lib.lib.dbf_prefill_fused_workspace_bytes if fused else _lib.lib.dbf_prefill_workspace_bytes)(layer.k, T)
+    ws = _workspace(ws_bytes, X.device)
     _lib.check(
-        _lib.lib.dbf_forward_prefill(
+        getattr(_lib.lib, name)(
             A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1],
             layer.a.data_ptr(), layer.mid.data_ptr(), layer.b.data_ptr(), layer.n, layer.k, layer.m_dim,
             X.data_ptr(), T, X.stride(0), Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(), _lib.stream_ptr(),
         ),
-        "dbf_forward_prefill",
+        name,
     )
     return Y
 

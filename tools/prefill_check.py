@@ -59,6 +59,19 @@ def main():
     flops = 2.0 * T * k * (n + m)
     print(f"forward {us:.1f} us  {flops / us / 1e6:.1f} TFLOP/s")
 
+    Yf = P.forward_prefill(X, layer)
+    torch.cuda.synchronize()
+    errF = (Yf.float() - refY).abs().max().item() / refY.abs().max().item()
+    for _ in range(3):
+        P.forward_prefill(X, layer, out=Yf)
+    e0.record()
+    for _ in range(reps):
+        P.forward_prefill(X, layer, out=Yf)
+    e1.record()
+    e1.synchronize()
+    usf = e0.elapsed_time(e1) * 1e3 / reps
+    print(f"fused forward {usf:.1f} us  {flops / usf / 1e6:.1f} TFLOP/s  max rel err {errF:.3e}")
+
     def g1():
         _lib.lib.dbf_sign_gemm(X.data_ptr(), T, m, m, layer.B.paired.data_ptr(), layer.B.paired.shape[1], k,
                                layer.b.data_ptr(), layer.mid.data_ptr(), out.data_ptr(), k, _lib.stream_ptr())

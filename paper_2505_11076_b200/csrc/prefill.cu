@@ -97,7 +97,9 @@ __device__ __forceinline__ void expand_word(uint32_t w, const uint32_t* ks, uint
   for (int q = 0; q < 16; ++q) v[q] = ((nw << (15 - q)) & 0x80008000u) ^ ks[q];
 }
 
-template <bool KSCALE>
+// MC: CTA pairs (cluster 2x1) that share a token tile; each loads half of the activation box and
+// multicasts it to both, so every SM pulls 16 KB instead of 32 KB per K block through TMA.
+template <bool KSCALE, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     sign_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bar.full_act[s], 1);
       mbar_init(&bar.full_a[s], kExpWarps);
-      mbar_init(&bar.empty[s], 1);
+      mbar_init(&bar.empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs must be done with the slot
     }
     mbar_init(&bar.acc_full, 1);
     fence_mbar_init();
@@ -132,8 +134,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // the peer's barriers exist before any multicast reaches them
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
+  const uint32_t rank = MC ? cluster_ctarank() : 0u;
   const bool tracing = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
 
   if (warp == 0 || warp == 2 || warp == 3) {
@@ -149,7 +153,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bar.empty[s], ph ^ 1);
         if (tracing) p.trace[5 * p.num_kb + kb] = clock64();
         mbar_arrive_expect_tx(&bar.full_act[s], kActStageBytes);
-        tma_load_2d(act + (size_t)s * kActStageBytes, &act_map, kb * BK, tok0, &bar.full_act[s], pol);
+        if constexpr (MC)
+          tma_load_2d_mc(act + (size_t)s * kActStageBytes + rank * (kActStageBytes / 2), &act_map, kb * BK,
+                         tok0 + (int)rank * (BN / 2), &bar.full_act[s], (uint16_t)0x3, pol);
+        else
+          tma_load_2d(act + (size_t)s * kActStageBytes, &act_map, kb * BK, tok0, &bar.full_act[s], pol);
       }
     }
   } else if (warp == 1) {
@@ -174,7 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_f16_ts(tmem + kAccCol + h * BN, a_base + h * kAColsPerHalf + kk * (UK / 2), bd, idesc,
                        (kb | kk) != 0);
         }
-        mma_commit(&bar.empty[s]);
+        if constexpr (MC) mma_commit_mc(&bar.empty[s], (uint16_t)0x3);
+        else mma_commit(&bar.empty[s]);
       }
       mma_commit(&bar.acc_full);
     }
@@ -248,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -273,12 +283,12 @@ static EncodeTiledFn encode_fn() {
 }
 
 // act: T x K fp16, row stride ld elements (ld*2 % 16 == 0, 16-byte aligned base)
-static int make_act_map(CUtensorMap* map, const void* act, int64_t T, int64_t K, int64_t ld) {
+static int make_act_map(CUtensorMap* map, const void* act, int64_t T, int64_t K, int64_t ld, int box_rows = BN) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return DBF_ERR_CUDA;
   const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)T};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  const cuuint32_t box[2] = {BK, BN};
+  const cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(act), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -297,8 +307,9 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   if (pitch * 32 < ceil_div(K, BK) * BK) return DBF_ERR_SHAPE;  // a K block would read past the row
   if (T > INT32_MAX || rows > INT32_MAX || K > INT32_MAX) return DBF_ERR_UNSUPPORTED;
   if (kscale && K > kMaxKScale) return DBF_ERR_UNSUPPORTED;
+  static const bool mc = getenv("DBF_PREFILL_MULTICAST") != nullptr;  // measured slower
   CUtensorMap map;
-  int st = make_act_map(&map, act, T, K, ld_act);
+  int st = make_act_map(&map, act, T, K, ld_act, mc ? BN / 2 : BN);
   if (st != DBF_OK) return st;
   Params p;
   p.words = words;
@@ -316,14 +327,30 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
     if (!trace_buf) cudaMalloc(&trace_buf, 8 * 6 * 4096);
     p.trace = trace_buf;
   }
-  dim3 grid((unsigned)ceil_div(rows, BM), (unsigned)ceil_div(T, BN));
+  const unsigned gx = (unsigned)ceil_div(rows, BM);
+  dim3 grid(mc ? (gx + 1) / 2 * 2 : gx, (unsigned)ceil_div(T, BN));
   const size_t smem = smem_bytes(p.num_kb, kscale != nullptr);
-  auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, kThreads, smem, stream>>>(map, p);
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = mc ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, map, p);
   };
-  if (kscale) go(sign_gemm_kernel<true>);
-  else go(sign_gemm_kernel<false>);
+  cudaError_t e;
+  if (mc) e = kscale ? go(sign_gemm_kernel<true, true>) : go(sign_gemm_kernel<false, true>);
+  else e = kscale ? go(sign_gemm_kernel<true, false>) : go(sign_gemm_kernel<false, false>);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   return check_launch();
 }
 

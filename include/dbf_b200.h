@@ -89,6 +89,11 @@ int64_t dbf_tiled_bytes(int64_t rows, int64_t cols);
 int dbf_pack_signs(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t ld,
                    uint32_t* words, int64_t word_pitch, int64_t* d_first_bad, void* stream);
 
+/* dbf_pack_sign_of -- pack(np.where(Z >= 0, 1, -1)) of svid.svid (svid.py:99-103): bit = (v >= 0),
+ * canonical words, no +-1 validation (the caller rejects non-finite input like as_matrix). */
+int dbf_pack_sign_of(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t ld,
+                     uint32_t* words, int64_t word_pitch, void* stream);
+
 /* dbf_unpack_signs -- replaces bitcore.unpack (bitcore.py:88-91): canonical words -> +-1. */
 int dbf_unpack_signs(const uint32_t* words, int64_t rows, int64_t cols, int64_t word_pitch,
                      void* dense, int dtype, int64_t ld, void* stream);

@@ -14,9 +14,11 @@ from .bitcore import (
     dumps_dbf,
     load_dbf,
     pack,
+    pack_sign_of,
     reconstruct,
     row_bytes,
     save_dbf,
+    transpose_signs,
     unpack,
 )
 from .budget import middle_dim, storage_bits
@@ -57,6 +59,7 @@ __all__ = [
     "load_dbf",
     "middle_dim",
     "pack",
+    "pack_sign_of",
     "random_device_layer",
     "reconstruct",
     "row_bytes",
@@ -64,5 +67,6 @@ __all__ = [
     "sign_matvec",
     "sign_matvec_device",
     "storage_bits",
+    "transpose_signs",
     "unpack",
 ]

@@ -39,6 +39,7 @@ SIGNATURES: dict[str, tuple] = {
     "dbf_tiled_bytes": (_i64, [_i64, _i64]),
     "dbf_pack_signs": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _vp]),
     "dbf_unpack_signs": (_int, [_vp, _i64, _i64, _i64, _vp, _int, _i64, _vp]),
+    "dbf_pack_sign_of": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp]),
     "dbf_repack_u8": (_int, [_vp, _i64, _i64, _vp, _i64, _vp]),
     "dbf_words_to_u8": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "dbf_tile_signs": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),

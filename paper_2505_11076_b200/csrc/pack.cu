@@ -27,6 +27,21 @@ __global__ void pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t c
   if (lane == 0) words[r * pitch + wj] = w;
 }
 
+// ---- sign-of pack: bit = (v >= 0), the svid projection's np.where(Z >= 0, 1, -1) followed by
+// pack (svid.py:99-103); no +-1 validation.
+template <typename T>
+__global__ void pack_sign_of_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols, int64_t ld,
+                                    uint32_t* __restrict__ words, int64_t pitch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= rows * pitch) return;
+  const int64_t r = warp / pitch, wj = warp % pitch;
+  const int64_t c = wj * 32 + lane;
+  const bool plus = c < cols && to_f64<T>(dense[r * ld + c]) >= 0.0;
+  const uint32_t w = __ballot_sync(0xffffffffu, plus);
+  if (lane == 0) words[r * pitch + wj] = w;
+}
+
 __global__ void init_first_bad_kernel(unsigned long long* p) { *p = ~0ull; }
 
 // ---- unpack: one thread per element (coalesced stores).
@@ -291,4 +306,17 @@ extern "C" int dbf_sign_gemm_f64(const uint32_t* words, int64_t rows, int64_t co
   sign_gemm_f64_kernel<<<(unsigned)ceil_div(nwarps * 32, 256), 256, 0, (cudaStream_t)stream>>>(
       words, rows, cols, word_pitch, x, ldx, batch, out, ldo);
   return check_launch();
+}
+
+extern "C" int dbf_pack_sign_of(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t ld,
+                                uint32_t* words, int64_t word_pitch, void* stream) {
+  if (!dense || !words || rows < 1 || cols < 1 || ld < cols || word_pitch < canonical_pitch(cols))
+    return DBF_ERR_INVALID_ARGUMENT;
+  const int64_t threads = rows * word_pitch * 32;
+  return dispatch_float(dtype, [&](auto tag) {
+    using T = decltype(tag);
+    pack_sign_of_kernel<T><<<grid_for(threads, 256), 256, 0, (cudaStream_t)stream>>>((const T*)dense, rows, cols,
+                                                                                        ld, words, word_pitch);
+    return check_launch();
+  });
 }

@@ -8,6 +8,8 @@ theirs (pkg/tests/conftest.py:17-24, test_budget.py:94-145, test_factorize.py:23
 
 from __future__ import annotations
 
+# also: svid sign projection + packed transpose fixtures
+
 import sys
 from pathlib import Path
 
@@ -53,6 +55,18 @@ def main():
         g[f"c{i}_rloss"] = np.array(float(np.sum((dbf.forward(Xr, out) - Yr) ** 2)))
         g[f"c{i}_ploss"] = np.array(float(np.sum((dbf.forward(Xr, pert) - Yr) ** 2)))
     g["count"] = np.array(len(cases))
+    # sign packing inside the factorization loop: svid's sign projection
+    # (svid.py:99-103) and _assemble's transpose (factorize.py:193-195)
+    shapes = [(1, 1), (7, 9), (33, 31), (64, 100), (130, 257)]
+    for j, (r, c) in enumerate(shapes):
+        Z = rng.standard_normal((r, c))
+        Z[rng.random((r, c)) < 0.05] = 0.0  # zeros project to +1
+        g[f"s{j}_Z"] = Z
+        g[f"s{j}_signs"] = dbf.svid(Z).signs.bits
+        S = dbf.pack(rng.integers(0, 2, (r, c)) * 2.0 - 1.0)
+        g[f"s{j}_S"] = S.bits
+        g[f"s{j}_ST"] = dbf.pack(dbf.unpack(S).T).bits
+    g["scount"] = np.array(len(shapes))
     np.savez_compressed(OUT / "golden_staged.npz", **g)
     print(f"wrote {OUT / 'golden_staged.npz'} ({len(g)} arrays)")
 

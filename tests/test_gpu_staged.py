@@ -153,3 +153,16 @@ def test_rejects_bad_batches(rng):
         P.channel_scores(layer, [], [])
     with pytest.raises(ValueError):
         P.channel_scores(layer, [np.ones((4, 5))], [np.ones((4, 8))])
+
+
+def test_factorization_sign_packing_matches_reference(gs):
+    """svid sign projection (svid.py:99-103) and the packed transpose of _assemble
+    (factorize.py:193-195): bit-exact against the reference's own packed bytes."""
+    for j in range(int(gs["scount"])):
+        Z = gs[f"s{j}_Z"]
+        np.testing.assert_array_equal(P.pack_sign_of(Z).bits, gs[f"s{j}_signs"])
+        S = gs[f"s{j}_S"]
+        r, c = Z.shape
+        T = P.transpose_signs(P.SignMatrix(r, c, S.copy()))
+        assert (T.rows, T.cols) == (c, r)
+        np.testing.assert_array_equal(T.bits, gs[f"s{j}_ST"])

@@ -27,3 +27,13 @@ def test_oracle_staged_matches_reference(gs):
         assert loss == pytest.approx(float(p("loss")), rel=1e-12)
         for got, ref in ((ga, p("ga")), (gm, p("gm")), (gb, p("gb"))):
             np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+def test_sign_projection_restatement_matches_reference(gs):
+    """numpy restatement of the svid sign projection (the checker for pack_sign_of)."""
+    for j in range(int(gs["scount"])):
+        Z = gs[f"s{j}_Z"]
+        np.testing.assert_array_equal(np.packbits(Z >= 0.0, axis=1, bitorder="little"), gs[f"s{j}_signs"])
+        r, c = Z.shape
+        S = npo.unpack_bits(gs[f"s{j}_S"], c)
+        np.testing.assert_array_equal(npo.pack_bits(S.T), gs[f"s{j}_ST"])

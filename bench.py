@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--layer-kernels", action="store_true", help="per-layer GEMV kernels instead of the engine")
     return ap.parse_args()
@@ -315,6 +316,41 @@ def prefill_bench(model: str, bpw: float, tokens: int, steps: int, warmup: int):
             "speedup_vs_cublas_dense": total_dense_us / total_us, "layers": rows}
 
 
+def sweep_bench(steps: int):
+    """BASELINE configs[3] / [4] at one GPU: the decode engine (batch 1) over Llama-2-70B shapes at
+    2 bpw and Llama-2-13B shapes across bits/weight, plus 13B at batch 8 (int8 tensor-core GEMV
+    chain) and batch 64 (tcgen05 prefill chain); every number is a full model step of linears."""
+    import torch
+
+    from paper_2505_11076_b200.plan import llama_decode_plan
+
+    rows = []
+
+    def one(model, bpw, batch, engine):
+        g = torch.Generator(device="cuda")
+        g.manual_seed(5)
+        plan = llama_decode_plan(model, bpw=bpw, batch=batch, generator=g)
+        plan.buffers[plan.input_buffer].normal_(generator=g)
+        plan.use_engine() if engine else plan.use_layer_kernels()
+        plan.capture()
+        ms = time_graph(plan._graph, steps, 3)
+        b = plan.bytes_per_step()
+        rows.append({"model": model, "bpw": bpw, "batch": batch,
+                     "path": "engine" if engine else ("tcgen05 prefill chain" if batch >= 64 else
+                                                      "int8 GEMV chain (pre-quantized batch)"),
+                     "ms_per_step": ms, "gbs": b / (ms * 1e-3) / 1e9,
+                     "tokens_per_s_linears_only": batch * 1e3 / ms, "layers": len(plan.ops)})
+        del plan
+        torch.cuda.empty_cache()
+
+    one("llama2-70b", 2.0, 1, True)
+    for bpw in (1.0, 1.5, 2.0, 2.3):
+        one("llama2-13b", bpw, 1, True)
+    one("llama2-13b", 1.5, 8, False)
+    one("llama2-13b", 1.5, 64, False)
+    return rows
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -422,6 +458,10 @@ def main():
                                "unit": "TFLOP/s", "frac": prefill["tflops"] / bf16_peak,
                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense fp16 = bf16 rate)"}
 
+    sweep = None
+    if rank == 0 and not args.no_sweep:
+        sweep = sweep_bench(max(args.steps // 4, 3))
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         ref = CpuReference(args.model, args.bpw)
@@ -463,6 +503,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "prefill": prefill,
+            "sweep": sweep,
             "gpu_launches": launches * args.steps,
             "clocks": clk,
         }

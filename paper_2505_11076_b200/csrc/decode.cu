@@ -157,11 +157,36 @@ __device__ void quantize_row(const GemvParams& p, int slot, int nkb, int lpk, ui
   __syncthreads();
 }
 
+// Batched launches quantize every input row ONCE (one CTA per row, fragments written to the
+// workspace in the B-fragment layout with lpk = 32) instead of once per GEMV CTA; the GEMV CTAs
+// then only copy the fragments of their row pairs into shared memory (PRE = true).
+template <typename AT>
+__global__ void __launch_bounds__(kThreads) quantize_rows_kernel(GemvParams p, int batch_total, int nkb,
+                                                                 uint8_t* gfrag, int* gF, long long* gT) {
+  __shared__ AT red_max[kWarps];
+  __shared__ long long red_sum[kWarps];
+  __shared__ int sF;
+  __shared__ long long sT;
+  const int slot = blockIdx.x;
+  if (slot < batch_total) {
+    quantize_row<AT>(p, slot, nkb, 32, gfrag, &sF, &sT, red_max, red_sum);
+    if (threadIdx.x == 0) { gF[slot] = sF; gT[slot] = sT; }
+  } else {  // zero half of the last pair
+    const int pair = slot >> 1, bsub = slot & 1;
+    for (int q = threadIdx.x; q < nkb * 16; q += kThreads) {
+      const int kb = q >> 4, rem = q & 15;
+      *(uint2*)(gfrag + ((int64_t)(pair * nkb + kb) * 32 + 16 * bsub + rem) * 8) = make_uint2(0, 0);
+    }
+    if (threadIdx.x == 0) { gF[slot] = 0; gT[slot] = 0; }
+  }
+}
+
 // One CTA = 8 warps; a 16-row block is split across warps by 256-column chunks.
 // NP = pairs of input rows per launch (B-fragment columns n = 4*bsub + plane).
 // SINGLE = one input row: only lanes 0..15 carry B fragments (lanes 16..31 feed zeros).
-template <int NP, bool SINGLE>
-__global__ void __launch_bounds__(kThreads) gemv_i8_kernel(GemvParams p) {
+template <int NP, bool SINGLE, bool PRE>
+__global__ void __launch_bounds__(kThreads) gemv_i8_kernel(GemvParams p, const uint8_t* gfrag, const int* gF,
+                                                          const long long* gT) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int nkb = p.nchunks * 8;
   constexpr int lpk = SINGLE ? 16 : 32;
@@ -173,9 +198,18 @@ __global__ void __launch_bounds__(kThreads) gemv_i8_kernel(GemvParams p) {
   double* red_max = (double*)(sF + 2 * NP + 2);                  // [kWarps] (8-byte aligned)
   long long* red_sum = (long long*)(red_max + kWarps);           // [kWarps]
 
-  // ---- prologue: quantize every input row of this launch into smem B fragments
+  // ---- prologue: B fragments of every input row of this launch into shared memory
   const int slots = SINGLE ? 1 : 2 * NP;
-  for (int s = 0; s < slots; ++s) {
+  if constexpr (PRE) {  // pre-quantized by quantize_rows_kernel: a straight copy
+    const uint4* src = (const uint4*)gfrag;
+    uint4* dst = (uint4*)xfrag;
+    const int n16 = (int)(xfrag_bytes / 16);
+    for (int i = threadIdx.x; i < n16; i += kThreads) dst[i] = __ldg(src + i);
+    if (threadIdx.x < slots) {
+      sF[threadIdx.x] = gF[threadIdx.x];
+      sT[threadIdx.x] = gT[threadIdx.x];
+    }
+  } else for (int s = 0; s < slots; ++s) {
     if (s < p.batch) {
       if (p.x_dtype == DBF_F64)
         quantize_row<double>(p, s, nkb, lpk, xfrag, sF + s, sT + s, red_max, red_sum);
@@ -261,28 +295,78 @@ size_t gemv_smem_bytes(int np, bool single, int nchunks) {
          (2 * np + 2) * 4 + kWarps * 8 + kWarps * 8 + 16;
 }
 
-template <int NP, bool SINGLE>
-int launch_gemv_t(const GemvParams& p, cudaStream_t s) {
+template <int NP, bool SINGLE, bool PRE = false>
+int launch_gemv_t(const GemvParams& p, cudaStream_t s, const uint8_t* gfrag = nullptr, const int* gF = nullptr,
+                  const long long* gT = nullptr) {
   const size_t smem = gemv_smem_bytes(NP, SINGLE, p.nchunks);
   static bool configured = false;  // attribute set once per instantiation (max opt-in smem)
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_i8_kernel<NP, SINGLE>,
+    cudaError_t e = cudaFuncSetAttribute(gemv_i8_kernel<NP, SINGLE, PRE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
     configured = true;
   }
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemv_i8_kernel<NP, SINGLE>, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemv_i8_kernel<NP, SINGLE, PRE>, kThreads, smem);
   per_sm = std::max(per_sm, 1);
   const int grid = std::min<int64_t>(p.nrb, (int64_t)kNumSMs * per_sm);
-  gemv_i8_kernel<NP, SINGLE><<<grid, kThreads, smem, s>>>(p);
+  gemv_i8_kernel<NP, SINGLE, PRE><<<grid, kThreads, smem, s>>>(p, gfrag, gF, gT);
   return check_launch();
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
 
+// Workspace for pre-quantized fragments of `batch` rows of `cols` columns (lpk = 32 layout).
+size_t frag_bytes(int64_t cols, int64_t batch) {
+  const int64_t pairs = (batch + 1) / 2;
+  return (size_t)pairs * chunks(cols) * 8 * 32 * 8 + (size_t)(2 * pairs) * (4 + 8) + 64;
+}
+
+// Batched rows (>= 2): quantize once into `ws` (frag_bytes), then one GEMV launch per group of up
+// to 8 row pairs copying its fragments.
+int run_gemv_pre(GemvParams p, int batch_total, cudaStream_t s, uint8_t* ws) {
+  const int nkb = p.nchunks * 8;
+  const int64_t pairs = (batch_total + 1) / 2;
+  uint8_t* gfrag = ws;
+  long long* gT = (long long*)(ws + (size_t)pairs * nkb * 32 * 8);
+  int* gF = (int*)(gT + 2 * pairs);
+  const int qgrid = (int)(2 * pairs);
+  if (p.x_dtype == DBF_F64)
+    quantize_rows_kernel<double><<<qgrid, kThreads, 0, s>>>(p, batch_total, nkb, gfrag, gF, gT);
+  else
+    quantize_rows_kernel<float><<<qgrid, kThreads, 0, s>>>(p, batch_total, nkb, gfrag, gF, gT);
+  int st = check_launch();
+  if (st != DBF_OK) return st;
+  const size_t ysz = dtype_size(p.y_dtype);
+  int done = 0;  // rows
+  while (done < batch_total) {
+    const int left = batch_total - done;
+    int np = 8;
+    while (np > 1 && (2 * np > left + 1 || gemv_smem_bytes(np, false, p.nchunks) > 227 * 1024)) np >>= 1;
+    if (gemv_smem_bytes(np, false, p.nchunks) > 227 * 1024) return DBF_ERR_UNSUPPORTED;
+    const int take = std::min(left, 2 * np);
+    GemvParams q = p;
+    q.y = (char*)p.y + (int64_t)done * p.ldy * ysz;
+    q.batch = take;
+    const int pair0 = done / 2;
+    const uint8_t* f = gfrag + (size_t)pair0 * nkb * 32 * 8;
+    switch (np) {
+      case 8: st = launch_gemv_t<8, false, true>(q, s, f, gF + done, gT + done); break;
+      case 4: st = launch_gemv_t<4, false, true>(q, s, f, gF + done, gT + done); break;
+      case 2: st = launch_gemv_t<2, false, true>(q, s, f, gF + done, gT + done); break;
+      default: st = launch_gemv_t<1, false, true>(q, s, f, gF + done, gT + done); break;
+    }
+    if (st != DBF_OK) return st;
+    done += take;
+  }
+  return DBF_OK;
+}
+
 // Runs the GEMV for all `batch` rows, grouping rows so that the B fragments fit in smem.
-int run_gemv(GemvParams p, int batch_total, cudaStream_t s) {
+int run_gemv(GemvParams p, int batch_total, cudaStream_t s, uint8_t* ws = nullptr, size_t ws_bytes = 0) {
+  if (batch_total >= 2 && ws && ws_bytes >= frag_bytes(p.cols, batch_total) &&
+      gemv_smem_bytes(1, false, p.nchunks) <= 227 * 1024)
+    return run_gemv_pre(p, batch_total, s, ws);
   const size_t xsz = dtype_size(p.x_dtype), ysz = dtype_size(p.y_dtype);
   int done = 0;
   while (done < batch_total) {
@@ -345,22 +429,23 @@ inline size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 using namespace dbf;
 
 extern "C" size_t dbf_forward_workspace_bytes(int64_t n, int64_t k, int64_t m, int64_t batch) {
-  (void)n; (void)m;
+  (void)n;
   if (k < 1 || batch < 1) return 0;
-  return align256((size_t)batch * k * sizeof(float));
+  // t (fp32) + pre-quantized B fragments for the wider stage input (batches >= 2)
+  const size_t frag = batch >= 2 ? frag_bytes(std::max(k, m), batch) : 0;
+  return align256((size_t)batch * k * sizeof(float)) + align256(frag);
 }
 
 extern "C" int dbf_sign_matvec(const void* S_tiled, int64_t rows, int64_t cols, const void* X,
                                int x_dtype, int64_t batch, int64_t ldx, void* Y, int y_dtype,
                                int64_t ldy, void* workspace, size_t workspace_bytes,
                                void* stream) {
-  (void)workspace; (void)workspace_bytes;
   if (!S_tiled || !X || !Y || rows < 1 || cols < 1 || batch < 1 || ldx < cols || ldy < rows ||
       !io_dtype_ok(x_dtype) || !io_dtype_ok(y_dtype) || rows > INT32_MAX || cols > INT32_MAX)
     return DBF_ERR_INVALID_ARGUMENT;
   GemvParams p = make_params(S_tiled, rows, cols, X, x_dtype, ldx, nullptr, nullptr, DBF_F32, Y,
                              y_dtype, ldy);
-  return run_gemv(p, (int)batch, (cudaStream_t)stream);
+  return run_gemv(p, (int)batch, (cudaStream_t)stream, (uint8_t*)workspace, workspace ? workspace_bytes : 0);
 }
 
 extern "C" int dbf_forward(const void* A_tiled, const void* B_tiled, const void* a, const void* mid,
@@ -376,13 +461,15 @@ extern "C" int dbf_forward(const void* A_tiled, const void* B_tiled, const void*
     return DBF_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   float* t = (float*)workspace;
+  uint8_t* fw = (uint8_t*)workspace + align256((size_t)batch * k * sizeof(float));
+  const size_t fwb = workspace_bytes - align256((size_t)batch * k * sizeof(float));
   // stage 1: t = mid * (B . (b * x))      (kernel.py:59 + the `* layer.mid` of kernel.py:60)
   GemvParams p1 = make_params(B_tiled, k, m, X, x_dtype, ldx, b, mid, scale_dtype, t, DBF_F32, k);
-  int st = run_gemv(p1, (int)batch, s);
+  int st = run_gemv(p1, (int)batch, s, fw, fwb);
   if (st != DBF_OK) return st;
   // stage 2: y = a * (A . t)               (kernel.py:60-61)
   GemvParams p2 = make_params(A_tiled, n, k, t, DBF_F32, k, nullptr, a, scale_dtype, Y, y_dtype, ldy);
-  return run_gemv(p2, (int)batch, s);
+  return run_gemv(p2, (int)batch, s, fw, fwb);
 }
 
 extern "C" int dbf_forward_partial(const void* A_shard_tiled, const void* B_shard_tiled,
@@ -397,13 +484,15 @@ extern "C" int dbf_forward_partial(const void* A_shard_tiled, const void* B_shar
     return DBF_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   float* t = (float*)workspace;
+  uint8_t* fw = (uint8_t*)workspace + align256((size_t)batch * k_shard * sizeof(float));
+  const size_t fwb = workspace_bytes - align256((size_t)batch * k_shard * sizeof(float));
   GemvParams p1 = make_params(B_shard_tiled, k_shard, m, X, x_dtype, ldx, b, mid_shard, scale_dtype,
                               t, DBF_F32, k_shard);
-  int st = run_gemv(p1, (int)batch, s);
+  int st = run_gemv(p1, (int)batch, s, fw, fwb);
   if (st != DBF_OK) return st;
   GemvParams p2 = make_params(A_shard_tiled, n, k_shard, t, DBF_F32, k_shard, nullptr, nullptr,
                               scale_dtype, P, DBF_F32, n);
-  return run_gemv(p2, (int)batch, s);
+  return run_gemv(p2, (int)batch, s, fw, fwb);
 }
 
 namespace dbf {

@@ -127,7 +127,8 @@ class DecodePlan:
 
 
 def llama_decode_plan(model: str = "llama2-7b", bpw: float = 2.0, batch: int = 1, blocks: int | None = None,
-                      generator=None, act_dtype=None, scale_dtype=None, device="cuda") -> DecodePlan:
+                      generator=None, act_dtype=None, scale_dtype=None, device="cuda",
+                      keep_words: bool | None = None) -> DecodePlan:
     """Synthetic random-init DBF factors of every linear layer of a Llama-2 model (§8d)."""
     import torch
 
@@ -147,7 +148,8 @@ def llama_decode_plan(model: str = "llama2-7b", bpw: float = 2.0, batch: int = 1
     for _ in range(nblocks):
         for name, n, m in shapes:
             k = middle_dim(n, m, bpw, 32)
-            layers.append(random_device_layer(n, k, m, generator=generator, scale_dtype=scale_dtype, device=device))
+            layers.append(random_device_layer(n, k, m, generator=generator, scale_dtype=scale_dtype, device=device,
+                                              keep_words=batch >= 64 if keep_words is None else keep_words))
             ops.append(PlanOp(len(layers) - 1, idx[src_of[name]], idx[dst_of[name]], name))
     if s["kv"] != s["hidden"]:
         # GQA (70B): v is narrower than o's input; o reads q's output instead

@@ -317,9 +317,10 @@ def prefill_bench(model: str, bpw: float, tokens: int, steps: int, warmup: int):
 
 
 def sweep_bench(steps: int):
-    """BASELINE configs[3] / [4] at one GPU: the decode engine (batch 1) over Llama-2-70B shapes at
-    2 bpw and Llama-2-13B shapes across bits/weight, plus 13B at batch 8 (int8 tensor-core GEMV
-    chain) and batch 64 (tcgen05 prefill chain); every number is a full model step of linears."""
+    """BASELINE configs[3] / [4] at one GPU: the decode engine (batch 1 and 4: up to 4 tokens share
+    every MMA) over Llama-2-70B shapes at 2 bpw and Llama-2-13B shapes across bits/weight, plus 13B
+    at batch 8 (int8 tensor-core GEMV chain) and batch 64 (tcgen05 prefill chain); every number is
+    a full model step of linears."""
     import torch
 
     from paper_2505_11076_b200.plan import llama_decode_plan
@@ -344,8 +345,11 @@ def sweep_bench(steps: int):
         torch.cuda.empty_cache()
 
     one("llama2-70b", 2.0, 1, True)
+    one("llama2-70b", 2.0, 4, True)
     for bpw in (1.0, 1.5, 2.0, 2.3):
         one("llama2-13b", bpw, 1, True)
+    one("llama2-7b", 2.0, 4, True)
+    one("llama2-13b", 1.5, 4, True)
     one("llama2-13b", 1.5, 8, False)
     one("llama2-13b", 1.5, 64, False)
     return rows

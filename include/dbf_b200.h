@@ -188,8 +188,9 @@ int dbf_sign_matvec_xor(const uint32_t* words, int64_t rows, int64_t cols, int64
 /* ---- decode engine: a whole chain of DBF layers in ONE persistent kernel ---------------- */
 /*
  * A program is a list of SEGMENTS (one sign GEMV each: y = oscale * (S . (iscale * v))) over
- * VECTORS.  Vector kind 0 = plain (dtype `dtype`, ready when the kernel starts, e.g. the token
- * input); kind 1 = LL ("low-latency": uint32 words {fp16 value (low 16 bits), 16-bit epoch},
+ * VECTORS, each holding `batch` tokens (1..4; every tensor-core MMA serves all of them: B columns
+ * 2*token + digit plane).  Vector kind 0 = plain (dtype `dtype`, batch x len contiguous, ready when
+ * the kernel starts, e.g. the token input); kind 1 = LL ("low-latency": uint32 words {fp16 value (low 16 bits), 16-bit epoch},
  * produced inside the kernel by another segment and consumed by polling the words themselves;
  * the buffer is padded to a multiple of 256 words).  Every segment's work is split into UNITS of
  * 16 rows; each CTA executes a list of RUNS -- up to dbf_engine_run_limits() consecutive units of
@@ -217,7 +218,7 @@ typedef struct {
 } dbf_engine_segment;
 
 typedef struct {
-  void* data;           /* plain: `len` values of `dtype`; LL: uint32 words, padded to 256 */
+  void* data;           /* plain: batch x len values of `dtype`; LL: batch x (len padded to 256) uint32 words */
   int32_t len;
   int32_t kind;         /* 0 plain, 1 LL */
   int32_t dtype;        /* plain dtype (F16/F32) */
@@ -255,7 +256,7 @@ typedef struct {
   int32_t nvectors;
   int32_t grid;                       /* CTAs (<= number of SMs; one per SM)                    */
   int32_t max_cols;                   /* largest segment `cols` (sizes shared memory)          */
-  int32_t pad;
+  int32_t batch;                      /* tokens per step, 1..4 (vectors hold batch rows each)   */
 } dbf_engine_program;
 
 /*
@@ -265,12 +266,13 @@ typedef struct {
  */
 int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t nsegments,
                           const dbf_engine_vector* vectors, int32_t nvectors, const int32_t* runs,
-                          int32_t nruns, uint32_t* ready, dbf_engine_run* out);
+                          int32_t nruns, int32_t batch, uint32_t* ready, dbf_engine_run* out);
 
-/* Largest run the engine accepts: units per run and packed-sign bytes per run. */
-int dbf_engine_run_limits(int32_t* max_units, int64_t* max_run_bytes);
-/* Dynamic shared memory the engine needs for max_cols; DBF_ERR_UNSUPPORTED if it cannot fit. */
-int dbf_engine_smem_bytes(int32_t max_cols, size_t* bytes);
+/* Largest run the engine accepts at this batch: units per run and packed-sign bytes per run. */
+int dbf_engine_run_limits(int32_t batch, int32_t* max_units, int64_t* max_run_bytes);
+/* Dynamic shared memory the engine needs for max_cols at this batch (1..4); DBF_ERR_UNSUPPORTED if
+ * it cannot fit. */
+int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* bytes);
 /* Resident engine CTAs per SM and registers per thread for max_cols (diagnostics). */
 int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, int32_t* regs_per_thread);
 /* Launch one run of the program (cooperative: all CTAs co-resident) + the epoch advance. */

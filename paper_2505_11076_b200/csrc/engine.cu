@@ -41,9 +41,11 @@ constexpr int kMaxUnits = 8;                  // units per run (the host splits 
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMinSlots = 4;
 constexpr int kMaxSlots = 16;
-constexpr int kChunkQBytes = 8 * 64;          // one quantized chunk: 8 k-blocks x (2 planes x 4 lanes x 8 B)
-constexpr int kXsBytes = 2 * kChunkQBytes;    // per-warp B-fragment scratch: the warp's (up to) 2 chunks
-constexpr int kPartFloats = kWarps * kMaxUnits * 16;  // one partial buffer
+// Per token of a batch (NB tokens share every MMA: B column n = 2*token + digit plane):
+constexpr int kChunkQBytes1 = 8 * 64;         // one quantized chunk: 8 k-blocks x (2 planes x 4 lanes x 8 B)
+constexpr int kPartFloats1 = kWarps * kMaxUnits * 16;  // one partial buffer
+template <int NB> constexpr int xs_chunks() { return NB <= 2 ? 2 : 1; }  // chunks a warp keeps for reuse
+template <int NB> constexpr int xs_bytes() { return xs_chunks<NB>() * kChunkQBytes1 * NB; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -127,7 +129,14 @@ struct InSpec {
   const void* x;
   const void* iscale;
   int kind, dtype, sdt, cols;
+  int64_t tstride;  // elements between consecutive tokens of the vector
 };
+__device__ __forceinline__ InSpec token_of(const InSpec& in, int t) {
+  InSpec o = in;
+  const int esz = in.kind == 1 ? 4 : (in.dtype == DBF_F16 ? 2 : 4);
+  o.x = (const char*)in.x + (int64_t)t * in.tstride * esz;
+  return o;
+}
 
 // The 4 input scales of columns col0..col0+3 (1 when there is no input scale, 0 beyond cols).
 __device__ __forceinline__ void load_scale4(const InSpec& in, int col0, float (&s)[4]) {
@@ -186,7 +195,7 @@ __device__ __forceinline__ bool load_group(const InSpec& in, int col0, uint32_t 
 // MMA A bytes are 2^t * bit_j for k-block r = 2s + t (the packed word pre-shifted by 2s), so the B
 // operand carries Y_j = X_j * 2^(1-t) as two balanced int8 digits (planes = MMA columns 0, 1) and
 // every k-block contributes 2 * sum bit_j X_j alike.  Returns F and T = sum_j X_j.
-__device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t epoch, uint8_t* xs,
+__device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t epoch, uint8_t* xs, int kb_stride,
                                                int& F_out, int& T_out) {
   const int lane = threadIdx.x & 31;
   float u[2][4], sc[2][4];
@@ -234,7 +243,7 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
     }
     const uint32_t lo = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
     const uint32_t hi = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
-    uint8_t* base = xs + kb * 64 + 4 * half + tig * 8;
+    uint8_t* base = xs + kb * kb_stride + 4 * half + tig * 8;
     *(uint32_t*)(base + 0) = lo ^ 0x80808080u;   // plane 0 -> MMA column 0 (lanes 0-3)
     *(uint32_t*)(base + 32) = hi ^ 0x80808080u;  // plane 1 -> MMA column 1 (lanes 4-7)
   }
@@ -245,13 +254,15 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
   T_out = ts;
 }
 
+template <int NB>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program prog, int ring_slots) {
+  constexpr int kChunkQ = kChunkQBytes1 * NB, kPartFloats = kPartFloats1 * NB;
   extern __shared__ __align__(128) uint8_t smem[];
   Smem sm;
   sm.ring = smem;
   sm.hdr = (dbf_engine_run*)(sm.ring + (size_t)ring_slots * kSlotBytes);
   sm.xs = (uint8_t*)(sm.hdr + kMaxSlots);
-  sm.part = (float*)(sm.xs + kWarps * kXsBytes);
+  sm.part = (float*)(sm.xs + kWarps * xs_bytes<NB>());
   sm.full = (uint64_t*)(sm.part + 2 * kPartFloats);
   sm.empty = sm.full + kMaxSlots;
 
@@ -302,13 +313,15 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 
   // ---------------- compute warps -------------------------------------------------------------
   const int g = lane >> 2, tig = lane & 3;
-  uint8_t* xs = sm.xs + warp * kXsBytes;
-  const int xlane = ((lane >> 2) & 1) * 32 + (lane & 3) * 8;  // this lane's B fragment in a k-block
+  const int batch = prog.batch < 1 ? 1 : prog.batch;  // tokens present (<= NB)
+  uint8_t* xs = sm.xs + warp * xs_bytes<NB>();
+  // this lane's B fragment in a k-block: column g = 2*token + plane (columns >= 2*NB mirror)
+  const int xlane = ((lane >> 2) % (2 * NB)) * 32 + (lane & 3) * 8;
   // the quantized chunks stay valid for the next run when it reads the same vector with the same
   // input scale (a stage's units split over several runs of one CTA)
   int cur_vec = -1;
   const void* cur_iscale = nullptr;
-  int qF[2] = {0, 0}, qT[2] = {0, 0};
+  int qF[xs_chunks<NB>()][NB], qT[xs_chunks<NB>()][NB];
   int P = 0;  // ring pieces consumed before the current run
   for (int i = r0; i < r1; ++i) {
     const int j = i - r0, buf = j & 1;
@@ -326,8 +339,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     in.dtype = H.in_dtype;
     in.sdt = H.scale_dtype;
     in.cols = cols;
+    in.tstride = in.kind == 1 ? (int64_t)((cols + kChunkCols - 1) / kChunkCols) * kChunkCols : cols;
     // finalize fields (the record's ring slot is recycled once the run is released)
     const int rows = H.rows, rb = H.rb, odt = H.out_dtype;
+    const int64_t out_ll_stride = (int64_t)((rows + kChunkCols - 1) / kChunkCols) * kChunkCols;
     const void* oscale = H.oscale;
     void* out_plain = H.out_plain;
     uint32_t* ll_out = (uint32_t*)H.ll_out;
@@ -335,50 +350,56 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     const int nch = (cols + kChunkCols - 1) / kChunkCols;
     const int npieces = (nunits * nch * kChunkBytes + kSlotBytes - 1) / kSlotBytes;
     const uint32_t ep_in = H.in_kind == 1 ? epoch16(run_ctr, prog.nvectors, H.in_vec) : 0u;
-    int64_t* dbg = (prog.trace && prog.pad && blockIdx.x == 0 && lane == 0) ? prog.trace + prog.pad + (j * kWarps + warp) * 4 : nullptr;
-    if (dbg) dbg[0] = clock64();
-    int nwait = 0;
-    float acc0[kMaxUnits], acc1[kMaxUnits];  // rows g and g+8 of each unit (lanes with tig == 0)
+    float acc0[kMaxUnits], acc1[kMaxUnits];  // rows g, g+8 of each unit for token tig (tig < NB)
 #pragma unroll
     for (int u = 0; u < kMaxUnits; ++u) acc0[u] = acc1[u] = 0.f;
     // all of the run's signs are resident before the MMA loop (no waits inside it, so the
     // compiler can interleave the units' loads and MMAs)
-    {
-      long long tw = dbg ? clock64() : 0;
-      for (int p = 1; p < npieces; ++p) {
-        int sl = slot0 + p;
-        uint32_t ph = phase0;
-        if (sl >= ring_slots) { sl -= ring_slots; ph ^= 1u; }
-        mbar_wait(&sm.full[sl], ph);
-      }
-      if (dbg) nwait = (int)(clock64() - tw);
+    for (int p = 1; p < npieces; ++p) {
+      int sl = slot0 + p;
+      uint32_t ph = phase0;
+      if (sl >= ring_slots) { sl -= ring_slots; ph ^= 1u; }
+      mbar_wait(&sm.full[sl], ph);
     }
     const float osc = (oscale && warp < nunits && lane < 16 && (rb + warp) * 16 + lane < rows)
                           ? ld_scale(oscale, in.sdt, (rb + warp) * 16 + lane)
                           : 1.f;
-    const bool reuse = in.kind >= 0 && H.in_vec == cur_vec && in.iscale == cur_iscale && nch <= 2 * kWarps;
-    cur_vec = nch <= 2 * kWarps ? H.in_vec : -1;
+    constexpr int kReuseChunks = xs_chunks<NB>() * kWarps;
+    const bool reuse = H.in_vec == cur_vec && in.iscale == cur_iscale && nch <= kReuseChunks;
+    cur_vec = nch <= kReuseChunks ? H.in_vec : -1;
     cur_iscale = in.iscale;
     bool first = true;
     for (int c = warp; c < nch; c += kWarps) {
-      int F, T;
-      const int qs = (c / kWarps) & 1;
-      uint8_t* xq = xs + qs * kChunkQBytes;
+      const int qs = (c / kWarps) % xs_chunks<NB>();
+      uint8_t* xq = xs + qs * kChunkQ;
+      int F[NB], T[NB];
       if (reuse) {
-        F = qF[qs];
-        T = qT[qs];
+#pragma unroll
+        for (int t = 0; t < NB; ++t) F[t] = qF[qs][t], T[t] = qT[qs][t];
       } else {
-        quantize_chunk(in, c, ep_in, xq, F, T);
-        qF[qs] = F;
-        qT[qs] = T;
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+          if (t < batch) {
+            quantize_chunk(token_of(in, t), c, ep_in, xq + t * 64, NB * 64, F[t], T[t]);
+          } else {  // absent token: zero digits
+            for (int e = lane; e < 8 * 16; e += 32)
+              *(uint32_t*)(xq + (e >> 4) * NB * 64 + t * 64 + (e & 15) * 4) = 0u;
+            __syncwarp();
+            F[t] = 0, T[t] = 0;
+          }
+          qF[qs][t] = F[t], qT[qs][t] = T[t];
+        }
       }
       if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
-      if (dbg && first) dbg[1] = clock64();
       uint2 b[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * 64 + xlane);
-      const float inv = __int_as_float((127 - F) << 23);  // 2^-F  (|F| <= 125)
+      for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * NB * 64 + xlane);
+      // this lane's token tig: its chunk exponent and quantized sum
+      int Ft = F[0], Tt = T[0];
 #pragma unroll
+      for (int t = 1; t < NB; ++t)
+        if (tig == t) Ft = F[t], Tt = T[t];
+      const float inv = __int_as_float((127 - Ft) << 23);  // 2^-F  (|F| <= 125)
       // units in pairs: two independent MMA streams per warp (the second repeats the last unit
       // when nunits is odd and is then discarded)
 #pragma unroll
@@ -408,13 +429,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         float v[2][2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          // columns 0, 1 (planes) of rows g, g+8 live in lanes tig == 0: s = 2 * sum bit X
+          // columns 2*tig, 2*tig+1 (token tig's digit planes) of rows g, g+8: s = 2 * sum bit X
           const int s0 = (ac[h][0][0] + ac[h][1][0]) + (ac[h][2][0] + ac[h][3][0]);
           const int s1 = (ac[h][0][1] + ac[h][1][1]) + (ac[h][2][1] + ac[h][3][1]);
           const int s2 = (ac[h][0][2] + ac[h][1][2]) + (ac[h][2][2] + ac[h][3][2]);
           const int s3 = (ac[h][0][3] + ac[h][1][3]) + (ac[h][2][3] + ac[h][3][3]);
-          v[h][0] = (float)(s0 + 256 * s1 - T) * inv;
-          v[h][1] = (float)(s2 + 256 * s3 - T) * inv;
+          v[h][0] = (float)(s0 + 256 * s1 - Tt) * inv;
+          v[h][1] = (float)(s2 + 256 * s3 - Tt) * inv;
         }
         acc0[u0] += v[0][0];
         acc1[u0] += v[0][1];
@@ -426,15 +447,15 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       first = false;
     }
     if (tr && warp == 0 && lane == 0) tr[2] = gtimer();
-    if (dbg) { dbg[2] = clock64(); dbg[3] = nwait; }
     // partials -> shared memory (double-buffered by run parity), then the compute warps meet once
     float* part = sm.part + buf * kPartFloats;
-    if (tig == 0) {
+    if (tig < NB) {
 #pragma unroll
       for (int u = 0; u < kMaxUnits; ++u) {
         if (u < nunits) {
-          part[(warp * kMaxUnits + u) * 16 + g] = acc0[u];
-          part[(warp * kMaxUnits + u) * 16 + g + 8] = acc1[u];
+          float* pu = part + ((warp * kMaxUnits + u) * NB + tig) * 16;
+          pu[g] = acc0[u];
+          pu[g + 8] = acc1[u];
         }
       }
     }
@@ -445,19 +466,25 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         if (sl >= ring_slots) sl -= ring_slots;
         mbar_arrive(&sm.empty[sl]);
       }
-    // warp u finalizes unit u: sum the 16 warps' partials in warp order (deterministic), scale, publish
-    if (warp < nunits && lane < 16) {
-      const int row = (rb + warp) * 16 + lane;
-      if (row < rows) {
-        float v = 0.f;
+    // warp u finalizes unit u: sum the 16 warps' partials in warp order (deterministic), scale,
+    // publish; lanes 0-15 / 16-31 take one token each per pass
+    const float osc_row = __shfl_sync(0xffffffffu, osc, lane & 15);
+    if (warp < nunits) {
+      const int row = (rb + warp) * 16 + (lane & 15);
 #pragma unroll
-        for (int w2 = 0; w2 < kWarps; ++w2) v += part[(w2 * kMaxUnits + warp) * 16 + lane];
-        v *= osc;
-        const __half h = __float2half_rn(v);
-        if (ll_out) st_ll16(ll_out + row, h, ep_out);
-        if (out_plain) {
-          if (odt == DBF_F16) ((__half*)out_plain)[row] = h;
-          else ((float*)out_plain)[row] = __half2float(h);
+      for (int t0 = 0; t0 < NB; t0 += 2) {
+        const int t = t0 + (lane >> 4);
+        if (t < NB && t < batch && row < rows) {
+          float v = 0.f;
+#pragma unroll
+          for (int w2 = 0; w2 < kWarps; ++w2) v += part[((w2 * kMaxUnits + warp) * NB + t) * 16 + (lane & 15)];
+          v *= osc_row;
+          const __half h = __float2half_rn(v);
+          if (ll_out) st_ll16(ll_out + t * out_ll_stride + row, h, ep_out);
+          if (out_plain) {
+            if (odt == DBF_F16) ((__half*)out_plain)[(int64_t)t * rows + row] = h;
+            else ((float*)out_plain)[(int64_t)t * rows + row] = __half2float(h);
+          }
         }
       }
     }
@@ -468,10 +495,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 
 __global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; }
 
-constexpr size_t kFixedSmem = kMaxSlots * sizeof(dbf_engine_run) + kWarps * kXsBytes + 2 * kPartFloats * 4 +
-                              2 * kMaxSlots * 8 + 4 * 4 + 128;
-int ring_slots() { return std::min((int)((kMaxSmem - kFixedSmem) / kSlotBytes), kMaxSlots); }
-size_t smem_bytes(int slots) { return (size_t)slots * kSlotBytes + kFixedSmem; }
+inline size_t fixed_smem(int nb) {
+  const int xs = (nb <= 2 ? 2 : 1) * kChunkQBytes1 * nb;
+  return kMaxSlots * sizeof(dbf_engine_run) + (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 +
+         2 * kMaxSlots * 8 + 128;
+}
+inline int ring_slots(int nb = 1) { return std::min((int)((kMaxSmem - fixed_smem(nb)) / kSlotBytes), kMaxSlots); }
+inline size_t smem_bytes(int slots, int nb = 1) { return (size_t)slots * kSlotBytes + fixed_smem(nb); }
+inline int nb_for(int batch) { return batch <= 1 ? 1 : (batch <= 2 ? 2 : 4); }
 
 }  // namespace engine
 }  // namespace dbf
@@ -482,7 +513,7 @@ static_assert(sizeof(dbf_engine_run) == 128, "run record must be 128 bytes");
 
 extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t nsegments,
                                      const dbf_engine_vector* vectors, int32_t nvectors, const int32_t* runs,
-                                     int32_t nruns, uint32_t* ready, dbf_engine_run* out) {
+                                     int32_t nruns, int32_t batch, uint32_t* ready, dbf_engine_run* out) {
   if (!segments || !vectors || !runs || !out || nsegments < 1 || nvectors < 1 || nruns < 0)
     return DBF_ERR_INVALID_ARGUMENT;
   // units producing each vector (one segment writes each LL vector)
@@ -503,7 +534,8 @@ extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t
     if ((int64_t)(rb + n) * kRowBlock > (int64_t)((g.rows + kRowBlock - 1) / kRowBlock) * kRowBlock)
       return DBF_ERR_SHAPE;
     if (n > engine::kMaxUnits ||
-        (int64_t)n * chunks(g.cols) * kChunkBytes > (int64_t)(engine::ring_slots() / 2) * engine::kSlotBytes)
+        (int64_t)n * chunks(g.cols) * kChunkBytes >
+            (int64_t)(engine::ring_slots(engine::nb_for(batch)) / 2) * engine::kSlotBytes)
       return DBF_ERR_SHAPE;  // split longer runs (dbf_engine_run_limits)
     const dbf_engine_vector& vin = vectors[g.in_vec];
     if (vin.len != g.cols) return DBF_ERR_SHAPE;
@@ -535,59 +567,61 @@ extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t
   return DBF_OK;
 }
 
-extern "C" int dbf_engine_smem_bytes(int32_t max_cols, size_t* bytes) {
-  if (max_cols < 1 || !bytes) return DBF_ERR_INVALID_ARGUMENT;
-  const int slots = engine::ring_slots();
-  // one 16-row unit of the widest segment must fit the ring with a slot to spare
-  if (slots < engine::kMinSlots || chunks(max_cols) * kChunkBytes > (int64_t)(slots - 1) * engine::kSlotBytes)
+extern "C" int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* bytes) {
+  if (max_cols < 1 || !bytes || batch < 1 || batch > 4) return DBF_ERR_INVALID_ARGUMENT;
+  const int nb = engine::nb_for(batch);
+  const int slots = engine::ring_slots(nb);
+  // one 16-row unit of the widest segment must fit half the ring
+  if (slots < engine::kMinSlots || chunks(max_cols) * kChunkBytes > (int64_t)(slots / 2) * engine::kSlotBytes)
     return DBF_ERR_UNSUPPORTED;
-  *bytes = engine::smem_bytes(slots);
+  *bytes = engine::smem_bytes(slots, nb);
   return DBF_OK;
 }
 
-extern "C" int dbf_engine_run_limits(int32_t* max_units, int64_t* max_run_bytes) {
-  if (!max_units || !max_run_bytes) return DBF_ERR_INVALID_ARGUMENT;
+extern "C" int dbf_engine_run_limits(int32_t batch, int32_t* max_units, int64_t* max_run_bytes) {
+  if (!max_units || !max_run_bytes || batch < 1 || batch > 4) return DBF_ERR_INVALID_ARGUMENT;
   *max_units = engine::kMaxUnits;
   // a run's signs stay resident until every compute warp is done with it; leave room to prefetch
-  *max_run_bytes = (int64_t)(engine::ring_slots() / 2) * engine::kSlotBytes;
+  *max_run_bytes = (int64_t)(engine::ring_slots(engine::nb_for(batch)) / 2) * engine::kSlotBytes;
+  return DBF_OK;
+}
+
+template <typename K>
+static int engine_occupancy_of(K kern, size_t smem, int32_t* blocks_per_sm, int32_t* regs_per_thread) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, engine::kMaxSmem);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  *regs_per_thread = fa.numRegs;
+  int nb = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, engine::kThreads, smem);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  *blocks_per_sm = nb;
   return DBF_OK;
 }
 
 extern "C" int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, int32_t* regs_per_thread) {
   if (!blocks_per_sm || !regs_per_thread || max_cols < 1) return DBF_ERR_INVALID_ARGUMENT;
   size_t smem = 0;
-  int st = dbf_engine_smem_bytes(max_cols, &smem);
+  int st = dbf_engine_smem_bytes(max_cols, 1, &smem);
   if (st != DBF_OK) return st;
-  cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       engine::kMaxSmem);
-  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
-  cudaFuncAttributes fa;
-  e = cudaFuncGetAttributes(&fa, engine::engine_kernel);
-  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
-  *regs_per_thread = fa.numRegs;
-  int nb = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, engine::engine_kernel, engine::kThreads, smem);
-  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
-  *blocks_per_sm = nb;
-  return DBF_OK;
+  return engine_occupancy_of(engine::engine_kernel<1>, smem, blocks_per_sm, regs_per_thread);
 }
 
-extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream) {
-  if (!program || !program->runs || !program->cta_offsets || !program->run_counter || program->grid < 1 ||
-      program->max_cols < 1)
-    return DBF_ERR_INVALID_ARGUMENT;
+template <int NB>
+static int engine_launch_nb(const dbf_engine_program* program, cudaStream_t s) {
   size_t smem = 0;
-  int st = dbf_engine_smem_bytes(program->max_cols, &smem);
+  int st = dbf_engine_smem_bytes(program->max_cols, NB, &smem);
   if (st != DBF_OK) return st;
-  const int slots = engine::ring_slots();
+  const int slots = engine::ring_slots(NB);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          engine::kMaxSmem);
     if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
     configured = true;
   }
-  cudaStream_t s = (cudaStream_t)stream;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(program->grid);
   cfg.blockDim = dim3(engine::kThreads);
@@ -599,8 +633,20 @@ extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   dbf_engine_program prog = *program;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, engine::engine_kernel, prog, slots);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, engine::engine_kernel<NB>, prog, slots);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  return DBF_OK;
+}
+
+extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream) {
+  if (!program || !program->runs || !program->cta_offsets || !program->run_counter || program->grid < 1 ||
+      program->max_cols < 1 || program->batch < 1 || program->batch > 4)
+    return DBF_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = engine::nb_for(program->batch);
+  const int st = nb == 1 ? engine_launch_nb<1>(program, s)
+                         : (nb == 2 ? engine_launch_nb<2>(program, s) : engine_launch_nb<4>(program, s));
+  if (st != DBF_OK) return st;
   engine::advance_run_kernel<<<1, 1, 0, s>>>(program->run_counter);
   return check_launch();
 }

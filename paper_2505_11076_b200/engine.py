@@ -51,17 +51,18 @@ class _Program(ctypes.Structure):
         ("nvectors", ctypes.c_int32),
         ("grid", ctypes.c_int32),
         ("max_cols", ctypes.c_int32),
-        ("pad", ctypes.c_int32),
+        ("batch", ctypes.c_int32),
     ]
 
 
 _lib.lib.dbf_engine_smem_bytes.restype = ctypes.c_int
-_lib.lib.dbf_engine_smem_bytes.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
+_lib.lib.dbf_engine_smem_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
 _lib.lib.dbf_engine_occupancy.restype = ctypes.c_int
 _lib.lib.dbf_engine_occupancy.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
 _lib.lib.dbf_engine_build_runs.restype = ctypes.c_int
 _lib.lib.dbf_engine_build_runs.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32,
-                                           ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+                                           ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                                           ctypes.c_void_p]
 _lib.lib.dbf_engine_launch.restype = ctypes.c_int
 _lib.lib.dbf_engine_launch.argtypes = [ctypes.POINTER(_Program), ctypes.c_void_p]
 
@@ -73,10 +74,10 @@ def occupancy(max_cols: int) -> tuple[int, int]:
     return b.value, r.value
 
 
-def run_limits() -> tuple[int, int]:
-    """(units per run, packed-sign bytes per run) the engine accepts."""
+def run_limits(batch: int = 1) -> tuple[int, int]:
+    """(units per run, packed-sign bytes per run) the engine accepts at this batch."""
     u, b = ctypes.c_int32(0), ctypes.c_int64(0)
-    _lib.check(_lib.lib.dbf_engine_run_limits(ctypes.byref(u), ctypes.byref(b)), "dbf_engine_run_limits")
+    _lib.check(_lib.lib.dbf_engine_run_limits(batch, ctypes.byref(u), ctypes.byref(b)), "dbf_engine_run_limits")
     return u.value, b.value
 
 
@@ -113,8 +114,9 @@ class EngineProgram:
         self.grid = int(grid or props.multi_processor_count)
         dev = torch.device(device)
         act = plan.buffers[plan.input_buffer]
-        if act.shape[0] != 1:
-            raise ValueError("the decode engine currently runs batch 1 (use forward_device for batches)")
+        self.batch = int(act.shape[0])
+        if not 1 <= self.batch <= 4:
+            raise ValueError("the decode engine runs 1..4 tokens per step (use forward_device for larger batches)")
         act_code = _lib.dtype_code(act.dtype)
         if act_code not in (_lib.F16, _lib.F32):
             raise ValueError("engine activations must be float16 or float32")
@@ -124,8 +126,9 @@ class EngineProgram:
         self._keep = []
 
         def ll_vector(length: int) -> int:
-            # uint32 {fp16, epoch16} words, padded to whole 256-column chunks (the kernel reads them)
-            t = torch.zeros(((length + 255) // 256) * 256, dtype=torch.int32, device=dev)
+            # uint32 {fp16, epoch16} words, padded to whole 256-column chunks (the kernel reads them),
+            # one padded row per token
+            t = torch.zeros(self.batch * (((length + 255) // 256) * 256), dtype=torch.int32, device=dev)
             self._keep.append(t)
             vecs.append((t.data_ptr(), length, 1, 0))
             return len(vecs) - 1
@@ -171,7 +174,7 @@ class EngineProgram:
             rot = (rot + len(units)) % self.grid
         # compress each CTA's unit list into runs: consecutive row blocks of one segment, at most
         # max_units units / max_run_bytes of packed signs each (dbf_engine_run_limits)
-        max_units, max_bytes = run_limits()
+        max_units, max_bytes = run_limits(self.batch)
         unit_bytes = {j: ((sg[2] + 255) // 256) * 512 for j, sg in enumerate(segs)}
         per_cta_runs: list[list[tuple[int, int, int]]] = []
         for lst in per_cta:
@@ -210,7 +213,7 @@ class EngineProgram:
         _lib.check(
             _lib.lib.dbf_engine_build_runs(
                 seg_arr.ctypes.data, len(segs), vec_arr.ctypes.data, len(vecs), flat.ctypes.data, len(flat),
-                self.ready.data_ptr(), records.ctypes.data,
+                self.batch, self.ready.data_ptr(), records.ctypes.data,
             ),
             "dbf_engine_build_runs",
         )
@@ -226,12 +229,12 @@ class EngineProgram:
         self.nsegments = len(segs)
         self._prog = _Program(
             dev_bytes(records), dev_bytes(offsets), self.run_counter.data_ptr(), None,
-            len(vecs), self.grid, self.max_cols, 0,
+            len(vecs), self.grid, self.max_cols, self.batch,
         )
         self._offsets = offsets
         self._flat = flat
         size = ctypes.c_size_t(0)
-        _lib.check(_lib.lib.dbf_engine_smem_bytes(self.max_cols, ctypes.byref(size)), "dbf_engine_smem_bytes")
+        _lib.check(_lib.lib.dbf_engine_smem_bytes(self.max_cols, self.batch, ctypes.byref(size)), "dbf_engine_smem_bytes")
         self.smem_bytes = size.value
 
     def enable_trace(self):

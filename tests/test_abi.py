@@ -53,8 +53,10 @@ def test_invalid_arguments_are_rejected_without_a_gpu():
     assert L.dbf_tile_signs(None, 1, 1, 4, None, None) == _lib.ERR_INVALID_ARGUMENT
     assert L.dbf_forward_workspace_bytes(4096, 4096, 4096, 2) >= 2 * 4096 * 4
     size = ctypes.c_size_t(0)
-    assert L.dbf_engine_smem_bytes(11008, ctypes.byref(size)) == 0 and 200_000 < size.value <= 227 * 1024
-    assert L.dbf_engine_smem_bytes(10**7, ctypes.byref(size)) == _lib.ERR_UNSUPPORTED
+    assert L.dbf_engine_smem_bytes(11008, 1, ctypes.byref(size)) == 0 and 200_000 < size.value <= 227 * 1024
+    assert L.dbf_engine_smem_bytes(11008, 4, ctypes.byref(size)) == 0 and size.value <= 227 * 1024
+    assert L.dbf_engine_smem_bytes(10**7, 1, ctypes.byref(size)) == _lib.ERR_UNSUPPORTED
+    assert L.dbf_engine_smem_bytes(4096, 5, ctypes.byref(size)) == _lib.ERR_INVALID_ARGUMENT
 
 
 def test_engine_run_records_resolve_everything_on_the_host():
@@ -71,7 +73,7 @@ def test_engine_run_records_resolve_everything_on_the_host():
     runs = np.array([[0, 0, 3], [1, 2, 3]], dtype=np.int32)
     out = np.zeros(2 * 128, dtype=np.uint8)
     ready = 0x7000
-    st = _lib.lib.dbf_engine_build_runs(segs.ctypes.data, 2, vecs.ctypes.data, 3, runs.ctypes.data, 2, ready, out.ctypes.data)
+    st = _lib.lib.dbf_engine_build_runs(segs.ctypes.data, 2, vecs.ctypes.data, 3, runs.ctypes.data, 2, 1, ready, out.ctypes.data)
     assert st == 0
     q = out.view(np.uint64)
     i32 = out.view(np.int32)
@@ -83,4 +85,4 @@ def test_engine_run_records_resolve_everything_on_the_host():
     assert r1[0] == 0x9000 + 2 * 1 * 512 and r1[4] == 0x5000 and r1[6] == ready + 4 and r1[7] == ready + 8
     assert i32[32 + 27] == 3  # in_producers of vec1 = ceil(40/16) units of segment 0
     bad = np.array([[1, 4, 2]], dtype=np.int32)  # rows 64..95 of a 70-row segment: out of range
-    assert _lib.lib.dbf_engine_build_runs(segs.ctypes.data, 2, vecs.ctypes.data, 3, bad.ctypes.data, 1, ready, out.ctypes.data) == _lib.ERR_SHAPE
+    assert _lib.lib.dbf_engine_build_runs(segs.ctypes.data, 2, vecs.ctypes.data, 3, bad.ctypes.data, 1, 1, ready, out.ctypes.data) == _lib.ERR_SHAPE

@@ -83,3 +83,26 @@ def test_engine_single_layer_vs_oracle(n, k, m):
     ref = oracle.c_forward(bufs[0].double().cpu().numpy(), layer.a.double().cpu().numpy(), layer.A.to_host().bits,
                            layer.mid.double().cpu().numpy(), layer.B.to_host().bits, layer.b.double().cpu().numpy())
     assert rel_max(y, ref) <= TOL and rel_norm(y, ref) <= TOL, (rel_max(y, ref), rel_norm(y, ref))
+
+
+@pytest.mark.parametrize("batch", [2, 3, 4])
+def test_batched_engine_matches_layer_chain(batch):
+    """1..4 tokens per step share every tensor-core MMA (B columns = 2*token + digit plane); each
+    token matches the per-layer chain and is independent of the others and of the grid."""
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(40 + batch)
+    plan = llama_decode_plan("llama2-7b", bpw=2.0, batch=batch, blocks=1, generator=g)
+    x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
+    ref = _run(plan.use_layer_kernels(), x)
+    out = _run(plan.use_engine(grid=148), x)
+    for t in range(batch):
+        ok, err = _close(out[t:t + 1], ref[t:t + 1])
+        assert ok, (t, err)
+    assert torch.equal(_run(plan.use_engine(grid=37), x), out)
+    # token 0 alone through a batch-1 engine: the same numbers (tokens do not interact)
+    g1 = torch.Generator(device="cuda")
+    g1.manual_seed(40 + batch)
+    plan1 = llama_decode_plan("llama2-7b", bpw=2.0, batch=1, blocks=1, generator=g1).use_engine(grid=148)
+    assert torch.equal(_run(plan1, x[:1]), out[:1])

@@ -38,6 +38,10 @@ constexpr int kProdWarp = kWarps;             // producer warp index
 constexpr int kThreads = (kWarps + 1) * 32;
 constexpr int kSlotBytes = 16384;             // one ring slot = 32 chunks of 512 B
 constexpr int kMaxUnits = 8;                  // units per run (the host splits longer runs)
+#ifndef DBF_POLL_NS
+#define DBF_POLL_NS 32
+#endif
+constexpr int kPollSleepNs = DBF_POLL_NS;     // back-off between LL polls of a not-yet-published chunk
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMinSlots = 4;
 constexpr int kMaxSlots = 16;
@@ -207,7 +211,7 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
     const bool ok0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
     const bool ok1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
     if (__all_sync(0xffffffffu, ok0 && ok1)) break;
-    __nanosleep(32);
+    if (kPollSleepNs) __nanosleep(kPollSleepNs);
   }
   float mx = 0.f;
 #pragma unroll

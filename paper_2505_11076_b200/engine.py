@@ -92,13 +92,44 @@ def levels_of(ops, input_buffer: int) -> list[int]:
     return lv
 
 
-def distribute(units: list[tuple[int, int]], grid: int, rotate: int) -> list[list[tuple[int, int]]]:
-    """Block distribution of a stage's units over CTAs, starting at CTA `rotate`."""
+def distribute(units: list[tuple[int, int]], grid: int, rotate: int,
+               unit_bytes: dict | None = None) -> list[list[tuple[int, int]]]:
+    """Distribution of a stage's units over CTAs, starting at CTA `rotate`.
+
+    A stage with several segments (q/k/v, gate/up) gives every segment its own set of CTAs, sized
+    in proportion to the segment's bytes, and block-distributes each segment's units over its set:
+    no CTA then holds units of two segments, which would make it run two runs back to back and
+    finish the stage last.  A single segment (or more segments than CTAs) is block-distributed."""
     out: list[list[tuple[int, int]]] = [[] for _ in range(grid)]
-    n = len(units)
-    for c in range(grid):
-        lo, hi = (c * n) // grid, ((c + 1) * n) // grid
-        out[(c + rotate) % grid].extend(units[lo:hi])
+    segs: dict[int, list[tuple[int, int]]] = {}
+    for u in units:
+        segs.setdefault(u[0], []).append(u)
+    if len(segs) == 1 or len(segs) > grid:
+        n = len(units)
+        for c in range(grid):
+            lo, hi = (c * n) // grid, ((c + 1) * n) // grid
+            out[(c + rotate) % grid].extend(units[lo:hi])
+        return out
+    order = list(segs)
+    weight = [len(segs[sg]) * ((unit_bytes or {}).get(sg, 1)) for sg in order]
+    total = float(sum(weight))
+    # largest-remainder apportionment of the CTAs, at least one per segment
+    quota = [max(1.0, grid * w / total) for w in weight]
+    counts = [max(1, int(q)) for q in quota]
+    while sum(counts) > grid:
+        i = max(range(len(counts)), key=lambda j: (counts[j] - quota[j], counts[j]))
+        counts[i] -= 1
+    while sum(counts) < grid:
+        i = max(range(len(counts)), key=lambda j: quota[j] - counts[j])
+        counts[i] += 1
+    base = 0
+    for sg, cnt in zip(order, counts):
+        lst = segs[sg]
+        n = len(lst)
+        for c in range(cnt):
+            lo, hi = (c * n) // cnt, ((c + 1) * n) // cnt
+            out[(base + c + rotate) % grid].extend(lst[lo:hi])
+        base += cnt
     return out
 
 
@@ -165,11 +196,12 @@ class EngineProgram:
             for stage, seg_idx, rows in ((2 * lv[i], len(segs) - 2, layer.k), (2 * lv[i] + 1, len(segs) - 1, layer.n)):
                 stage_units.setdefault(stage, []).extend((seg_idx, rb) for rb in range((rows + 15) // 16))
 
+        seg_unit_bytes = {j: ((sg[2] + 255) // 256) * 512 for j, sg in enumerate(segs)}
         per_cta: list[list[tuple[int, int]]] = [[] for _ in range(self.grid)]
         rot = 0
         for stage in sorted(stage_units):
             units = stage_units[stage]
-            for c, lst in enumerate(distribute(units, self.grid, rot)):
+            for c, lst in enumerate(distribute(units, self.grid, rot, seg_unit_bytes)):
                 per_cta[c].extend(lst)
             rot = (rot + len(units)) % self.grid
         # compress each CTA's unit list into runs: consecutive row blocks of one segment, at most

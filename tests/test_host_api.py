@@ -126,3 +126,17 @@ def test_slice_columns_matches_numpy(rng):
     bits = _bits(M)
     for c0, c1 in [(0, 32), (32, 300), (64, 100), (296, 300), (0, 300)]:
         assert np.array_equal(sharded.slice_columns(bits, 300, c0, c1), _bits(M[:, c0:c1]))
+
+
+@pytest.mark.parametrize("grid,rot", [(148, 0), (148, 77), (64, 3), (7, 2)])
+def test_multi_segment_stage_gives_each_cta_one_segment(grid, rot):
+    # q/k/v of a 7B block: three segments of 256 units, equal bytes
+    units = [(s, i) for s in range(3) for i in range(256)]
+    per = distribute(units, grid, rot, {0: 8192, 1: 8192, 2: 8192})
+    assert sorted(u for lst in per for u in lst) == sorted(units)
+    for lst in per:
+        assert len({u[0] for u in lst}) <= 1  # never two segments on one CTA
+        rbs = [u[1] for u in lst]
+        assert rbs == list(range(rbs[0], rbs[0] + len(rbs))) if rbs else True
+    sizes = [len(x) for x in per]
+    assert max(sizes) <= -(-256 // (grid // 3))  # each segment spread over its share of the CTAs

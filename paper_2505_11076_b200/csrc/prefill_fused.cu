@@ -27,9 +27,9 @@ namespace prefill_fused {
 using namespace sm100;
 
 constexpr int BM = 128, BN = 256, BK = 64, UK = 16;
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 6;
 constexpr int kActStageBytes = BN * BK * 2;   // 32 KB
-constexpr int kStageBytes = BN * BM * 2;      // 64 KB epilogue staging (fp16 [256 tokens][128 rows])
+constexpr int kStageBytes = BN / 2 * BM * 2;  // 32 KB epilogue staging (fp16 [128 tokens][128 rows]), 2 halves per tile
 constexpr int kAColsPerStage = BK / 2;
 constexpr int kACol0 = BN;
 constexpr int kTmemCols = 512;
@@ -292,35 +292,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rows = g1 ? p.k : p.n;
       const int grow = ti.rt * BM + r;
       const float rs = grow < rows ? __half2float((g1 ? p.mid : p.a)[grow]) : 0.f;
-      // the previous tile's TMA store must have read the staging buffer
-      if (threadIdx.x == kEpiWarp0 * 32) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
       if (lane == 0) mbar_wait_guarded(&bar.acc_full, j & 1);
       __syncwarp();
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t acc[32];
-        tmem_ld32(tmem + lane_addr + c * 32, acc);
-        tmem_wait_ld();
-        if (c == BN / 32 - 1) {  // accumulator drained: the next tile's MMAs may start
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bar.acc_empty);
-        }
+      for (int hh = 0; hh < 2; ++hh) {  // tokens [128*hh, 128*hh + 128) through the staging tile
+        // the previous store must have read the staging buffer
+        if (threadIdx.x == kEpiWarp0 * 32) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t acc[32];
+          tmem_ld32(tmem + lane_addr + hh * (BN / 2) + c * 32, acc);
+          tmem_wait_ld();
+          if (hh == 1 && c == BN / 64 - 1) {  // accumulator drained: the next tile's MMAs may start
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar.acc_empty);
+          }
 #pragma unroll
-        for (int e = 0; e < 32; ++e) st[(c * 32 + e) * BM + r] = __float2half_rn(__uint_as_float(acc[e]) * rs);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      if (threadIdx.x == kEpiWarp0 * 32) {
-        tma_store_2d(g1 ? &t_store : &y_store, st, ti.rt * BM, ti.tb * BN);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        if (g1) {  // publish t of this tile before counting it done (GEMM2 reads it via TMA)
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.done1 + ti.tb) : "memory");
+          for (int e = 0; e < 32; ++e) st[(c * 32 + e) * BM + r] = __float2half_rn(__uint_as_float(acc[e]) * rs);
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (threadIdx.x == kEpiWarp0 * 32) {
+          tma_store_2d(g1 ? &t_store : &y_store, st, ti.rt * BM, ti.tb * BN + hh * (BN / 2));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+      if (threadIdx.x == kEpiWarp0 * 32 && g1) {  // publish t of this tile before counting it done
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.done1 + ti.tb) : "memory");
       }
     }
     if (threadIdx.x == kEpiWarp0 * 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -408,7 +411,7 @@ int dbf_forward_prefill_fused(const uint32_t* A_paired, int64_t A_pitch, const u
   const size_t smem = fixed + (size_t)p.stages * kActStageBytes;
   CUtensorMap xm, tm, ts, ys;
   if (!make_map(&xm, X, m, tokens, ldx, BK, BN, true) || !make_map(&tm, t, k, tokens, ldt, BK, BN, true) ||
-      !make_map(&ts, t, k, tokens, ldt, BM, BN, false) || !make_map(&ys, Y, n, tokens, ldy, BM, BN, false))
+      !make_map(&ts, t, k, tokens, ldt, BM, BN / 2, false) || !make_map(&ys, Y, n, tokens, ldy, BM, BN / 2, false))
     return DBF_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(ctr, 0, 16 + (size_t)p.tbs * 4, s);

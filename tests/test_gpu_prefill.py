@@ -123,10 +123,15 @@ def test_fused_prefill_equals_two_launch_path(T, n, k, m):
     g.manual_seed(T + n)
     dl = P.random_device_layer(n, k, m, generator=g, keep_words=True)
     X = torch.randn((T, m), generator=g, device="cuda").half()
-    ref = P.forward_prefill(X, dl)
+    A, B = dl.A.paired, dl.B.paired
+    ref = torch.empty((T, n), dtype=torch.half, device="cuda")
+    ws2 = torch.empty(_lib.lib.dbf_prefill_workspace_bytes(k, T), dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib.dbf_forward_prefill(
+        A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], dl.a.data_ptr(), dl.mid.data_ptr(),
+        dl.b.data_ptr(), n, k, m, X.data_ptr(), T, m, ref.data_ptr(), n, ws2.data_ptr(), ws2.numel(),
+        _lib.stream_ptr()), "two-launch")
     Y = torch.empty_like(ref)
     ws = torch.empty(_lib.lib.dbf_prefill_fused_workspace_bytes(k, T), dtype=torch.uint8, device="cuda")
-    A, B = dl.A.paired, dl.B.paired
     for _ in range(2):  # the per-call counter reset makes repeated calls independent
         _lib.check(_lib.lib.dbf_forward_prefill_fused(
             A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], dl.a.data_ptr(), dl.mid.data_ptr(),

@@ -46,6 +46,8 @@ constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMinSlots = 4;
 constexpr int kMaxSlots = 16;
 // Per token of a batch (NB tokens share every MMA: B column n = 2*token + digit plane):
+constexpr float kQScale = 4079.f / 4096.f;    // keeps 8 * |X| below the two-digit limit 32640
+constexpr float kQInv = 4096.f / 4079.f;
 constexpr int kChunkQBytes1 = 8 * 64;         // one quantized chunk: 8 k-blocks x (2 planes x 4 lanes x 8 B)
 constexpr int kPartFloats1 = kWarps * kMaxUnits * 16;  // one partial buffer
 template <int NB> constexpr int xs_chunks() { return NB <= 2 ? 2 : 1; }  // chunks a warp keeps for reuse
@@ -195,10 +197,12 @@ __device__ __forceinline__ bool load_group(const InSpec& in, int col0, uint32_t 
 }
 
 // Quantize chunk c of the run's input (256 columns, warp-local) into this warp's B-fragment
-// scratch.  X_j = round(x_j * 2^F) on a 14-bit grid relative to the CHUNK max (|X| < 2^13); the
-// MMA A bytes are 2^t * bit_j for k-block r = 2s + t (the packed word pre-shifted by 2s), so the B
-// operand carries Y_j = X_j * 2^(1-t) as two balanced int8 digits (planes = MMA columns 0, 1) and
-// every k-block contributes 2 * sum bit_j X_j alike.  Returns F and T = sum_j X_j.
+// scratch.  X_j = round(x_j * 2^F * kQScale) on a 13-bit grid relative to the CHUNK max
+// (|X| <= 4079); the MMA A bytes are 2^t * bit_j for k-block r = 4s + t (the packed word
+// pre-shifted by 4s: one shift per word serves four k-blocks), so the B operand carries
+// Y_j = X_j * 2^(3-t) as two balanced int8 digits (planes = MMA columns 0, 1; |Y| < 32640 keeps
+// both digits in [-128, 127]) and every k-block contributes 8 * sum bit_j X_j alike.
+// Returns F and T = sum_j X_j.
 __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t epoch, uint8_t* xs, int kb_stride,
                                                int& F_out, int& T_out) {
   const int lane = threadIdx.x & 31;
@@ -227,17 +231,17 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
   int F = 0;
   if (mx > 0.f) {
     int e;
-    frexpf(mx, &e);  // mx in [2^(e-1), 2^e)  ->  |X| <= 2^13
-    F = 13 - e;
+    frexpf(mx, &e);  // mx in [2^(e-1), 2^e)  ->  |X| <= 4096 * kQScale <= 4079
+    F = 12 - e;
     F = F > 125 ? 125 : (F < -125 ? -125 : F);
   }
-  const float scale = __int_as_float((F + 127) << 23);
+  const float scale = __int_as_float((F + 127) << 23) * kQScale;
   int ts = 0;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int q = lane + 32 * h;
     const int kb = q >> 3, tig = q & 3, half = (q >> 2) & 1;
-    const int sh = 1 - (kb & 1);  // Y = X * 2^(1-t)
+    const int sh = 3 - (kb & 3);  // Y = X * 2^(3-t), |Y| <= 32632 < 32640 (two balanced digits)
     uint32_t v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 #pragma unroll
       for (int t = 1; t < NB; ++t)
         if (tig == t) Ft = F[t], Tt = T[t];
-      const float inv = __int_as_float((127 - Ft) << 23);  // 2^-F  (|F| <= 125)
+      const float inv = __int_as_float((127 - Ft) << 23) * kQInv;  // 1 / (2^F * kQScale)
       // units in pairs: two independent MMA streams per warp (the second repeats the last unit
       // when nunits is odd and is then discarded)
 #pragma unroll
@@ -422,9 +426,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         int ac[2][4][4] = {};  // per unit: four independent accumulator chains
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          // k-block r = 2s + t reads (word >> 2s) & (0x01010101 << t): A bytes 2^t * bit
-          const uint32_t m = 0x01010101u << (r & 1);
-          const int sh = 2 * (r >> 1);
+          // k-block r = 4s + t reads (word >> 4s) & (0x01010101 << t): A bytes 2^t * bit
+          const uint32_t m = 0x01010101u << (r & 3);
+          const int sh = 4 * (r >> 2);
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             imma(ac[h][r & 3], (w[h].x >> sh) & m, (w[h].y >> sh) & m, (w[h].z >> sh) & m, (w[h].w >> sh) & m,
@@ -433,13 +437,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         float v[2][2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          // columns 2*tig, 2*tig+1 (token tig's digit planes) of rows g, g+8: s = 2 * sum bit X
+          // columns 2*tig, 2*tig+1 (token tig's digit planes) of rows g, g+8: s = 8 * sum bit X
           const int s0 = (ac[h][0][0] + ac[h][1][0]) + (ac[h][2][0] + ac[h][3][0]);
           const int s1 = (ac[h][0][1] + ac[h][1][1]) + (ac[h][2][1] + ac[h][3][1]);
           const int s2 = (ac[h][0][2] + ac[h][1][2]) + (ac[h][2][2] + ac[h][3][2]);
           const int s3 = (ac[h][0][3] + ac[h][1][3]) + (ac[h][2][3] + ac[h][3][3]);
-          v[h][0] = (float)(s0 + 256 * s1 - Tt) * inv;
-          v[h][1] = (float)(s2 + 256 * s3 - Tt) * inv;
+          v[h][0] = (float)(((s0 + 256 * s1) >> 2) - Tt) * inv;
+          v[h][1] = (float)(((s2 + 256 * s3) >> 2) - Tt) * inv;
         }
         acc0[u0] += v[0][0];
         acc1[u0] += v[0][1];

@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--layer-kernels", action="store_true", help="per-layer GEMV kernels instead of the engine")
     return ap.parse_args()
@@ -355,6 +356,63 @@ def sweep_bench(steps: int):
     return rows
 
 
+def sharded_bench(world: int, rank: int, steps: int, warmup: int, barrier, dist=None):
+    """BASELINE configs[3]: the Llama-2-70B linears at 2 bpw with the middle dimension
+    k sharded over the `world` GPUs of the run (word-aligned uneven shards).  Per shape and batch:
+    the local partial alone, the NCCL path (partial -> NCCL all-reduce -> finalize) and the fused
+    path (dbf_forward_allreduce: partials pushed to every peer's symmetric-memory buffer from the
+    GEMV2 epilogue).  Each timing replays a CUDA graph over enough distinct layer instances to
+    exceed 2x L2; µs are per layer, max over ranks."""
+    import torch
+
+    import paper_2505_11076_b200 as P
+    from paper_2505_11076_b200 import sharded
+
+    shapes = [("q,o", 8192, 8192, 8192), ("k,v", 1024, 1792, 8192), ("gate,up", 28672, 12736, 8192),
+              ("down", 8192, 12736, 28672)]
+
+    def mx(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    rows = []
+    for batch in (1, 16):
+        for name, n, k, m in shapes:
+            k0, k1 = sharded.shard_bounds(k, world)[rank]
+            g = torch.Generator(device="cuda")
+            g.manual_seed(77 + 1000 * rank)
+            bytes_rank = (n * ((k1 - k0 + 7) // 8) + (k1 - k0) * ((m + 7) // 8) + 2 * (n + (k1 - k0) + m)
+                          + 2 * batch * (m + n))
+            inst = int(min(64, max(2, -(-260_000_000 // bytes_rank))))
+            shards = [sharded.DeviceShard.from_device_layer(P.random_device_layer(n, k1 - k0, m, generator=g),
+                                                            rank, world, k0) for _ in range(inst)]
+            gx = torch.Generator(device="cuda")
+            gx.manual_seed(5)  # x is replicated
+            X = torch.randn((batch, m), generator=gx, device="cuda").half()
+            ar = sharded.FusedAllReduce(n, batch)
+            y_n = shards[0].forward(X)
+            y_f = ar.forward(shards[0], X)
+            torch.cuda.synchronize()
+            diff = float(((y_f.float() - y_n.float()).abs().max() / y_n.float().abs().max().clamp_min(1e-30)).item())
+            g_p = graph_of(lambda: [s.partial(X) for s in shards])
+            g_n = graph_of(lambda: [s.forward(X) for s in shards])
+            g_f = graph_of(lambda: [ar.forward(s, X) for s in shards])
+            us = [mx(time_graph(gr, steps, warmup, barrier)) * 1e3 / inst for gr in (g_p, g_n, g_f)]
+            rows.append({"layer": name, "n": n, "k": k, "m": m, "batch": batch, "k_shard": [k0, k1],
+                         "instances": inst, "us_partial": us[0], "us_nccl_path": us[1], "us_fused": us[2],
+                         "us_allreduce_nccl": us[1] - us[0], "us_allreduce_fused": us[2] - us[0],
+                         "gbs_per_rank_fused": bytes_rank / (us[2] * 1e-6) / 1e9,
+                         "fused_vs_nccl_max_rel_diff": diff})
+            del g_p, g_n, g_f, shards, ar
+            torch.cuda.empty_cache()
+    return {"world": world, "model": "llama2-70b", "bpw": 2.0,
+            "note": "k-sharded layers, fp16 io; us per layer = max over ranks of graph time / instances",
+            "rows": rows}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -434,6 +492,14 @@ def main():
            "d2h_bytes_per_step": host_y.numel() * host_y.element_size(),
            "ms_per_step": ms_e2e, "api": "paper_2505_11076_b200.plan.DecodePlan.run-equivalent (pinned H2D, graph replay, D2H)"}
 
+    # ---- k-sharded 70B layers: NCCL all-reduce vs the all-reduce fused into GEMV2 (all ranks) ---
+    shard = None
+    if not args.no_sharded:
+        try:
+            shard = sharded_bench(world, rank, max(args.steps // 2, 5), 3, barrier, dist)
+        except Exception as e:  # noqa: BLE001 - report, keep the headline line
+            shard = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     # ---- cuBLAS fp16 GEMV over the same 224 shapes and dataflow -----------------------------
     cublas = None
     if not args.no_cublas:
@@ -508,6 +574,7 @@ def main():
             "e2e": e2e,
             "prefill": prefill,
             "sweep": sweep,
+            "sharded": shard,
             "gpu_launches": launches * args.steps,
             "clocks": clk,
         }

@@ -177,6 +177,32 @@ int dbf_finalize_partial(const float* P, const void* a, int scale_dtype, int64_t
                          void* Y, int y_dtype, int64_t ldy, void* stream);
 
 /*
+ * dbf_forward_allreduce -- the k-sharded layer with its all-reduce fused into GEMV2 (SURVEY §8e,
+ * step 2; replaces dbf_forward_partial + an NCCL all-reduce + dbf_finalize_partial, i.e. the
+ * reference's kernel.forward, kernel.py:48-62, computed across `world` GPUs).  Every rank calls
+ * it with the same n, batch and epoch.  GEMV2's epilogue stores each fp32 partial row block
+ * straight into slot `rank` of every peer's receive buffer (NVLink P2P stores through mapped peer
+ * addresses), then releases it with a per-(rank, row block) flag = epoch; each row block is then
+ * combined on every rank as soon as all ranks have released it:
+ *   Y[i, r] = a[r] * sum_{g = 0..world-1} P_g[i, r]   (rank order -> identical bits on all ranks)
+ * peer_recv / peer_flags: DEVICE arrays of `world` device addresses (uint64) of every rank's
+ * receive buffer (dbf_allreduce_recv_bytes) and flag array (dbf_allreduce_flag_bytes, zeroed
+ * once before the first call), e.g. from torch symmetric memory.  epoch_counter: a LOCAL device
+ * u32, zeroed with the flags; each call advances it on the device (so a captured CUDA graph
+ * replays correctly) and uses the new value as its epoch: receive buffers alternate by epoch
+ * parity and flags compare >= epoch, so nothing is cleared between calls.  batch <= 16.  A rank
+ * that waits more than 20 s for a peer traps.
+ */
+size_t dbf_allreduce_recv_bytes(int64_t n, int64_t batch, int world);
+size_t dbf_allreduce_flag_bytes(int64_t n, int world);
+int dbf_forward_allreduce(const void* A_shard_tiled, const void* B_shard_tiled, const void* a,
+                          const void* mid_shard, const void* b, int scale_dtype, int64_t n,
+                          int64_t k_shard, int64_t m, const void* X, int x_dtype, int64_t batch,
+                          int64_t ldx, void* Y, int y_dtype, int64_t ldy, const uint64_t* peer_recv,
+                          const uint64_t* peer_flags, int world, int rank, uint32_t* epoch_counter,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Ablation kernel (north_star wording): the classic CUDA-core decode that XORs the fp16 sign
  * bit of x with the packed sign and accumulates with HADD2.  Same semantics as
  * dbf_sign_matvec for batch 1 but reads the canonical layout; kept only to measure against the

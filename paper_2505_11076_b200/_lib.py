@@ -56,6 +56,13 @@ SIGNATURES: dict[str, tuple] = {
         [_vp, _vp, _vp, _vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _i64, _vp, _vp, _sz, _vp],
     ),
     "dbf_finalize_partial": (_int, [_vp, _vp, _int, _i64, _i64, _vp, _int, _i64, _vp]),
+    "dbf_allreduce_recv_bytes": (_sz, [_i64, _i64, _int]),
+    "dbf_allreduce_flag_bytes": (_sz, [_i64, _int]),
+    "dbf_forward_allreduce": (
+        _int,
+        [_vp, _vp, _vp, _vp, _vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _i64, _vp, _int, _i64, _vp, _vp,
+         _int, _int, _vp, _vp, _sz, _vp],
+    ),
     "dbf_sign_matvec_xor": (_int, [_vp, _i64, _i64, _i64, _vp, _int, _vp, _vp]),
     "dbf_engine_smem_bytes": (_int, [_c.c_int32, _c.c_int32, _c.POINTER(_sz)]),
     "dbf_engine_occupancy": (_int, [_c.c_int32, _c.POINTER(_c.c_int32), _c.POINTER(_c.c_int32)]),

@@ -38,7 +38,33 @@ struct GemvParams {
   void* y;             // output rows (y_dtype), row stride ldy
   int64_t ldy;
   int y_dtype;
+  // fused one-shot all-reduce (k-sharded GEMV2, dbf_forward_allreduce); ar_world == 0 = off
+  int ar_world, ar_rank, ar_group, ar_bt, ar_row0;
+  const uint32_t* ar_epoch;  // device call counter (GEMV2 reads it)
+  uint32_t* bump;            // GEMV1's first launch advances the counter (block 0, thread 0)
+  const uint64_t* ar_recv;   // [world] peer receive buffers, each [2][world][ar_bt][rows] fp32
+  const uint64_t* ar_flags;  // [world] peer flag arrays, each [kArGroups][world][nrb] u32
+  const void* ar_a;          // output scale a (scale_dtype)
+  void* ar_y;                // final output (ar_ydt), row stride ar_ldy
+  int64_t ar_ldy;
+  int ar_ydt;
 };
+
+constexpr int kArGroups = 16;  // launches per call that may share the flag array (batch <= 32)
+
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ double load_any(const void* p, int dt, int64_t i) {
   switch (dt) {
@@ -230,6 +256,8 @@ __global__ void __launch_bounds__(kThreads) gemv_i8_kernel(GemvParams p, const u
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
   const uint2* xf2 = (const uint2*)xfrag;
+  if (p.bump && blockIdx.x == 0 && threadIdx.x == 0) *p.bump += 1u;
+  const uint32_t ar_epoch = p.ar_world ? *(const volatile uint32_t*)p.ar_epoch : 0u;
 
   for (int rb = blockIdx.x; rb < p.nrb; rb += gridDim.x) {
     int acc[NP][4];
@@ -281,10 +309,57 @@ __global__ void __launch_bounds__(kThreads) gemv_i8_kernel(GemvParams p, const u
         const long long P = 2 * (s128 >> 7) - sT[slot];
         double v = (double)P * pow2(-sF[slot]);
         if (p.oscale) v *= load_any(p.oscale, p.scale_dtype, grow);
-        store_any(p.y, p.y_dtype, (int64_t)slot * p.ldy + grow, v);
+        if (p.ar_world) {
+          // one-shot all-reduce, push half: this rank's fp32 partial into slot `ar_rank` of every
+          // peer's receive buffer (NVLink P2P stores through the peers' mapped addresses)
+          const float fv = (float)v;
+          const size_t idx = (size_t)(ar_epoch & 1u) * p.ar_world * p.ar_bt * p.rows +
+                             ((size_t)p.ar_rank * p.ar_bt + p.ar_row0 + slot) * p.rows + grow;
+          for (int g2 = 0; g2 < p.ar_world; ++g2) ((float*)p.ar_recv[g2])[idx] = fv;
+        } else {
+          store_any(p.y, p.y_dtype, (int64_t)slot * p.ldy + grow, v);
+        }
       }
     }
     __syncthreads();
+  }
+  if (!p.ar_world) return;
+  // this CTA's row blocks are out: ONE system-scope fence, then release them to every peer
+  // (flag = epoch, monotonic); a fence per row block cost more than the GEMV itself
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int rb = blockIdx.x; rb < p.nrb; rb += gridDim.x)
+      for (int g2 = 0; g2 < p.ar_world; ++g2)
+        st_relaxed_sys((uint32_t*)p.ar_flags[g2] + ((size_t)p.ar_group * p.ar_world + p.ar_rank) * p.nrb + rb,
+                       ar_epoch);
+  }
+  // ---- one-shot all-reduce, combine half: wait until every rank has pushed every row block this
+  // CTA produced (all flags polled in parallel), then y = a * sum over ranks in rank order
+  // (identical bits on every rank)
+  const uint32_t* myflags = (const uint32_t*)p.ar_flags[p.ar_rank] + (size_t)p.ar_group * p.ar_world * p.nrb;
+  const float* recv = (const float*)p.ar_recv[p.ar_rank] + (size_t)(ar_epoch & 1u) * p.ar_world * p.ar_bt * p.rows;
+  const int nmy = (p.nrb - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  for (int i = threadIdx.x; i < nmy * p.ar_world; i += kThreads) {
+    const int rb = blockIdx.x + (i / p.ar_world) * gridDim.x, src = i % p.ar_world;
+    const uint32_t* f = myflags + (size_t)src * p.nrb + rb;
+    const uint64_t t0 = global_ns();
+    // epochs only grow: a peer already on the next call has also pushed this one
+    while ((int32_t)(ld_acquire_sys(f) - ar_epoch) < 0) {
+      __nanosleep(64);
+      if (global_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();  // 20 s watchdog: a peer is gone
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nmy * 16 * slots; i += kThreads) {
+    const int t = i % (16 * slots), row = t & 15, slot = t >> 4;
+    const int grow = (blockIdx.x + (i / (16 * slots)) * gridDim.x) * 16 + row;
+    if (slot < p.batch && grow < p.rows) {
+      double acc = 0.0;
+      for (int src = 0; src < p.ar_world; ++src)
+        acc += (double)__ldcg(recv + ((size_t)src * p.ar_bt + p.ar_row0 + slot) * p.rows + grow);
+      store_any(p.ar_y, p.ar_ydt, (int64_t)(p.ar_row0 + slot) * p.ar_ldy + grow,
+                (double)(float)acc * load_any(p.ar_a, p.scale_dtype, grow));
+    }
   }
 }
 
@@ -339,6 +414,7 @@ int run_gemv_pre(GemvParams p, int batch_total, cudaStream_t s, uint8_t* ws) {
   if (st != DBF_OK) return st;
   const size_t ysz = dtype_size(p.y_dtype);
   int done = 0;  // rows
+  int group = 0;
   while (done < batch_total) {
     const int left = batch_total - done;
     int np = 8;
@@ -348,6 +424,12 @@ int run_gemv_pre(GemvParams p, int batch_total, cudaStream_t s, uint8_t* ws) {
     GemvParams q = p;
     q.y = (char*)p.y + (int64_t)done * p.ldy * ysz;
     q.batch = take;
+    if (done > 0) q.bump = nullptr;
+    if (q.ar_world) {
+      q.ar_row0 = done;
+      q.ar_group = group++;
+      if (q.ar_group >= kArGroups) return DBF_ERR_UNSUPPORTED;
+    }
     const int pair0 = done / 2;
     const uint8_t* f = gfrag + (size_t)pair0 * nkb * 32 * 8;
     switch (np) {
@@ -368,12 +450,18 @@ int run_gemv(GemvParams p, int batch_total, cudaStream_t s, uint8_t* ws = nullpt
       gemv_smem_bytes(1, false, p.nchunks) <= 227 * 1024)
     return run_gemv_pre(p, batch_total, s, ws);
   const size_t xsz = dtype_size(p.x_dtype), ysz = dtype_size(p.y_dtype);
-  int done = 0;
+  int done = 0, group = 0;
   while (done < batch_total) {
     const int left = batch_total - done;
     GemvParams q = p;
     q.x = (const char*)p.x + (int64_t)done * p.ldx * xsz;
     q.y = (char*)p.y + (int64_t)done * p.ldy * ysz;
+    if (done > 0) q.bump = nullptr;
+    if (q.ar_world) {
+      q.ar_row0 = done;
+      q.ar_group = group++;
+      if (q.ar_group >= kArGroups) return DBF_ERR_UNSUPPORTED;
+    }
     int st;
     int take;
     if (left == 1 || gemv_smem_bytes(1, false, p.nchunks) > kMaxSmem) {
@@ -492,6 +580,56 @@ extern "C" int dbf_forward_partial(const void* A_shard_tiled, const void* B_shar
   if (st != DBF_OK) return st;
   GemvParams p2 = make_params(A_shard_tiled, n, k_shard, t, DBF_F32, k_shard, nullptr, nullptr,
                               scale_dtype, P, DBF_F32, n);
+  return run_gemv(p2, (int)batch, s, fw, fwb);
+}
+
+extern "C" size_t dbf_allreduce_recv_bytes(int64_t n, int64_t batch, int world) {
+  if (n < 1 || batch < 1 || world < 1) return 0;
+  return (size_t)2 * world * batch * n * sizeof(float);
+}
+
+extern "C" size_t dbf_allreduce_flag_bytes(int64_t n, int world) {
+  if (n < 1 || world < 1) return 0;
+  return (size_t)kArGroups * world * row_blocks(n) * sizeof(uint32_t);
+}
+
+extern "C" int dbf_forward_allreduce(const void* A_shard_tiled, const void* B_shard_tiled, const void* a,
+                                     const void* mid_shard, const void* b, int scale_dtype, int64_t n,
+                                     int64_t k_shard, int64_t m, const void* X, int x_dtype, int64_t batch,
+                                     int64_t ldx, void* Y, int y_dtype, int64_t ldy, const uint64_t* peer_recv,
+                                     const uint64_t* peer_flags, int world, int rank, uint32_t* epoch_counter,
+                                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (!A_shard_tiled || !B_shard_tiled || !a || !mid_shard || !b || !X || !Y || !peer_recv || !peer_flags ||
+      n < 1 || k_shard < 1 || m < 1 || batch < 1 || ldx < m || ldy < n || world < 1 || rank < 0 ||
+      rank >= world || !epoch_counter || !io_dtype_ok(x_dtype) || !io_dtype_ok(y_dtype) ||
+      !scale_dtype_ok(scale_dtype) || n > INT32_MAX)
+    return DBF_ERR_INVALID_ARGUMENT;
+  if (!workspace || workspace_bytes < dbf_forward_workspace_bytes(n, k_shard, m, batch))
+    return DBF_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  float* t = (float*)workspace;
+  uint8_t* fw = (uint8_t*)workspace + align256((size_t)batch * k_shard * sizeof(float));
+  const size_t fwb = workspace_bytes - align256((size_t)batch * k_shard * sizeof(float));
+  // GEMV1 on the local shard: t_g = mid_g * (B_g . (b * x)), no communication
+  GemvParams p1 = make_params(B_shard_tiled, k_shard, m, X, x_dtype, ldx, b, mid_shard, scale_dtype,
+                              t, DBF_F32, k_shard);
+  p1.bump = epoch_counter;  // this call's epoch = counter + 1, visible to GEMV2 by stream order
+  int st = run_gemv(p1, (int)batch, s, fw, fwb);
+  if (st != DBF_OK) return st;
+  // GEMV2 with the all-reduce in its epilogue: partial rows pushed to every rank as they are
+  // produced, each row block combined as soon as all ranks have released it
+  GemvParams p2 = make_params(A_shard_tiled, n, k_shard, t, DBF_F32, k_shard, nullptr, nullptr,
+                              scale_dtype, nullptr, DBF_F32, n);
+  p2.ar_world = world;
+  p2.ar_rank = rank;
+  p2.ar_epoch = epoch_counter;
+  p2.ar_bt = (int)batch;
+  p2.ar_recv = peer_recv;
+  p2.ar_flags = peer_flags;
+  p2.ar_a = a;
+  p2.ar_y = Y;
+  p2.ar_ldy = ldy;
+  p2.ar_ydt = y_dtype;
   return run_gemv(p2, (int)batch, s, fw, fwb);
 }
 

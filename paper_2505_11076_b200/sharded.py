@@ -6,6 +6,9 @@ Rank g owns rows K_g of B, columns K_g of A and mid[K_g]; x, b and a are replica
 computes its fp32 partial ``P_g = A_g . (mid_g * (B_g . (b * x)))`` with no communication
 (``dbf_forward_partial``), one SUM all-reduce combines the partials over NVLink (NCCL through
 ``torch.distributed``), and ``y = a * P`` is applied after the reduce (``dbf_finalize_partial``).
+``FusedAllReduce`` + ``DeviceShard.forward_allreduce`` fuse that exchange into GEMV2 instead
+(``dbf_forward_allreduce``): partial row blocks are pushed into every peer's symmetric-memory
+receive buffer from the kernel epilogue and combined per row block as soon as all ranks released it.
 
 Shard boundaries are multiples of 32 columns so every shard of A is a word-aligned slice of the
 packed rows (the reference's LSB-first layout, bitcore.py:7-9): k = 12736 over 4 ranks gives
@@ -93,6 +96,20 @@ def shard_layer(layer, rank: int, world: int, align: int = 32) -> LayerShard:
     )
 
 
+@dataclass(frozen=True)
+class _ShardShape:
+    rank: int
+    world: int
+    k0: int
+    k1: int
+    n: int
+    m_dim: int
+
+    @property
+    def k_shard(self) -> int:
+        return self.k1 - self.k0
+
+
 class DeviceShard:
     """Device image of a LayerShard (tiled A_g, B_g; scales in `scale_dtype`)."""
 
@@ -109,6 +126,15 @@ class DeviceShard:
         self.a = torch.as_tensor(np.array(shard.a)).to(dev, sd)
         self.mid = torch.as_tensor(np.array(shard.mid)).to(dev, sd)
         self.b = torch.as_tensor(np.array(shard.b)).to(dev, sd)
+
+    @classmethod
+    def from_device_layer(cls, layer, rank: int, world: int, k0: int = 0):
+        """Wrap a DeviceLayer that already holds one rank's shard (A_g n x k_g, B_g k_g x m) --
+        e.g. synthetic shards generated on each GPU for benchmarks."""
+        self = cls.__new__(cls)
+        self.shard = _ShardShape(rank, world, k0, k0 + layer.k, layer.n, layer.B.cols)
+        self.A, self.B, self.a, self.mid, self.b = layer.A, layer.B, layer.a, layer.mid, layer.b
+        return self
 
     def partial(self, X):
         """fp32 partial P_g (batch x n) for a CUDA tensor X (batch x m)."""
@@ -153,8 +179,88 @@ class DeviceShard:
         import torch.distributed as dist
 
         P = self.partial(X)
-        dist.all_reduce(P, op=dist.ReduceOp.SUM, group=group)
+        if dist.is_initialized():  # a single process without a group has nothing to reduce
+            dist.all_reduce(P, op=dist.ReduceOp.SUM, group=group)
         return self.finalize(P, out_dtype=out_dtype or X.dtype)
+
+
+    def forward_allreduce(self, X, peer_recv, peer_flags, epoch_counter, out_dtype=None):
+        """dbf_forward_allreduce: the layer with its all-reduce fused into GEMV2's epilogue.
+
+        ``peer_recv`` / ``peer_flags``: int64 CUDA tensors holding every rank's receive-buffer and
+        flag-array device addresses (``FusedAllReduce`` builds them from symmetric memory);
+        ``epoch_counter``: a 1-element int32 CUDA tensor the call advances on the device."""
+        import torch
+
+        from . import _lib
+        from .kernel import _workspace
+
+        sh = self.shard
+        X2 = X if X.ndim == 2 else X.unsqueeze(0)
+        X2 = X2.contiguous()
+        Y = torch.empty((X2.shape[0], sh.n), dtype=out_dtype or X2.dtype, device=X2.device)
+        ws = _workspace(_lib.lib.dbf_forward_workspace_bytes(sh.n, sh.k_shard, sh.m_dim, X2.shape[0]), X2.device)
+        _lib.check(
+            _lib.lib.dbf_forward_allreduce(
+                self.A.tiled.data_ptr(), self.B.tiled.data_ptr(), self.a.data_ptr(), self.mid.data_ptr(),
+                self.b.data_ptr(), _lib.dtype_code(self.a.dtype), sh.n, sh.k_shard, sh.m_dim, X2.data_ptr(),
+                _lib.dtype_code(X2.dtype), X2.shape[0], X2.stride(0), Y.data_ptr(), _lib.dtype_code(Y.dtype),
+                Y.stride(0), peer_recv.data_ptr(), peer_flags.data_ptr(), sh.world, sh.rank, epoch_counter.data_ptr(),
+                ws.data_ptr(), ws.numel(), _lib.stream_ptr(),
+            ),
+            "dbf_forward_allreduce",
+        )
+        return Y
+
+
+class FusedAllReduce:
+    """Receive buffers and flags of ``dbf_forward_allreduce`` in torch symmetric memory: every
+    rank maps every peer's buffers, so GEMV2's epilogue stores partials straight into them over
+    NVLink.  One instance serves every call with at most (n, batch); calls are counted on the
+    device, so a captured CUDA graph of ``forward`` replays correctly."""
+
+    def __init__(self, n: int, batch: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from . import _lib
+
+        if batch > 16:
+            raise ValueError("the fused all-reduce handles batch <= 16")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n, self.batch = n, batch
+        self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        if not dist.is_initialized():  # one process, no group: the buffers are local
+            self.world, self.rank = 1, 0
+            self.recv = torch.empty(_lib.lib.dbf_allreduce_recv_bytes(n, batch, 1) // 4, dtype=torch.float32,
+                                    device=dev)
+            self.flags = torch.zeros(_lib.lib.dbf_allreduce_flag_bytes(n, 1) // 4, dtype=torch.int32, device=dev)
+            self.peer_recv = torch.tensor([self.recv.data_ptr()], dtype=torch.int64, device=dev)
+            self.peer_flags = torch.tensor([self.flags.data_ptr()], dtype=torch.int64, device=dev)
+            return
+        grp = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(grp)
+        self.rank = dist.get_rank(grp)
+        rb = _lib.lib.dbf_allreduce_recv_bytes(n, batch, self.world)
+        fb = _lib.lib.dbf_allreduce_flag_bytes(n, self.world)
+        self.recv = symm_mem.empty(rb // 4, dtype=torch.float32, device=dev)
+        self.flags = symm_mem.empty(fb // 4, dtype=torch.int32, device=dev)
+        self.flags.zero_()
+        torch.cuda.synchronize(dev)
+        hr = symm_mem.rendezvous(self.recv, grp)
+        hf = symm_mem.rendezvous(self.flags, grp)
+        self.peer_recv = torch.tensor(list(hr.buffer_ptrs), dtype=torch.int64, device=dev)
+        self.peer_flags = torch.tensor(list(hf.buffer_ptrs), dtype=torch.int64, device=dev)
+        self._handles = (hr, hf)
+        dist.barrier(group=grp)  # every rank's flags are zero before anyone pushes
+
+    def forward(self, shard: "DeviceShard", X, out_dtype=None):
+        if (X.shape[0] if X.ndim == 2 else 1) > self.batch or shard.shard.n != self.n:
+            raise ValueError("layer/batch larger than this FusedAllReduce was sized for")
+        if shard.shard.world != self.world or shard.shard.rank != self.rank:
+            raise ValueError("shard rank/world do not match the process group")
+        return shard.forward_allreduce(X, self.peer_recv, self.peer_flags, self.counter, out_dtype=out_dtype)
 
 
 def reduce_partials_host(partials, a) -> np.ndarray:

@@ -62,3 +62,127 @@ def test_nccl_single_rank_group():
         assert rel_max(y, ref) <= 1e-2
     finally:
         dist.destroy_process_group()
+
+
+# ---- all-reduce fused into GEMV2 (dbf_forward_allreduce) -----------------------------------------
+
+def _ptrs(ts):
+    import torch
+
+    return torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device="cuda")
+
+
+@pytest.mark.parametrize("batch", [1, 3, 16])
+def test_fused_allreduce_single_rank_equals_partial_path(batch):
+    """world = 1: the fused kernel's push/flag/combine path gives the same bits as
+    dbf_forward_partial + dbf_finalize_partial, over several epochs (both buffer parities)."""
+    import torch
+
+    from paper_2505_11076_b200 import _lib
+
+    rng = np.random.default_rng(20 + batch)
+    layer = _host_layer(rng, 1000, 640, 1024)
+    ds = sharded.DeviceShard(sharded.shard_layer(layer, 0, 1), scale_dtype=torch.float16)
+    recv = torch.empty(_lib.lib.dbf_allreduce_recv_bytes(1000, batch, 1) // 4, dtype=torch.float32, device="cuda")
+    flags = torch.zeros(_lib.lib.dbf_allreduce_flag_bytes(1000, 1) // 4, dtype=torch.int32, device="cuda")
+    counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for epoch in range(1, 5):
+        X = torch.from_numpy(rng.standard_normal((batch, 1024)).astype(np.float16)).cuda()
+        ref = ds.finalize(ds.partial(X), out_dtype=torch.float16)
+        y = ds.forward_allreduce(X, _ptrs([recv]), _ptrs([flags]), counter)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref), epoch
+        assert int(counter.item()) == epoch
+        assert int(flags.view(16, 1, -1)[0].min()) == epoch
+    out = oracle.c_forward(X.double().cpu().numpy(), layer.a, layer.A.bits, layer.mid, layer.B.bits, layer.b)
+    assert rel_max(y.float().cpu().numpy(), out) <= 1e-2
+
+
+@pytest.mark.parametrize("world,rank,batch", [(4, 1, 2), (2, 0, 1), (8, 7, 16)])
+def test_fused_allreduce_combines_pushed_peer_partials(world, rank, batch):
+    """One rank of a `world`-GPU group on one GPU, the other ranks' pushes staged beforehand (their
+    partials written into this rank's receive slots and their flags raised), so nothing waits on
+    another kernel: the result is a * (sum of all ranks' partials in rank order) bit for bit, and
+    this rank's own partial lands in slot `rank` of every peer buffer."""
+    import torch
+
+    from paper_2505_11076_b200 import _lib
+
+    rng = np.random.default_rng(world * 10 + rank)
+    n, k, m = 1000, 1792, 2048
+    layer = _host_layer(rng, n, k, m)
+    X = torch.from_numpy(rng.standard_normal((batch, m)).astype(np.float16)).cuda()
+    shards = [sharded.DeviceShard(sharded.shard_layer(layer, g, world), scale_dtype=torch.float16) for g in range(world)]
+    parts = [s.partial(X) for s in shards]
+    nrb = -(-n // 16)
+    rbytes = _lib.lib.dbf_allreduce_recv_bytes(n, batch, world)
+    recvs = [torch.zeros(rbytes // 4, dtype=torch.float32, device="cuda") for _ in range(world)]
+    flags = [torch.zeros(_lib.lib.dbf_allreduce_flag_bytes(n, world) // 4, dtype=torch.int32, device="cuda")
+             for _ in range(world)]
+    counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for epoch in (1, 2):
+        mine = recvs[rank].view(2, world, batch, n)[epoch & 1]
+        for g in range(world):
+            if g != rank:
+                mine[g].copy_(parts[g])
+        fl = flags[rank].view(16, world, nrb)
+        for g in range(world):
+            if g != rank:
+                fl[:, g, :] = epoch
+        torch.cuda.synchronize()
+        y = shards[rank].forward_allreduce(X, _ptrs(recvs), _ptrs(flags), counter, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        acc = np.zeros((batch, n))
+        for g in range(world):
+            acc += parts[g].double().cpu().numpy()
+        a = shards[rank].a.double().cpu().numpy()
+        want = (acc.astype(np.float32).astype(np.float64) * a[None, :]).astype(np.float32)
+        np.testing.assert_array_equal(y.cpu().numpy(), want)
+        for g in range(world):  # the push: our partial in slot `rank` of every buffer, our flag raised
+            assert torch.equal(recvs[g].view(2, world, batch, n)[epoch & 1][rank], parts[rank])
+            assert int(flags[g].view(16, world, nrb)[0, rank].min()) == epoch
+    ref = oracle.c_forward(X.double().cpu().numpy(), layer.a, layer.A.bits, layer.mid, layer.B.bits, layer.b)
+    assert rel_max(y.cpu().numpy(), ref) <= 1e-2 and rel_norm(y.cpu().numpy(), ref) <= 1e-2
+
+
+def test_fused_allreduce_symmetric_memory_single_rank():
+    """FusedAllReduce over a 1-rank NCCL group: buffers from torch symmetric memory."""
+    import torch
+    import torch.distributed as dist
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(9)
+        layer = _host_layer(rng, 512, 640, 1024)
+        ds = sharded.DeviceShard(sharded.shard_layer(layer, 0, 1), scale_dtype=torch.float16)
+        try:
+            ar = sharded.FusedAllReduce(512, 4)
+        except Exception as e:  # noqa: BLE001 - symmetric memory needs driver/fabric support
+            pytest.skip(f"torch symmetric memory unavailable: {e}")
+        for _ in range(3):
+            X = torch.from_numpy(rng.standard_normal((4, 1024)).astype(np.float16)).cuda()
+            y = ar.forward(ds, X)
+            assert torch.equal(y, ds.forward(X))
+        # graph replay: the device-side call counter gives every replay a fresh epoch
+        X = torch.from_numpy(rng.standard_normal((4, 1024)).astype(np.float16)).cuda()
+        ref = ds.forward(X)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            ar.forward(ds, X)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            yg = ar.forward(ds, X)
+        for _ in range(4):
+            yg.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(yg, ref)
+        assert int(ar.counter.item()) == 3 + 1 + 4  # eager calls, warm-up call, replays (capture runs nothing)
+    finally:
+        dist.destroy_process_group()

@@ -335,9 +335,18 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     const int j = i - r0, buf = j & 1;
     int64_t* tr = prog.trace ? prog.trace + 4 * (size_t)i : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
+#ifdef DBF_ENGINE_WARP_TRACE
+    // debug build only: per (run, warp) stamps [start, pieces, quantized x3, computed x3, barrier, final]
+    int64_t* wt = prog.trace ? prog.trace + 4 * (size_t)prog.cta_offsets[gridDim.x] + ((size_t)i * kWarps + warp) * 10
+                             : nullptr;
+#define WT(k) do { if (wt && lane == 0) wt[k] = gtimer(); } while (0)
+#else
+#define WT(k) do { } while (0)
+#endif
     const int slot0 = P % ring_slots;
     const uint32_t phase0 = (uint32_t)(P / ring_slots) & 1u;
     mbar_wait(&sm.full[slot0], phase0);  // first piece: holds the record
+    WT(0);
     const dbf_engine_run& H = sm.hdr[slot0];
     const int cols = H.cols, nunits = H.nunits;
     InSpec in;
@@ -369,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       if (sl >= ring_slots) { sl -= ring_slots; ph ^= 1u; }
       mbar_wait(&sm.full[sl], ph);
     }
+    WT(1);
     const float osc = (oscale && warp < nunits && lane < 16 && (rb + warp) * 16 + lane < rows)
                           ? ld_scale(oscale, in.sdt, (rb + warp) * 16 + lane)
                           : 1.f;
@@ -399,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         }
       }
       if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
+      { const int jj = c / kWarps; if (jj < 3) WT(2 + jj); }
       uint2 b[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * NB * 64 + xlane);
@@ -452,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           acc1[u0 + 1] += v[1][1];
         }
       }
+      { const int jj = c / kWarps; if (jj < 3) WT(5 + jj); }
       first = false;
     }
     if (tr && warp == 0 && lane == 0) tr[2] = gtimer();
@@ -468,6 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+    WT(8);
     if (warp == 0 && lane == 0)  // every compute warp is done with the run's signs
       for (int p = 0; p < npieces; ++p) {
         int sl = slot0 + p;
@@ -497,6 +510,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       }
     }
     if (tr && threadIdx.x == 0) tr[3] = gtimer();
+    WT(9);
+#undef WT
     P += npieces;
   }
 }

@@ -117,8 +117,10 @@ __device__ __forceinline__ long long gtimer() {
 __device__ __forceinline__ float ld_scale(const void* p, int dt, int i) {
   return dt == DBF_F16 ? __half2float(((const __half*)p)[i]) : ((const float*)p)[i];
 }
-__device__ __forceinline__ uint32_t epoch16(uint32_t run_ctr, int nvectors, int vec) {
-  return (uint32_t)(((uint64_t)run_ctr * (uint64_t)nvectors + (uint64_t)vec) % 65535ull) + 1u;
+// epoch of vector `vec` in this launch: (launch * nvectors + vec) mod 65535 + 1, from the launch's
+// base (launch * nvectors) mod 65535
+__device__ __forceinline__ uint32_t epoch16(uint32_t base, int vec) {
+  return (base + (uint32_t)vec) % 65535u + 1u;
 }
 
 struct Smem {
@@ -273,6 +275,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   sm.part = (float*)(sm.xs + kWarps * xs_bytes<NB>());
   sm.full = (uint64_t*)(sm.part + 2 * kPartFloats);
   sm.empty = sm.full + kMaxSlots;
+  // rarely-read per-warp / per-CTA scalars live in shared memory, not in (spilled) registers:
+  // the quantized chunks' F and T for reuse across runs, and the launch's epoch base
+  int* qft = (int*)(sm.empty + kMaxSlots);  // [kWarps][xs_chunks][NB][2]
+  uint32_t* ep_base_s = (uint32_t*)(qft + kWarps * xs_chunks<NB>() * NB * 2);
+  // input key (vector, input scale) of the quantized chunks, double-buffered by run parity: run j
+  // reads slot (j+1)&1 (written by warp 0 during run j-1, before that run's barrier) and writes j&1
+  struct InKey { const void* iscale; int vec; int pad; };
+  InKey* inkey = (InKey*)(ep_base_s + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -285,7 +295,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   __syncthreads();
 
   const int r0 = prog.cta_offsets[blockIdx.x], r1 = prog.cta_offsets[blockIdx.x + 1];
-  const uint32_t run_ctr = *prog.run_counter;
+  if (threadIdx.x == 0) {
+    *ep_base_s = (uint32_t)(((uint64_t)*prog.run_counter * (uint64_t)prog.nvectors) % 65535ull);
+    inkey[0].vec = inkey[1].vec = -1;
+    inkey[0].iscale = inkey[1].iscale = nullptr;
+  }
+  __syncthreads();
   const dbf_engine_run* R = prog.runs;
 
   if (warp == kProdWarp) {
@@ -302,16 +317,18 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         const int cols = n_cols, nunits = n_units;
         if (i + 1 < r1) { n_tiled = R[i + 1].tiled; n_cols = R[i + 1].cols; n_units = R[i + 1].nunits; }
         const int total = nunits * ((cols + kChunkCols - 1) / kChunkCols) * kChunkBytes;
+        // every piece of the run completes on the FIRST slot's full barrier (armed once with the
+        // run's total bytes), so the compute warps wait on one barrier instead of one per piece
+        int slot0 = slot;
         for (int off = 0; off < total; off += kSlotBytes) {
           const int n = min(kSlotBytes, total - off);
           mbar_wait(&sm.empty[slot], phase ^ 1u);
           if (off == 0) {
-            mbar_arrive_expect_tx(&sm.full[slot], n + (int)sizeof(dbf_engine_run));
-            bulk_g2s(&sm.hdr[slot], R + i, sizeof(dbf_engine_run), &sm.full[slot], pol);
-          } else {
-            mbar_arrive_expect_tx(&sm.full[slot], n);
+            slot0 = slot;
+            mbar_arrive_expect_tx(&sm.full[slot0], total + (int)sizeof(dbf_engine_run));
+            bulk_g2s(&sm.hdr[slot0], R + i, sizeof(dbf_engine_run), &sm.full[slot0], pol);
           }
-          bulk_g2s(sm.ring + (size_t)slot * kSlotBytes, src + off, n, &sm.full[slot], pol);
+          bulk_g2s(sm.ring + (size_t)slot * kSlotBytes, src + off, n, &sm.full[slot0], pol);
           if (++slot == ring_slots) { slot = 0; phase ^= 1u; }
         }
       }
@@ -327,10 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   const int xlane = ((lane >> 2) % (2 * NB)) * 32 + (lane & 3) * 8;
   // the quantized chunks stay valid for the next run when it reads the same vector with the same
   // input scale (a stage's units split over several runs of one CTA)
-  int cur_vec = -1;
-  const void* cur_iscale = nullptr;
-  int qF[xs_chunks<NB>()][NB], qT[xs_chunks<NB>()][NB];
-  int P = 0;  // ring pieces consumed before the current run
+  int* wq = qft + warp * xs_chunks<NB>() * NB * 2;  // this warp's [xs_chunks][NB][F, T]
+  int P = 0;          // ring pieces consumed before the current run
+  uint32_t fph = 0u;  // parity of each slot's full barrier (flips only when a run starts there)
   for (int i = r0; i < r1; ++i) {
     const int j = i - r0, buf = j & 1;
     int64_t* tr = prog.trace ? prog.trace + 4 * (size_t)i : nullptr;
@@ -344,8 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 #define WT(k) do { } while (0)
 #endif
     const int slot0 = P % ring_slots;
-    const uint32_t phase0 = (uint32_t)(P / ring_slots) & 1u;
-    mbar_wait(&sm.full[slot0], phase0);  // first piece: holds the record
+    mbar_wait(&sm.full[slot0], (fph >> slot0) & 1u);  // the run's record and ALL its pieces
+    fph ^= 1u << slot0;
     WT(0);
     const dbf_engine_run& H = sm.hdr[slot0];
     const int cols = H.cols, nunits = H.nunits;
@@ -363,29 +379,26 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     const void* oscale = H.oscale;
     void* out_plain = H.out_plain;
     uint32_t* ll_out = (uint32_t*)H.ll_out;
-    const uint32_t ep_out = epoch16(run_ctr, prog.nvectors, H.out_vec);
+    const uint32_t ep_out = epoch16(*ep_base_s, H.out_vec);
     const int nch = (cols + kChunkCols - 1) / kChunkCols;
     const int npieces = (nunits * nch * kChunkBytes + kSlotBytes - 1) / kSlotBytes;
-    const uint32_t ep_in = H.in_kind == 1 ? epoch16(run_ctr, prog.nvectors, H.in_vec) : 0u;
+    const uint32_t ep_in = H.in_kind == 1 ? epoch16(*ep_base_s, H.in_vec) : 0u;
     float acc0[kMaxUnits], acc1[kMaxUnits];  // rows g, g+8 of each unit for token tig (tig < NB)
 #pragma unroll
     for (int u = 0; u < kMaxUnits; ++u) acc0[u] = acc1[u] = 0.f;
     // all of the run's signs are resident before the MMA loop (no waits inside it, so the
     // compiler can interleave the units' loads and MMAs)
-    for (int p = 1; p < npieces; ++p) {
-      int sl = slot0 + p;
-      uint32_t ph = phase0;
-      if (sl >= ring_slots) { sl -= ring_slots; ph ^= 1u; }
-      mbar_wait(&sm.full[sl], ph);
-    }
     WT(1);
     const float osc = (oscale && warp < nunits && lane < 16 && (rb + warp) * 16 + lane < rows)
                           ? ld_scale(oscale, in.sdt, (rb + warp) * 16 + lane)
                           : 1.f;
     constexpr int kReuseChunks = xs_chunks<NB>() * kWarps;
-    const bool reuse = H.in_vec == cur_vec && in.iscale == cur_iscale && nch <= kReuseChunks;
-    cur_vec = nch <= kReuseChunks ? H.in_vec : -1;
-    cur_iscale = in.iscale;
+    const InKey prev = inkey[buf ^ 1];
+    const bool reuse = H.in_vec == prev.vec && in.iscale == prev.iscale && nch <= kReuseChunks;
+    if (warp == 0 && lane == 0) {
+      inkey[buf].vec = nch <= kReuseChunks ? H.in_vec : -1;
+      inkey[buf].iscale = in.iscale;
+    }
     bool first = true;
     for (int c = warp; c < nch; c += kWarps) {
       const int qs = (c / kWarps) % xs_chunks<NB>();
@@ -393,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       int F[NB], T[NB];
       if (reuse) {
 #pragma unroll
-        for (int t = 0; t < NB; ++t) F[t] = qF[qs][t], T[t] = qT[qs][t];
+        for (int t = 0; t < NB; ++t) F[t] = wq[(qs * NB + t) * 2], T[t] = wq[(qs * NB + t) * 2 + 1];
       } else {
 #pragma unroll
         for (int t = 0; t < NB; ++t) {
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
             __syncwarp();
             F[t] = 0, T[t] = 0;
           }
-          qF[qs][t] = F[t], qT[qs][t] = T[t];
+          if (lane == 0) wq[(qs * NB + t) * 2] = F[t], wq[(qs * NB + t) * 2 + 1] = T[t];
         }
       }
       if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
@@ -434,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           if (slot >= ring_slots) slot -= ring_slots;
           w[h] = *((const uint4*)(sm.ring + (size_t)slot * kSlotBytes + (off & (kSlotBytes - 1))) + lane);
         }
-        int ac[2][4][4] = {};  // per unit: four independent accumulator chains
+        int ac[2][2][4] = {};  // per unit: two independent accumulator chains
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           // k-block r = 4s + t reads (word >> 4s) & (0x01010101 << t): A bytes 2^t * bit
@@ -442,17 +455,17 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           const int sh = 4 * (r >> 2);
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            imma(ac[h][r & 3], (w[h].x >> sh) & m, (w[h].y >> sh) & m, (w[h].z >> sh) & m, (w[h].w >> sh) & m,
+            imma(ac[h][r & 1], (w[h].x >> sh) & m, (w[h].y >> sh) & m, (w[h].z >> sh) & m, (w[h].w >> sh) & m,
                  b[r].x, b[r].y);
         }
         float v[2][2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           // columns 2*tig, 2*tig+1 (token tig's digit planes) of rows g, g+8: s = 8 * sum bit X
-          const int s0 = (ac[h][0][0] + ac[h][1][0]) + (ac[h][2][0] + ac[h][3][0]);
-          const int s1 = (ac[h][0][1] + ac[h][1][1]) + (ac[h][2][1] + ac[h][3][1]);
-          const int s2 = (ac[h][0][2] + ac[h][1][2]) + (ac[h][2][2] + ac[h][3][2]);
-          const int s3 = (ac[h][0][3] + ac[h][1][3]) + (ac[h][2][3] + ac[h][3][3]);
+          const int s0 = ac[h][0][0] + ac[h][1][0];
+          const int s1 = ac[h][0][1] + ac[h][1][1];
+          const int s2 = ac[h][0][2] + ac[h][1][2];
+          const int s3 = ac[h][0][3] + ac[h][1][3];
           v[h][0] = (float)(((s0 + 256 * s1) >> 2) - Tt) * inv;
           v[h][1] = (float)(((s2 + 256 * s3) >> 2) - Tt) * inv;
         }
@@ -521,7 +534,7 @@ __global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; 
 inline size_t fixed_smem(int nb) {
   const int xs = (nb <= 2 ? 2 : 1) * kChunkQBytes1 * nb;
   return kMaxSlots * sizeof(dbf_engine_run) + (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 +
-         2 * kMaxSlots * 8 + 128;
+         2 * kMaxSlots * 8 + (size_t)kWarps * 4 * 2 * 4 + 48 + 128;
 }
 inline int ring_slots(int nb = 1) { return std::min((int)((kMaxSmem - fixed_smem(nb)) / kSlotBytes), kMaxSlots); }
 inline size_t smem_bytes(int slots, int nb = 1) { return (size_t)slots * kSlotBytes + fixed_smem(nb); }

@@ -68,3 +68,20 @@ for s in range(per_block, 2 * per_block):
           f"pieces {cols[0]} q0 {cols[1]} c0 {cols[2]} q1 {cols[3]} c1 {cols[4]} q2 {cols[5]} c2 {cols[6]} "
           f"bar {int(np.median(bar))}/{int(bar.max())} fin {int(np.median(fin))}/{int(fin.max())} "
           f"stage {last_pub[s] - prev}{idle}")
+
+print("\ncritical CTA per stage (the last publisher): its phases relative to the previous stage's last publish (ns)")
+cta_of_run = np.searchsorted(eng._offsets, np.arange(nr), side="right") - 1
+prev_crit = None
+for s in range(per_block, 2 * per_block):
+    runs = np.where(stage == s)[0]
+    prev = last_pub.get(s - 1, tr[:, 0].min())
+    j = runs[np.argmax(tr[runs, 3])]
+    c = cta_of_run[j]
+    W = wt[j]
+    act = W[:, 0] > 0
+    q0 = W[act, 2].max() - prev
+    lastc = np.max(np.where(W[act, 7] > 0, W[act, 7], np.where(W[act, 6] > 0, W[act, 6], W[act, 5]))) - prev
+    print(f"{s:3d} {','.join(names[s]):22s} cta {c:3d} (prev crit {prev_crit}) runs-in-stage {np.sum(cta_of_run[runs] == c)} "
+          f"start {W[act, 0].min() - prev:6d} pieces {W[act, 1].max() - prev:6d} q0(max warp) {q0:6d} "
+          f"compute-done {lastc:6d} bar {W[act, 8].max() - prev:6d} pub {tr[j, 3] - prev:6d}")
+    prev_crit = c

@@ -114,6 +114,17 @@ __device__ __forceinline__ long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// non-blocking loads of raw scale bits (the consumer converts them when it needs the value)
+__device__ __forceinline__ uint32_t ld_nc_u16(const unsigned short* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ float ld_scale(const void* p, int dt, int i) {
   return dt == DBF_F16 ? __half2float(((const __half*)p)[i]) : ((const float*)p)[i];
 }
@@ -206,19 +217,23 @@ __device__ __forceinline__ bool load_group(const InSpec& in, int col0, uint32_t 
 // both digits in [-128, 127]) and every k-block contributes 8 * sum bit_j X_j alike.
 // Returns F and T = sum_j X_j.
 __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t epoch, uint8_t* xs, int kb_stride,
-                                               int& F_out, int& T_out) {
+                                               int& F_out, int& T_out, int64_t* dbg = nullptr) {
   const int lane = threadIdx.x & 31;
   float u[2][4], sc[2][4];
   const int c0 = c * kChunkCols;
   // groups q = lane and lane + 32 (64 groups of 4 columns per chunk); scales first (never wait)
   load_scale4(in, c0 + 4 * lane, sc[0]);
   load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
+  int npoll = 0;
+  if (dbg && lane == 0) dbg[0] = gtimer();
   for (;;) {
     const bool ok0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
     const bool ok1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
+    ++npoll;
     if (__all_sync(0xffffffffu, ok0 && ok1)) break;
     if (kPollSleepNs) __nanosleep(kPollSleepNs);
   }
+  if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[2] = npoll; }
   float mx = 0.f;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -352,8 +367,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     int64_t* tr = prog.trace ? prog.trace + 4 * (size_t)i : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
 #ifdef DBF_ENGINE_WARP_TRACE
-    // debug build only: per (run, warp) stamps [start, pieces, quantized x3, computed x3, barrier, final]
-    int64_t* wt = prog.trace ? prog.trace + 4 * (size_t)prog.cta_offsets[gridDim.x] + ((size_t)i * kWarps + warp) * 10
+    // debug build only: per (run, warp) stamps [start, pieces, quantized x3, computed x3, barrier, final,
+    // first chunk: poll start, poll success, poll count]
+    int64_t* wt = prog.trace ? prog.trace + 4 * (size_t)prog.cta_offsets[gridDim.x] + ((size_t)i * kWarps + warp) * 13
                              : nullptr;
 #define WT(k) do { if (wt && lane == 0) wt[k] = gtimer(); } while (0)
 #else
@@ -389,9 +405,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     // all of the run's signs are resident before the MMA loop (no waits inside it, so the
     // compiler can interleave the units' loads and MMAs)
     WT(1);
-    const float osc = (oscale && warp < nunits && lane < 16 && (rb + warp) * 16 + lane < rows)
-                          ? ld_scale(oscale, in.sdt, (rb + warp) * 16 + lane)
-                          : 1.f;
+    // the output scale is fetched now as RAW bits and converted only in the finalize: converting
+    // here would stall the finalizing warps for a full L2 round trip before their first poll
+    const int fu = kWarps - 1 - warp;  // the unit this warp finalizes (warps 15, 14, ...: they own
+                                       // the fewest chunks when a run's chunks do not divide by 16)
+    uint32_t osc_bits = in.sdt == DBF_F16 ? 0x3C00u : 0x3F800000u;  // 1.0
+    if (oscale && fu < nunits && lane < 16 && (rb + fu) * 16 + lane < rows) {
+      const int r = (rb + fu) * 16 + lane;
+      osc_bits = in.sdt == DBF_F16 ? (uint32_t)ld_nc_u16((const unsigned short*)oscale + r)
+                                   : ld_nc_u32((const uint32_t*)oscale + r);
+    }
     constexpr int kReuseChunks = xs_chunks<NB>() * kWarps;
     const InKey prev = inkey[buf ^ 1];
     const bool reuse = H.in_vec == prev.vec && in.iscale == prev.iscale && nch <= kReuseChunks;
@@ -411,7 +434,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 #pragma unroll
         for (int t = 0; t < NB; ++t) {
           if (t < batch) {
+#ifdef DBF_ENGINE_WARP_TRACE
+            quantize_chunk(token_of(in, t), c, ep_in, xq + t * 64, NB * 64, F[t], T[t],
+                           (wt && c == warp && t == 0) ? wt + 10 : nullptr);
+#else
             quantize_chunk(token_of(in, t), c, ep_in, xq + t * 64, NB * 64, F[t], T[t]);
+#endif
           } else {  // absent token: zero digits
             for (int e = lane; e < 8 * 16; e += 32)
               *(uint32_t*)(xq + (e >> 4) * NB * 64 + t * 64 + (e & 15) * 4) = 0u;
@@ -500,18 +528,20 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         if (sl >= ring_slots) sl -= ring_slots;
         mbar_arrive(&sm.empty[sl]);
       }
-    // warp u finalizes unit u: sum the 16 warps' partials in warp order (deterministic), scale,
+    // warp 15 - u finalizes unit u: sum the 16 warps' partials in warp order (deterministic), scale,
     // publish; lanes 0-15 / 16-31 take one token each per pass
-    const float osc_row = __shfl_sync(0xffffffffu, osc, lane & 15);
-    if (warp < nunits) {
-      const int row = (rb + warp) * 16 + (lane & 15);
+    const uint32_t osc_raw = __shfl_sync(0xffffffffu, osc_bits, lane & 15);
+    const float osc_row = in.sdt == DBF_F16 ? __half2float(__ushort_as_half((unsigned short)osc_raw))
+                                            : __uint_as_float(osc_raw);
+    if (fu < nunits) {
+      const int row = (rb + fu) * 16 + (lane & 15);
 #pragma unroll
       for (int t0 = 0; t0 < NB; t0 += 2) {
         const int t = t0 + (lane >> 4);
         if (t < NB && t < batch && row < rows) {
           float v = 0.f;
 #pragma unroll
-          for (int w2 = 0; w2 < kWarps; ++w2) v += part[((w2 * kMaxUnits + warp) * NB + t) * 16 + (lane & 15)];
+          for (int w2 = 0; w2 < kWarps; ++w2) v += part[((w2 * kMaxUnits + fu) * NB + t) * 16 + (lane & 15)];
           v *= osc_row;
           const __half h = __float2half_rn(v);
           if (ll_out) st_ll16(ll_out + t * out_ll_stride + row, h, ep_out);

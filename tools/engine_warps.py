@@ -22,14 +22,14 @@ plan.buffers[plan.input_buffer].normal_(generator=g)
 plan.use_engine()
 eng = plan.engine
 nr = eng.nruns
-eng.trace = torch.zeros(4 * nr + nr * 16 * 10, dtype=torch.int64, device="cuda")
+eng.trace = torch.zeros(4 * nr + nr * 16 * 13, dtype=torch.int64, device="cuda")
 eng._prog.trace = eng.trace.data_ptr()
 for _ in range(3):
     plan._eager()
 torch.cuda.synchronize()
 t = eng.trace.cpu().numpy().astype(np.int64)
 tr = t[: 4 * nr].reshape(nr, 4)
-wt = t[4 * nr:].reshape(nr, 16, 10)
+wt = t[4 * nr:].reshape(nr, 16, 13)
 lv = levels_of(plan.ops, plan.input_buffer)
 seg_stage = []
 for i in range(len(plan.ops)):
@@ -84,4 +84,8 @@ for s in range(per_block, 2 * per_block):
     print(f"{s:3d} {','.join(names[s]):22s} cta {c:3d} (prev crit {prev_crit}) runs-in-stage {np.sum(cta_of_run[runs] == c)} "
           f"start {W[act, 0].min() - prev:6d} pieces {W[act, 1].max() - prev:6d} q0(max warp) {q0:6d} "
           f"compute-done {lastc:6d} bar {W[act, 8].max() - prev:6d} pub {tr[j, 3] - prev:6d}")
+    ws = int(np.argmax(W[act, 2]))
+    print(f"      slowest-q0 warp {ws}: poll start {W[act, 10][ws] - prev} success {W[act, 11][ws] - prev} polls {W[act, 12][ws]}; "
+          f"all warps: poll start med {int(np.median(W[act, 10] - prev))} success med {int(np.median(W[act, 11] - prev))} "
+          f"max {int((W[act, 11] - prev).max())} polls med {int(np.median(W[act, 12]))} max {W[act, 12].max()}")
     prev_crit = c

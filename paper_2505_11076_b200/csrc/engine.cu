@@ -286,18 +286,20 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   Smem sm;
   sm.ring = smem;
   sm.hdr = (dbf_engine_run*)(sm.ring + (size_t)ring_slots * kSlotBytes);
-  sm.xs = (uint8_t*)(sm.hdr + kMaxSlots);
+  sm.xs = (uint8_t*)(sm.hdr + ring_slots);
   sm.part = (float*)(sm.xs + kWarps * xs_bytes<NB>());
   sm.full = (uint64_t*)(sm.part + 2 * kPartFloats);
-  sm.empty = sm.full + kMaxSlots;
+  sm.empty = sm.full + ring_slots;
   // rarely-read per-warp / per-CTA scalars live in shared memory, not in (spilled) registers:
-  // the quantized chunks' F and T for reuse across runs, and the launch's epoch base
-  int* qft = (int*)(sm.empty + kMaxSlots);  // [kWarps][xs_chunks][NB][2]
+  // the quantized chunks' F and T for reuse across runs, the launch's epoch base, and each
+  // warp's ring cursor {next first slot, full-barrier parities}
+  int* qft = (int*)(sm.empty + ring_slots);  // [kWarps][xs_chunks][NB][2]
   uint32_t* ep_base_s = (uint32_t*)(qft + kWarps * xs_chunks<NB>() * NB * 2);
   // input key (vector, input scale) of the quantized chunks, double-buffered by run parity: run j
   // reads slot (j+1)&1 (written by warp 0 during run j-1, before that run's barrier) and writes j&1
   struct InKey { const void* iscale; int vec; int pad; };
   InKey* inkey = (InKey*)(ep_base_s + 4);
+  int2* cursor = (int2*)(inkey + 2);  // [kWarps]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -360,8 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   // the quantized chunks stay valid for the next run when it reads the same vector with the same
   // input scale (a stage's units split over several runs of one CTA)
   int* wq = qft + warp * xs_chunks<NB>() * NB * 2;  // this warp's [xs_chunks][NB][F, T]
-  int P = 0;          // ring pieces consumed before the current run
-  uint32_t fph = 0u;  // parity of each slot's full barrier (flips only when a run starts there)
+  if (lane == 0) cursor[warp] = make_int2(0, 0);  // {first slot of the next run, full parities}
+  __syncwarp();
   for (int i = r0; i < r1; ++i) {
     const int j = i - r0, buf = j & 1;
     int64_t* tr = prog.trace ? prog.trace + 4 * (size_t)i : nullptr;
@@ -375,9 +377,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 #else
 #define WT(k) do { } while (0)
 #endif
-    const int slot0 = P % ring_slots;
-    mbar_wait(&sm.full[slot0], (fph >> slot0) & 1u);  // the run's record and ALL its pieces
-    fph ^= 1u << slot0;
+    const int2 cur = cursor[warp];
+    const int slot0 = cur.x;
+    mbar_wait(&sm.full[slot0], ((uint32_t)cur.y >> slot0) & 1u);  // the run's record and ALL its pieces
     WT(0);
     const dbf_engine_run& H = sm.hdr[slot0];
     const int cols = H.cols, nunits = H.nunits;
@@ -555,19 +557,26 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     if (tr && threadIdx.x == 0) tr[3] = gtimer();
     WT(9);
 #undef WT
-    P += npieces;
+    if (lane == 0) {
+      int nx = slot0 + npieces;
+      if (nx >= ring_slots) nx -= ring_slots;
+      cursor[warp] = make_int2(nx, cur.y ^ (1 << slot0));
+    }
+    __syncwarp();
   }
 }
 
 __global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; }
 
+// shared memory besides the per-slot parts (16 KB ring slot + 128 B record + 2 mbarriers)
 inline size_t fixed_smem(int nb) {
   const int xs = (nb <= 2 ? 2 : 1) * kChunkQBytes1 * nb;
-  return kMaxSlots * sizeof(dbf_engine_run) + (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 +
-         2 * kMaxSlots * 8 + (size_t)kWarps * 4 * 2 * 4 + 48 + 128;
+  return (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 + (size_t)kWarps * 4 * 2 * 4 + 48 +
+         (size_t)kWarps * 8 + 128;
 }
-inline int ring_slots(int nb = 1) { return std::min((int)((kMaxSmem - fixed_smem(nb)) / kSlotBytes), kMaxSlots); }
-inline size_t smem_bytes(int slots, int nb = 1) { return (size_t)slots * kSlotBytes + fixed_smem(nb); }
+constexpr size_t kPerSlot = kSlotBytes + sizeof(dbf_engine_run) + 2 * 8;
+inline int ring_slots(int nb = 1) { return std::min((int)((kMaxSmem - fixed_smem(nb)) / kPerSlot), kMaxSlots); }
+inline size_t smem_bytes(int slots, int nb = 1) { return (size_t)slots * kPerSlot + fixed_smem(nb); }
 inline int nb_for(int batch) { return batch <= 1 ? 1 : (batch <= 2 ? 2 : 4); }
 
 }  // namespace engine

@@ -243,12 +243,13 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
       mx = fmaxf(mx, fabsf(u[h][e]));
     }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  // |u| >= 0: the float bits order like unsigned integers, so one REDUX gives the warp max
+  const uint32_t mxb = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
   int F = 0;
-  if (mx > 0.f) {
-    int e;
-    frexpf(mx, &e);  // mx in [2^(e-1), 2^e)  ->  |X| <= 4096 * kQScale <= 4079
+  if (mxb != 0u) {
+    // mx in [2^(e-1), 2^e) with e = biased exponent - 126 (mx is a normal float: fp16 inputs
+    // times fp16/fp32 scales stay far above 2^-126)  ->  |X| <= 4096 * kQScale <= 4079
+    const int e = (int)(mxb >> 23) - 126;
     F = 12 - e;
     F = F > 125 ? 125 : (F < -125 ? -125 : F);
   }
@@ -272,9 +273,8 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
     *(uint32_t*)(base + 0) = lo ^ 0x80808080u;   // plane 0 -> MMA column 0 (lanes 0-3)
     *(uint32_t*)(base + 32) = hi ^ 0x80808080u;  // plane 1 -> MMA column 1 (lanes 4-7)
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
-  __syncwarp();
+  ts = __reduce_add_sync(0xffffffffu, ts);
+  __syncwarp();  // the digit stores above are visible to every lane of the warp
   F_out = F;
   T_out = ts;
 }

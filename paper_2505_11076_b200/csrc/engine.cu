@@ -221,9 +221,18 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
   const int lane = threadIdx.x & 31;
   float u[2][4], sc[2][4];
   const int c0 = c * kChunkCols;
-  // groups q = lane and lane + 32 (64 groups of 4 columns per chunk); scales first (never wait)
-  load_scale4(in, c0 + 4 * lane, sc[0]);
-  load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
+  // groups q = lane and lane + 32 (64 groups of 4 columns per chunk).  fp16 scales of whole
+  // groups are loaded as raw bits before the poll and converted after it (converting here would
+  // hold the first poll back by a full round trip); other scale layouts load directly.
+  const bool raw_sc = in.iscale && in.sdt == DBF_F16 && c0 + 4 * (lane + 32) + 3 < in.cols;
+  uint2 sr0 = make_uint2(0, 0), sr1 = make_uint2(0, 0);
+  if (raw_sc) {
+    sr0 = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * lane));
+    sr1 = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * (lane + 32)));
+  } else {
+    load_scale4(in, c0 + 4 * lane, sc[0]);
+    load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
+  }
   int npoll = 0;
   if (dbg && lane == 0) dbg[0] = gtimer();
   for (;;) {
@@ -234,6 +243,12 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
     if (kPollSleepNs) __nanosleep(kPollSleepNs);
   }
   if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[2] = npoll; }
+  if (raw_sc) {
+    const float2 a0 = __half22float2(*(const __half2*)&sr0.x), b0 = __half22float2(*(const __half2*)&sr0.y);
+    const float2 a1 = __half22float2(*(const __half2*)&sr1.x), b1 = __half22float2(*(const __half2*)&sr1.y);
+    sc[0][0] = a0.x, sc[0][1] = a0.y, sc[0][2] = b0.x, sc[0][3] = b0.y;
+    sc[1][0] = a1.x, sc[1][1] = a1.y, sc[1][2] = b1.x, sc[1][3] = b1.y;
+  }
   float mx = 0.f;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {

@@ -79,9 +79,10 @@ def as_device_signs(s) -> DeviceSignMatrix:
 # device fast path
 # ---------------------------------------------------------------------------------------------
 PREFILL_MIN_TOKENS = 64
-# one persistent kernel for both GEMMs (dbf_forward_prefill_fused, 1-2 % faster than two launches
-# on B200); DBF_PREFILL_UNFUSED=1 selects the two-launch path (dbf_forward_prefill)
-PREFILL_FUSED = not os.environ.get("DBF_PREFILL_UNFUSED")
+# two launches (dbf_forward_prefill) by default: over the 7 Llama-2-7B shapes at T = 2048 they
+# sustain 870 TFLOP/s against 781 for the one-kernel persistent variant
+# (dbf_forward_prefill_fused), which DBF_PREFILL_FUSED=1 selects
+PREFILL_FUSED = bool(os.environ.get("DBF_PREFILL_FUSED"))
 
 
 def _prefill_eligible(X2, layer: DeviceLayer, out_dtype) -> bool:

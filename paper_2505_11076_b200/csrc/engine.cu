@@ -34,8 +34,14 @@ namespace dbf {
 namespace engine {
 
 constexpr int kWarps = 16;                    // compute warps
-constexpr int kProdWarp = kWarps;             // producer warp index
-constexpr int kThreads = (kWarps + 1) * 32;
+constexpr int kProdWarp = kWarps;             // producer warp index (first warp of the last warpgroup)
+// 16 compute warps + one producer WARPGROUP (warp 16 streams, 17-19 only hand their registers
+// back): the producer warpgroup drops to kProdRegs with setmaxnreg and the compute warpgroups
+// grow to kComputeRegs, where 17 warps at launch cap every thread at 96 (5 warps on one SM
+// sub-partition).  120 would fit the register file on paper but setmaxnreg.inc never returns
+// with it on B200 (measured); 112 does.
+constexpr int kThreads = (kWarps + 4) * 32;
+constexpr int kProdRegs = 24, kComputeRegs = 112;
 constexpr int kSlotBytes = 16384;             // one ring slot = 32 chunks of 512 B
 constexpr int kMaxUnits = 8;                  // units per run (the host splits longer runs)
 #ifndef DBF_POLL_NS
@@ -209,46 +215,10 @@ __device__ __forceinline__ bool load_group(const InSpec& in, int col0, uint32_t 
   return true;
 }
 
-// Quantize chunk c of the run's input (256 columns, warp-local) into this warp's B-fragment
-// scratch.  X_j = round(x_j * 2^F * kQScale) on a 13-bit grid relative to the CHUNK max
-// (|X| <= 4079); the MMA A bytes are 2^t * bit_j for k-block r = 4s + t (the packed word
-// pre-shifted by 4s: one shift per word serves four k-blocks), so the B operand carries
-// Y_j = X_j * 2^(3-t) as two balanced int8 digits (planes = MMA columns 0, 1; |Y| < 32640 keeps
-// both digits in [-128, 127]) and every k-block contributes 8 * sum bit_j X_j alike.
-// Returns F and T = sum_j X_j.
-__device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t epoch, uint8_t* xs, int kb_stride,
-                                               int& F_out, int& T_out, int64_t* dbg = nullptr) {
-  const int lane = threadIdx.x & 31;
-  float u[2][4], sc[2][4];
-  const int c0 = c * kChunkCols;
-  // groups q = lane and lane + 32 (64 groups of 4 columns per chunk).  fp16 scales of whole
-  // groups are loaded as raw bits before the poll and converted after it (converting here would
-  // hold the first poll back by a full round trip); other scale layouts load directly.
-  const bool raw_sc = in.iscale && in.sdt == DBF_F16 && c0 + 4 * (lane + 32) + 3 < in.cols;
-  uint2 sr0 = make_uint2(0, 0), sr1 = make_uint2(0, 0);
-  if (raw_sc) {
-    sr0 = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * lane));
-    sr1 = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * (lane + 32)));
-  } else {
-    load_scale4(in, c0 + 4 * lane, sc[0]);
-    load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
-  }
-  int npoll = 0;
-  if (dbg && lane == 0) dbg[0] = gtimer();
-  for (;;) {
-    const bool ok0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
-    const bool ok1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
-    ++npoll;
-    if (__all_sync(0xffffffffu, ok0 && ok1)) break;
-    if (kPollSleepNs) __nanosleep(kPollSleepNs);
-  }
-  if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[2] = npoll; }
-  if (raw_sc) {
-    const float2 a0 = __half22float2(*(const __half2*)&sr0.x), b0 = __half22float2(*(const __half2*)&sr0.y);
-    const float2 a1 = __half22float2(*(const __half2*)&sr1.x), b1 = __half22float2(*(const __half2*)&sr1.y);
-    sc[0][0] = a0.x, sc[0][1] = a0.y, sc[0][2] = b0.x, sc[0][3] = b0.y;
-    sc[1][0] = a1.x, sc[1][1] = a1.y, sc[1][2] = b1.x, sc[1][3] = b1.y;
-  }
+// Scale and quantize one chunk (this lane: groups lane and lane + 32) into the warp's
+// B-fragment scratch; see quantize_chunk.  Returns F and T = sum_j X_j.
+__device__ __forceinline__ void emit_digits(float (&u)[2][4], const float (&sc)[2][4], uint8_t* xs, int kb_stride,
+                                            int lane, int& F_out, int& T_out) {
   float mx = 0.f;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -294,6 +264,105 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
   T_out = ts;
 }
 
+// Quantize chunk c of the run's input (256 columns, warp-local) into this warp's B-fragment
+// scratch.  X_j = round(x_j * 2^F * kQScale) on a 13-bit grid relative to the CHUNK max
+// (|X| <= 4079); the MMA A bytes are 2^t * bit_j for k-block r = 4s + t (the packed word
+// pre-shifted by 4s: one shift per word serves four k-blocks), so the B operand carries
+// Y_j = X_j * 2^(3-t) as two balanced int8 digits (planes = MMA columns 0, 1; |Y| < 32640 keeps
+// both digits in [-128, 127]) and every k-block contributes 8 * sum bit_j X_j alike.
+// Returns F and T = sum_j X_j.
+__device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t epoch, uint8_t* xs, int kb_stride,
+                                               int& F_out, int& T_out, int64_t* dbg = nullptr) {
+  const int lane = threadIdx.x & 31;
+  float u[2][4], sc[2][4];
+  const int c0 = c * kChunkCols;
+  // groups q = lane and lane + 32 (64 groups of 4 columns per chunk).  fp16 scales of whole
+  // groups are loaded as raw bits before the poll and converted after it (converting here would
+  // hold the first poll back by a full round trip); other scale layouts load directly.
+  const bool raw_sc = in.iscale && in.sdt == DBF_F16 && c0 + 4 * (lane + 32) + 3 < in.cols;
+  uint2 sr0 = make_uint2(0, 0), sr1 = make_uint2(0, 0);
+  if (raw_sc) {
+    sr0 = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * lane));
+    sr1 = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * (lane + 32)));
+  } else {
+    load_scale4(in, c0 + 4 * lane, sc[0]);
+    load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
+  }
+  int npoll = 0;
+  if (dbg && lane == 0) dbg[0] = gtimer();
+  for (;;) {
+    const bool ok0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
+    const bool ok1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
+    ++npoll;
+    if (__all_sync(0xffffffffu, ok0 && ok1)) break;
+    if (kPollSleepNs) __nanosleep(kPollSleepNs);
+  }
+  if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[2] = npoll; }
+  if (raw_sc) {
+    const float2 a0 = __half22float2(*(const __half2*)&sr0.x), b0 = __half22float2(*(const __half2*)&sr0.y);
+    const float2 a1 = __half22float2(*(const __half2*)&sr1.x), b1 = __half22float2(*(const __half2*)&sr1.y);
+    sc[0][0] = a0.x, sc[0][1] = a0.y, sc[0][2] = b0.x, sc[0][3] = b0.y;
+    sc[1][0] = a1.x, sc[1][1] = a1.y, sc[1][2] = b1.x, sc[1][3] = b1.y;
+  }
+  emit_digits(u, sc, xs, kb_stride, lane, F_out, T_out);
+}
+
+// NB > 1 tokens: the same for every present token of chunk c, polling two tokens at a time
+// (their loads are in flight together instead of one round trip per token); absent tokens get
+// zero digits.
+template <int NB>
+__device__ __forceinline__ void quantize_chunk_tokens(const InSpec& in, int c, uint32_t epoch, uint8_t* xq, int batch,
+                                                      int (&F)[NB], int (&T)[NB]) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = c * kChunkCols;
+  constexpr int G = 2;  // tokens polled together (registers: G x 8 values per lane)
+  float sc[2][4];
+  // fp16 scales: raw bits before the first poll, converted after it (see quantize_chunk)
+  const bool raw_sc = in.iscale && in.sdt == DBF_F16 && c0 + 4 * (lane + 32) + 3 < in.cols;
+  uint2 sr0 = make_uint2(0, 0), sr1 = make_uint2(0, 0);
+  if (raw_sc) {
+    sr0 = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * lane));
+    sr1 = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * (lane + 32)));
+  } else {
+    load_scale4(in, c0 + 4 * lane, sc[0]);
+    load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
+  }
+#pragma unroll
+  for (int t0 = 0; t0 < NB; t0 += G) {
+    float u[G][2][4];
+    for (;;) {
+      bool ok = true;
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        if (t0 + i < batch) {
+          const InSpec it = token_of(in, t0 + i);
+          ok &= load_group(it, c0 + 4 * lane, epoch, u[i][0]);
+          ok &= load_group(it, c0 + 4 * (lane + 32), epoch, u[i][1]);
+        }
+      }
+      if (__all_sync(0xffffffffu, ok)) break;
+      if (kPollSleepNs) __nanosleep(kPollSleepNs);
+    }
+    if (t0 == 0 && raw_sc) {
+      const float2 a0 = __half22float2(*(const __half2*)&sr0.x), b0 = __half22float2(*(const __half2*)&sr0.y);
+      const float2 a1 = __half22float2(*(const __half2*)&sr1.x), b1 = __half22float2(*(const __half2*)&sr1.y);
+      sc[0][0] = a0.x, sc[0][1] = a0.y, sc[0][2] = b0.x, sc[0][3] = b0.y;
+      sc[1][0] = a1.x, sc[1][1] = a1.y, sc[1][2] = b1.x, sc[1][3] = b1.y;
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int t = t0 + i;
+      if (t < batch) {
+        emit_digits(u[i], sc, xq + t * 64, NB * 64, lane, F[t], T[t]);
+      } else {  // absent token: zero digits
+        for (int e = lane; e < 8 * 16; e += 32) *(uint32_t*)(xq + (e >> 4) * NB * 64 + t * 64 + (e & 15) * 4) = 0u;
+        __syncwarp();
+        F[t] = 0, T[t] = 0;
+      }
+    }
+  }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program prog, int ring_slots) {
   constexpr int kChunkQ = kChunkQBytes1 * NB, kPartFloats = kPartFloats1 * NB;
@@ -335,9 +404,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   __syncthreads();
   const dbf_engine_run* R = prog.runs;
 
-  if (warp == kProdWarp) {
+  if (warp >= kProdWarp) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
     // ---------------- producer: stream each run's packed signs (contiguous) into the ring -----
-    if (lane == 0) {
+    if (warp == kProdWarp && lane == 0) {
       const uint64_t pol = evict_first_policy();
       int slot = 0;
       uint32_t phase = 0;
@@ -369,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   }
 
   // ---------------- compute warps -------------------------------------------------------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kComputeRegs));
   const int g = lane >> 2, tig = lane & 3;
   const int batch = prog.batch < 1 ? 1 : prog.batch;  // tokens present (<= NB)
   uint8_t* xs = sm.xs + warp * xs_bytes<NB>();
@@ -443,39 +514,38 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     for (int c = warp; c < nch; c += kWarps) {
       const int qs = (c / kWarps) % xs_chunks<NB>();
       uint8_t* xq = xs + qs * kChunkQ;
-      int F[NB], T[NB];
-      if (reuse) {
-#pragma unroll
-        for (int t = 0; t < NB; ++t) F[t] = wq[(qs * NB + t) * 2], T[t] = wq[(qs * NB + t) * 2 + 1];
-      } else {
-#pragma unroll
-        for (int t = 0; t < NB; ++t) {
-          if (t < batch) {
+      // the chunk exponent F and quantized sum T of this lane's token tig (lanes tig >= NB hold
+      // mirrored columns that are discarded); every token's pair is kept in shared memory (wq)
+      // for reuse by the next run, and for NB > 1 the lanes pick theirs up from there
+      int Ft, Tt;
+      if constexpr (NB == 1) {
+        if (reuse) {
+          Ft = wq[2 * qs], Tt = wq[2 * qs + 1];
+        } else {
 #ifdef DBF_ENGINE_WARP_TRACE
-            quantize_chunk(token_of(in, t), c, ep_in, xq + t * 64, NB * 64, F[t], T[t],
-                           (wt && c == warp && t == 0) ? wt + 10 : nullptr);
+          quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt, (wt && c == warp) ? wt + 10 : nullptr);
 #else
-            quantize_chunk(token_of(in, t), c, ep_in, xq + t * 64, NB * 64, F[t], T[t]);
+          quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt);
 #endif
-          } else {  // absent token: zero digits
-            for (int e = lane; e < 8 * 16; e += 32)
-              *(uint32_t*)(xq + (e >> 4) * NB * 64 + t * 64 + (e & 15) * 4) = 0u;
-            __syncwarp();
-            F[t] = 0, T[t] = 0;
-          }
-          if (lane == 0) wq[(qs * NB + t) * 2] = F[t], wq[(qs * NB + t) * 2 + 1] = T[t];
+          if (lane == 0) wq[2 * qs] = Ft, wq[2 * qs + 1] = Tt;
         }
+      } else {
+        if (!reuse) {
+          int F[NB], T[NB];
+          quantize_chunk_tokens<NB>(in, c, ep_in, xq, batch, F, T);
+#pragma unroll
+          for (int t = 0; t < NB; ++t)
+            if (lane == 0) wq[(qs * NB + t) * 2] = F[t], wq[(qs * NB + t) * 2 + 1] = T[t];
+          __syncwarp();
+        }
+        const int2 ftt = *(const int2*)(wq + (qs * NB + (tig < NB ? tig : 0)) * 2);
+        Ft = ftt.x, Tt = ftt.y;
       }
       if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
       { const int jj = c / kWarps; if (jj < 3) WT(2 + jj); }
       uint2 b[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * NB * 64 + xlane);
-      // this lane's token tig: its chunk exponent and quantized sum
-      int Ft = F[0], Tt = T[0];
-#pragma unroll
-      for (int t = 1; t < NB; ++t)
-        if (tig == t) Ft = F[t], Tt = T[t];
       const float inv = __int_as_float((127 - Ft) << 23) * kQInv;  // 1 / (2^F * kQScale)
       // units in pairs: two independent MMA streams per warp (the second repeats the last unit
       // when nunits is odd and is then discarded)

@@ -43,6 +43,9 @@ constexpr int kProdWarp = kWarps;             // producer warp index (first warp
 constexpr int kThreads = (kWarps + 4) * 32;
 constexpr int kProdRegs = 24, kComputeRegs = 112;
 constexpr int kSlotBytes = 16384;             // one ring slot = 32 chunks of 512 B
+#ifndef DBF_CHAINS
+#define DBF_CHAINS 1  // accumulator chains per unit (1, 2, 4 measured within 1 %; 1 issues fewest)
+#endif
 constexpr int kMaxUnits = 8;                  // units per run (the host splits longer runs)
 #ifndef DBF_POLL_NS
 #define DBF_POLL_NS 32
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           if (slot >= ring_slots) slot -= ring_slots;
           w[h] = *((const uint4*)(sm.ring + (size_t)slot * kSlotBytes + (off & (kSlotBytes - 1))) + lane);
         }
-        int ac[2][2][4] = {};  // per unit: two independent accumulator chains
+        int ac[2][DBF_CHAINS][4] = {};  // per unit: independent accumulator chains
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           // k-block r = 4s + t reads (word >> 4s) & (0x01010101 << t): A bytes 2^t * bit
@@ -570,17 +573,16 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           const int sh = 4 * (r >> 2);
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            imma(ac[h][r & 1], (w[h].x >> sh) & m, (w[h].y >> sh) & m, (w[h].z >> sh) & m, (w[h].w >> sh) & m,
+            imma(ac[h][r % DBF_CHAINS], (w[h].x >> sh) & m, (w[h].y >> sh) & m, (w[h].z >> sh) & m, (w[h].w >> sh) & m,
                  b[r].x, b[r].y);
         }
         float v[2][2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           // columns 2*tig, 2*tig+1 (token tig's digit planes) of rows g, g+8: s = 8 * sum bit X
-          const int s0 = ac[h][0][0] + ac[h][1][0];
-          const int s1 = ac[h][0][1] + ac[h][1][1];
-          const int s2 = ac[h][0][2] + ac[h][1][2];
-          const int s3 = ac[h][0][3] + ac[h][1][3];
+          int s0 = ac[h][0][0], s1 = ac[h][0][1], s2 = ac[h][0][2], s3 = ac[h][0][3];
+#pragma unroll
+          for (int q = 1; q < DBF_CHAINS; ++q) s0 += ac[h][q][0], s1 += ac[h][q][1], s2 += ac[h][q][2], s3 += ac[h][q][3];
           v[h][0] = (float)(((s0 + 256 * s1) >> 2) - Tt) * inv;
           v[h][1] = (float)(((s2 + 256 * s3) >> 2) - Tt) * inv;
         }

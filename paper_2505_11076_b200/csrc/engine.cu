@@ -188,6 +188,19 @@ __device__ __forceinline__ void load_scale4(const InSpec& in, int col0, float (&
   for (int e = 0; e < 4; ++e) s[e] = col0 + e < in.cols ? ld_scale(in.iscale, in.sdt, col0 + e) : 0.f;
 }
 
+// Decode 4 LL words {fp16, epoch16} of columns col0..col0+3 (0 beyond cols); true if all carry epoch.
+__device__ __forceinline__ bool ll_group(const uint4 v, int col0, int cols, uint32_t epoch, float (&u)[4]) {
+  const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+  bool ok = true;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const bool inb = col0 + e < cols;
+    ok &= !inb || (vv[e] >> 16) == epoch;
+    u[e] = inb ? __half2float(__ushort_as_half((unsigned short)(vv[e] & 0xFFFFu))) : 0.f;
+  }
+  return ok;
+}
+
 // Load the 4 values of columns col0..col0+3; for LL vectors also report whether all carry `epoch`.
 // Columns >= cols read as 0.
 __device__ __forceinline__ bool load_group(const InSpec& in, int col0, uint32_t epoch, float (&u)[4]) {
@@ -308,6 +321,49 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
     sc[1][0] = a1.x, sc[1][1] = a1.y, sc[1][2] = b1.x, sc[1][3] = b1.y;
   }
   emit_digits(u, sc, xs, kb_stride, lane, F_out, T_out);
+}
+
+// Batch 1, LL input: the next chunk's LL words (and raw fp16 scales) are loaded while the
+// current chunk's MMAs run, so a warp that owns several chunks of a run pays the L2 round trip
+// once (the words are re-polled only if they were not yet published when prefetched).
+struct ChunkFetch {
+  uint4 v[2];
+  uint2 s[2];
+};
+__device__ __forceinline__ void fetch_issue(const InSpec& in, int c, int lane, ChunkFetch& f) {
+  const int c0 = c * kChunkCols;
+  f.v[0] = ld_ll16x4((const uint32_t*)in.x + c0 + 4 * lane);
+  f.v[1] = ld_ll16x4((const uint32_t*)in.x + c0 + 4 * (lane + 32));
+  if (in.iscale && in.sdt == DBF_F16 && c0 + 4 * (lane + 32) + 3 < in.cols) {
+    f.s[0] = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * lane));
+    f.s[1] = __ldg((const uint2*)((const __half*)in.iscale + c0 + 4 * (lane + 32)));
+  }
+}
+__device__ __forceinline__ void quantize_fetched(const InSpec& in, int c, uint32_t epoch, uint8_t* xs, int& F_out,
+                                                 int& T_out, const ChunkFetch& f) {
+  const int lane = threadIdx.x & 31;
+  float u[2][4], sc[2][4];
+  const int c0 = c * kChunkCols;
+  const bool ok0 = ll_group(f.v[0], c0 + 4 * lane, in.cols, epoch, u[0]);
+  const bool ok1 = ll_group(f.v[1], c0 + 4 * (lane + 32), in.cols, epoch, u[1]);
+  if (!__all_sync(0xffffffffu, ok0 && ok1)) {
+    for (;;) {  // not all published when prefetched: poll as usual
+      const bool p0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
+      const bool p1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
+      if (__all_sync(0xffffffffu, p0 && p1)) break;
+      if (kPollSleepNs) __nanosleep(kPollSleepNs);
+    }
+  }
+  if (in.iscale && in.sdt == DBF_F16 && c0 + 4 * (lane + 32) + 3 < in.cols) {
+    const float2 a0 = __half22float2(*(const __half2*)&f.s[0].x), b0 = __half22float2(*(const __half2*)&f.s[0].y);
+    const float2 a1 = __half22float2(*(const __half2*)&f.s[1].x), b1 = __half22float2(*(const __half2*)&f.s[1].y);
+    sc[0][0] = a0.x, sc[0][1] = a0.y, sc[0][2] = b0.x, sc[0][3] = b0.y;
+    sc[1][0] = a1.x, sc[1][1] = a1.y, sc[1][2] = b1.x, sc[1][3] = b1.y;
+  } else {
+    load_scale4(in, c0 + 4 * lane, sc[0]);
+    load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
+  }
+  emit_digits(u, sc, xs, 64, lane, F_out, T_out);
 }
 
 // NB > 1 tokens: the same for every present token of chunk c, polling two tokens at a time
@@ -514,6 +570,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       inkey[buf].iscale = in.iscale;
     }
     bool first = true;
+    ChunkFetch nf;
+    bool fetched = false;
     for (int c = warp; c < nch; c += kWarps) {
       const int qs = (c / kWarps) % xs_chunks<NB>();
       uint8_t* xq = xs + qs * kChunkQ;
@@ -525,12 +583,18 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         if (reuse) {
           Ft = wq[2 * qs], Tt = wq[2 * qs + 1];
         } else {
+          if (fetched) {
+            quantize_fetched(in, c, ep_in, xq, Ft, Tt, nf);
+          } else {
 #ifdef DBF_ENGINE_WARP_TRACE
-          quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt, (wt && c == warp) ? wt + 10 : nullptr);
+            quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt, (wt && c == warp) ? wt + 10 : nullptr);
 #else
-          quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt);
+            quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt);
 #endif
+          }
           if (lane == 0) wq[2 * qs] = Ft, wq[2 * qs + 1] = Tt;
+          fetched = in.kind == 1 && c + kWarps < nch;
+          if (fetched) fetch_issue(in, c + kWarps, lane, nf);
         }
       } else {
         if (!reuse) {

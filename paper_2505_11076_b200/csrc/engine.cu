@@ -59,7 +59,13 @@ constexpr float kQScale = 4079.f / 4096.f;    // keeps 8 * |X| below the two-dig
 constexpr float kQInv = 4096.f / 4079.f;
 constexpr int kChunkQBytes1 = 8 * 64;         // one quantized chunk: 8 k-blocks x (2 planes x 4 lanes x 8 B)
 constexpr int kPartFloats1 = kWarps * kMaxUnits * 16;  // one partial buffer
-template <int NB> constexpr int xs_chunks() { return NB <= 2 ? 2 : 1; }  // chunks a warp keeps for reuse
+// chunks a warp keeps quantized for reuse by the next run on the same input (a stage split over
+// several runs of one CTA): inputs up to 16 * xs_chunks chunks
+#ifndef DBF_XS_CHUNKS1
+#define DBF_XS_CHUNKS1 4  // 64 chunks: the 70B gate/up A stage (50 chunks, 3 runs per CTA) quantizes once
+#endif
+template <int NB> constexpr int xs_chunks() { return NB == 1 ? DBF_XS_CHUNKS1 : (NB == 2 ? 2 : 1); }
+inline int xs_chunks_of(int nb) { return nb == 1 ? DBF_XS_CHUNKS1 : (nb == 2 ? 2 : 1); }
 template <int NB> constexpr int xs_bytes() { return xs_chunks<NB>() * kChunkQBytes1 * NB; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -723,8 +729,8 @@ __global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; 
 
 // shared memory besides the per-slot parts (16 KB ring slot + 128 B record + 2 mbarriers)
 inline size_t fixed_smem(int nb) {
-  const int xs = (nb <= 2 ? 2 : 1) * kChunkQBytes1 * nb;
-  return (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 + (size_t)kWarps * 4 * 2 * 4 + 48 +
+  const int xs = xs_chunks_of(nb) * kChunkQBytes1 * nb;
+  return (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 + (size_t)kWarps * xs_chunks_of(nb) * nb * 2 * 4 + 48 +
          (size_t)kWarps * 8 + 128;
 }
 constexpr size_t kPerSlot = kSlotBytes + sizeof(dbf_engine_run) + 2 * 8;

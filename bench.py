@@ -318,10 +318,11 @@ def prefill_bench(model: str, bpw: float, tokens: int, steps: int, warmup: int):
 
 
 def sweep_bench(steps: int):
-    """BASELINE configs[3] / [4] at one GPU: the decode engine (batch 1 and 4: up to 4 tokens share
-    every MMA) over Llama-2-70B shapes at 2 bpw and Llama-2-13B shapes across bits/weight, plus 13B
-    at batch 8 (int8 tensor-core GEMV chain) and batch 64 (tcgen05 prefill chain); every number is
-    a full model step of linears."""
+    """BASELINE configs[3] / [4] at one GPU: the decode engine over Llama-2-70B shapes at 2 bpw
+    (batch 1, 4, 16) and Llama-2-13B shapes across bits/weight (batch 1, 4, 8), plus 13B at batch 8
+    through the int8 GEMV layer chain and batch 64 through the tcgen05 prefill chain.  Up to 4
+    tokens share every MMA of one engine launch; larger batches run consecutive launches over
+    groups of 4.  Every number is a full model step of linears."""
     import torch
 
     from paper_2505_11076_b200.plan import llama_decode_plan
@@ -338,8 +339,9 @@ def sweep_bench(steps: int):
         ms = time_graph(plan._graph, steps, 3)
         b = plan.bytes_per_step()
         rows.append({"model": model, "bpw": bpw, "batch": batch,
-                     "path": "engine" if engine else ("tcgen05 prefill chain" if batch >= 64 else
-                                                      "int8 GEMV chain (pre-quantized batch)"),
+                     "path": (("engine" if batch <= 4 else f"engine, {-(-batch // 4)} launches of <= 4 tokens")
+                              if engine else ("tcgen05 prefill chain" if batch >= 64 else
+                                              "int8 GEMV chain (pre-quantized batch)")),
                      "ms_per_step": ms, "gbs": b / (ms * 1e-3) / 1e9,
                      "tokens_per_s_linears_only": batch * 1e3 / ms, "layers": len(plan.ops)})
         del plan
@@ -347,10 +349,12 @@ def sweep_bench(steps: int):
 
     one("llama2-70b", 2.0, 1, True)
     one("llama2-70b", 2.0, 4, True)
+    one("llama2-70b", 2.0, 16, True)
     for bpw in (1.0, 1.5, 2.0, 2.3):
         one("llama2-13b", bpw, 1, True)
     one("llama2-7b", 2.0, 4, True)
     one("llama2-13b", 1.5, 4, True)
+    one("llama2-13b", 1.5, 8, True)
     one("llama2-13b", 1.5, 8, False)
     one("llama2-13b", 1.5, 64, False)
     return rows

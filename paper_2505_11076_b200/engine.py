@@ -282,3 +282,24 @@ class EngineProgram:
 
     def kernel_launches_per_step(self) -> int:
         return 2  # the engine kernel + the one-thread epoch advance
+
+
+class EngineGroups:
+    """Batches above 4 tokens: one EngineProgram per group of <= 4 token rows, launched back to
+    back on the same stream (each group re-reads the weights; tokens never interact)."""
+
+    def __init__(self, groups):
+        self.groups = list(groups)
+
+    def launch(self, stream=None):
+        for g in self.groups:
+            g.launch(stream)
+
+    def kernel_launches_per_step(self) -> int:
+        return sum(g.kernel_launches_per_step() for g in self.groups)
+
+    def enable_trace(self):
+        for g in self.groups:
+            g.enable_trace()
+        return self
+

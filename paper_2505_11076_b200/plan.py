@@ -68,10 +68,21 @@ class DecodePlan:
 
     # ---- execution --------------------------------------------------------------------------
     def use_engine(self, grid: int | None = None):
-        """Run the whole chain in the persistent decode engine (one kernel per step)."""
-        from .engine import EngineProgram
+        """Run the whole chain in the persistent decode engine (one kernel per step).  One engine
+        launch carries up to 4 tokens (they share every tensor-core MMA); larger batches run as
+        consecutive launches over groups of <= 4 token rows of the same buffers."""
+        from .engine import EngineGroups, EngineProgram
 
-        self.engine = EngineProgram(self, grid=grid)
+        batch = int(self.buffers[self.input_buffer].shape[0])
+        if batch <= 4:
+            self.engine = EngineProgram(self, grid=grid)
+        else:
+            groups = []
+            for t0 in range(0, batch, 4):
+                sub = DecodePlan(self.layers, self.ops, [b[t0:t0 + 4] for b in self.buffers],
+                                 input_buffer=self.input_buffer, output_buffer=self.output_buffer)
+                groups.append(EngineProgram(sub, grid=grid))
+            self.engine = EngineGroups(groups)
         self._graph = None
         return self
 

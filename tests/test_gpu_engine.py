@@ -106,3 +106,24 @@ def test_batched_engine_matches_layer_chain(batch):
     g1.manual_seed(40 + batch)
     plan1 = llama_decode_plan("llama2-7b", bpw=2.0, batch=1, blocks=1, generator=g1).use_engine(grid=148)
     assert torch.equal(_run(plan1, x[:1]), out[:1])
+
+
+def test_engine_batch_8_runs_in_groups_of_4():
+    """8 tokens = two engine launches over token rows 0-3 and 4-7: each group equals a batch-4
+    engine over the same rows, and the whole matches the per-layer chain within tolerance."""
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    plan = llama_decode_plan("llama2-7b", bpw=2.0, batch=8, blocks=1, generator=g)
+    x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
+    ref = _run(plan.use_layer_kernels(), x)
+    out = _run(plan.use_engine(), x)
+    assert plan.engine.kernel_launches_per_step() == 4
+    for t in range(8):
+        ok, err = _close(out[t:t + 1], ref[t:t + 1])
+        assert ok, (t, err)
+    g4 = torch.Generator(device="cuda")
+    g4.manual_seed(77)
+    plan4 = llama_decode_plan("llama2-7b", bpw=2.0, batch=4, blocks=1, generator=g4).use_engine()
+    assert torch.equal(_run(plan4, x[4:]), out[4:])

@@ -378,11 +378,43 @@ __device__ __forceinline__ void quantize_fetched(const InSpec& in, int c, uint32
 // (their loads are in flight together instead of one round trip per token); absent tokens get
 // zero digits.
 template <int NB>
+__device__ __forceinline__ void emit_tokens(float (&u)[2][2][4], const float (&sc)[2][4], uint8_t* xq, int t0,
+                                            int batch, int lane, int (&F)[NB], int (&T)[NB]) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int t = t0 + i;
+    if (t < batch) {
+      emit_digits(u[i], sc, xq + t * 64, NB * 64, lane, F[t], T[t]);
+    } else {  // absent token: zero digits
+      for (int e = lane; e < 8 * 16; e += 32) *(uint32_t*)(xq + (e >> 4) * NB * 64 + t * 64 + (e & 15) * 4) = 0u;
+      __syncwarp();
+      F[t] = 0, T[t] = 0;
+    }
+  }
+}
+template <int NB>
+__device__ __forceinline__ void poll_tokens(const InSpec& in, int c0, int t0, int batch, uint32_t epoch, int lane,
+                                            float (&u)[2][2][4]) {
+  for (;;) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (t0 + i < batch) {
+        const InSpec it = token_of(in, t0 + i);
+        ok &= load_group(it, c0 + 4 * lane, epoch, u[i][0]);
+        ok &= load_group(it, c0 + 4 * (lane + 32), epoch, u[i][1]);
+      }
+    }
+    if (__all_sync(0xffffffffu, ok)) break;
+    if (kPollSleepNs) __nanosleep(kPollSleepNs);
+  }
+}
+
+template <int NB>
 __device__ __forceinline__ void quantize_chunk_tokens(const InSpec& in, int c, uint32_t epoch, uint8_t* xq, int batch,
-                                                      int (&F)[NB], int (&T)[NB]) {
+                                                      int (&F)[NB], int (&T)[NB], int64_t* dbg = nullptr) {
   const int lane = threadIdx.x & 31;
   const int c0 = c * kChunkCols;
-  constexpr int G = 2;  // tokens polled together (registers: G x 8 values per lane)
   float sc[2][4];
   // fp16 scales: raw bits before the first poll, converted after it (see quantize_chunk)
   const bool raw_sc = in.iscale && in.sdt == DBF_F16 && c0 + 4 * (lane + 32) + 3 < in.cols;
@@ -394,39 +426,49 @@ __device__ __forceinline__ void quantize_chunk_tokens(const InSpec& in, int c, u
     load_scale4(in, c0 + 4 * lane, sc[0]);
     load_scale4(in, c0 + 4 * (lane + 32), sc[1]);
   }
+  if (dbg && lane == 0) dbg[0] = gtimer();
+  float u[2][2][4];
+  poll_tokens<NB>(in, c0, 0, batch, epoch, lane, u);  // tokens 0, 1
+  if (raw_sc) {
+    const float2 a0 = __half22float2(*(const __half2*)&sr0.x), b0 = __half22float2(*(const __half2*)&sr0.y);
+    const float2 a1 = __half22float2(*(const __half2*)&sr1.x), b1 = __half22float2(*(const __half2*)&sr1.y);
+    sc[0][0] = a0.x, sc[0][1] = a0.y, sc[0][2] = b0.x, sc[0][3] = b0.y;
+    sc[1][0] = a1.x, sc[1][1] = a1.y, sc[1][2] = b1.x, sc[1][3] = b1.y;
+  }
+  if constexpr (NB > 2) {
+    // tokens 2, 3 of an LL input: their words are loaded now and stay in flight while tokens 0, 1
+    // are quantized (a second poll only if they were not all current)
+    uint4 v[2][2];
+    const bool ll = in.kind == 1;
+    if (ll) {
 #pragma unroll
-  for (int t0 = 0; t0 < NB; t0 += G) {
-    float u[G][2][4];
-    for (;;) {
-      bool ok = true;
-#pragma unroll
-      for (int i = 0; i < G; ++i) {
-        if (t0 + i < batch) {
-          const InSpec it = token_of(in, t0 + i);
-          ok &= load_group(it, c0 + 4 * lane, epoch, u[i][0]);
-          ok &= load_group(it, c0 + 4 * (lane + 32), epoch, u[i][1]);
+      for (int i = 0; i < 2; ++i) {
+        if (2 + i < batch) {
+          const uint32_t* x = (const uint32_t*)token_of(in, 2 + i).x;
+          v[i][0] = ld_ll16x4(x + c0 + 4 * lane);
+          v[i][1] = ld_ll16x4(x + c0 + 4 * (lane + 32));
         }
       }
-      if (__all_sync(0xffffffffu, ok)) break;
-      if (kPollSleepNs) __nanosleep(kPollSleepNs);
     }
-    if (t0 == 0 && raw_sc) {
-      const float2 a0 = __half22float2(*(const __half2*)&sr0.x), b0 = __half22float2(*(const __half2*)&sr0.y);
-      const float2 a1 = __half22float2(*(const __half2*)&sr1.x), b1 = __half22float2(*(const __half2*)&sr1.y);
-      sc[0][0] = a0.x, sc[0][1] = a0.y, sc[0][2] = b0.x, sc[0][3] = b0.y;
-      sc[1][0] = a1.x, sc[1][1] = a1.y, sc[1][2] = b1.x, sc[1][3] = b1.y;
-    }
+    if (dbg && lane == 0) dbg[1] = gtimer();
+    emit_tokens<NB>(u, sc, xq, 0, batch, lane, F, T);
+    if (dbg && lane == 0) dbg[3] = gtimer();
+    bool ok = ll;
+    if (ll) {
 #pragma unroll
-    for (int i = 0; i < G; ++i) {
-      const int t = t0 + i;
-      if (t < batch) {
-        emit_digits(u[i], sc, xq + t * 64, NB * 64, lane, F[t], T[t]);
-      } else {  // absent token: zero digits
-        for (int e = lane; e < 8 * 16; e += 32) *(uint32_t*)(xq + (e >> 4) * NB * 64 + t * 64 + (e & 15) * 4) = 0u;
-        __syncwarp();
-        F[t] = 0, T[t] = 0;
+      for (int i = 0; i < 2; ++i) {
+        if (2 + i < batch) {
+          ok &= ll_group(v[i][0], c0 + 4 * lane, in.cols, epoch, u[i][0]);
+          ok &= ll_group(v[i][1], c0 + 4 * (lane + 32), in.cols, epoch, u[i][1]);
+        }
       }
     }
+    if (!__all_sync(0xffffffffu, ok)) poll_tokens<NB>(in, c0, 2, batch, epoch, lane, u);
+    if (dbg && lane == 0) dbg[4] = gtimer();
+    emit_tokens<NB>(u, sc, xq, 2, batch, lane, F, T);
+    if (dbg && lane == 0) dbg[6] = gtimer();
+  } else {
+    emit_tokens<NB>(u, sc, xq, 0, batch, lane, F, T);
   }
 }
 
@@ -524,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 #ifdef DBF_ENGINE_WARP_TRACE
     // debug build only: per (run, warp) stamps [start, pieces, quantized x3, computed x3, barrier, final,
     // first chunk: poll start, poll success, poll count]
-    int64_t* wt = prog.trace ? prog.trace + 4 * (size_t)prog.cta_offsets[gridDim.x] + ((size_t)i * kWarps + warp) * 13
+    int64_t* wt = prog.trace ? prog.trace + 4 * (size_t)prog.cta_offsets[gridDim.x] + ((size_t)i * kWarps + warp) * 17
                              : nullptr;
 #define WT(k) do { if (wt && lane == 0) wt[k] = gtimer(); } while (0)
 #else
@@ -607,7 +649,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       } else {
         if (!reuse) {
           int F[NB], T[NB];
+#ifdef DBF_ENGINE_WARP_TRACE
+          quantize_chunk_tokens<NB>(in, c, ep_in, xq, batch, F, T, (wt && c == warp) ? wt + 10 : nullptr);
+#else
           quantize_chunk_tokens<NB>(in, c, ep_in, xq, batch, F, T);
+#endif
 #pragma unroll
           for (int t = 0; t < NB; ++t)
             if (lane == 0) wq[(qs * NB + t) * 2] = F[t], wq[(qs * NB + t) * 2 + 1] = T[t];

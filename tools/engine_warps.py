@@ -15,21 +15,22 @@ from paper_2505_11076_b200.engine import levels_of
 from paper_2505_11076_b200.plan import llama_decode_plan
 
 blocks = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
-plan = llama_decode_plan("llama2-7b", bpw=2.0, blocks=blocks, generator=g)
+plan = llama_decode_plan("llama2-7b", bpw=2.0, blocks=blocks, batch=batch, generator=g)
 plan.buffers[plan.input_buffer].normal_(generator=g)
 plan.use_engine()
 eng = plan.engine
 nr = eng.nruns
-eng.trace = torch.zeros(4 * nr + nr * 16 * 13, dtype=torch.int64, device="cuda")
+eng.trace = torch.zeros(4 * nr + nr * 16 * 17, dtype=torch.int64, device="cuda")
 eng._prog.trace = eng.trace.data_ptr()
 for _ in range(3):
     plan._eager()
 torch.cuda.synchronize()
 t = eng.trace.cpu().numpy().astype(np.int64)
 tr = t[: 4 * nr].reshape(nr, 4)
-wt = t[4 * nr:].reshape(nr, 16, 13)
+wt = t[4 * nr:].reshape(nr, 16, 17)
 lv = levels_of(plan.ops, plan.input_buffer)
 seg_stage = []
 for i in range(len(plan.ops)):
@@ -84,6 +85,13 @@ for s in range(per_block, 2 * per_block):
     print(f"{s:3d} {','.join(names[s]):22s} cta {c:3d} (prev crit {prev_crit}) runs-in-stage {np.sum(cta_of_run[runs] == c)} "
           f"start {W[act, 0].min() - prev:6d} pieces {W[act, 1].max() - prev:6d} q0(max warp) {q0:6d} "
           f"compute-done {lastc:6d} bar {W[act, 8].max() - prev:6d} pub {tr[j, 3] - prev:6d}")
+    if batch > 1:
+        Wa = W[act]
+        print(f"      tokens: entry med {int(np.median(Wa[:, 10] - prev))} pair0 polled {int(np.median(Wa[:, 11] - prev))} "
+              f"(polls max {Wa[:, 12].max()}) emitted {int(np.median(Wa[:, 13] - prev))} pair1 polled {int(np.median(Wa[:, 14] - prev))} "
+              f"(polls max {Wa[:, 15].max()}) emitted {int(np.median(Wa[:, 16] - prev))} max {int((Wa[:, 16] - prev).max())}")
+        prev_crit = c
+        continue
     ws = int(np.argmax(W[act, 2]))
     print(f"      slowest-q0 warp {ws}: poll start {W[act, 10][ws] - prev} success {W[act, 11][ws] - prev} polls {W[act, 12][ws]}; "
           f"all warps: poll start med {int(np.median(W[act, 10] - prev))} success med {int(np.median(W[act, 11] - prev))} "

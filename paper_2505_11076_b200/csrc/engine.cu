@@ -472,6 +472,51 @@ __device__ __forceinline__ void quantize_chunk_tokens(const InSpec& in, int c, u
   }
 }
 
+// The MMAs of units u0 and u0 + 1 (has1) against chunk c of the run (signs resident in the ring),
+// as the two units' fp32 chunk sums v[unit][row g / g + 8] of this lane's token.
+__device__ __forceinline__ void pair_mma(const uint8_t* ring, int ring_slots, int slot0, int nch, int c, int u0,
+                                         bool has1, const uint2 (&b)[8], int Tt, float inv, int lane,
+                                         float (&v)[2][2]) {
+        uint4 w[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int off = ((u0 + (h && has1 ? 1 : 0)) * nch + c) * kChunkBytes;
+          int slot = slot0 + (off >> 14);
+          if (slot >= ring_slots) slot -= ring_slots;
+          w[h] = *((const uint4*)(ring + (size_t)slot * kSlotBytes + (off & (kSlotBytes - 1))) + lane);
+        }
+        int ac[2][DBF_CHAINS][4] = {};  // per unit: independent accumulator chains
+        if (has1) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          // k-block r = 4s + t reads (word >> 4s) & (0x01010101 << t): A bytes 2^t * bit
+          const uint32_t m = 0x01010101u << (r & 3);
+          const int sh = 4 * (r >> 2);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            imma(ac[h][r % DBF_CHAINS], (w[h].x >> sh) & m, (w[h].y >> sh) & m, (w[h].z >> sh) & m, (w[h].w >> sh) & m,
+                 b[r].x, b[r].y);
+        }
+        } else {  // odd last unit: one MMA stream (its pair partner would be discarded)
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const uint32_t m = 0x01010101u << (r & 3);
+            const int sh = 4 * (r >> 2);
+            imma(ac[0][r % DBF_CHAINS], (w[0].x >> sh) & m, (w[0].y >> sh) & m, (w[0].z >> sh) & m,
+                 (w[0].w >> sh) & m, b[r].x, b[r].y);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          // columns 2*tig, 2*tig+1 (token tig's digit planes) of rows g, g+8: s = 8 * sum bit X
+          int s0 = ac[h][0][0], s1 = ac[h][0][1], s2 = ac[h][0][2], s3 = ac[h][0][3];
+#pragma unroll
+          for (int q = 1; q < DBF_CHAINS; ++q) s0 += ac[h][q][0], s1 += ac[h][q][1], s2 += ac[h][q][2], s3 += ac[h][q][3];
+          v[h][0] = (float)(((s0 + 256 * s1) >> 2) - Tt) * inv;
+          v[h][1] = (float)(((s2 + 256 * s3) >> 2) - Tt) * inv;
+        }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program prog, int ring_slots) {
   constexpr int kChunkQ = kChunkQBytes1 * NB, kPartFloats = kPartFloats1 * NB;
@@ -622,6 +667,44 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     bool first = true;
     ChunkFetch nf;
     bool fetched = false;
+    // A run whose input chunks are all quantized already (reuse) deals the chunk residue classes
+    // rotated by `rot` per unit pair, so warps that own one chunk more than others (nch not a
+    // multiple of 16) alternate with those that own one less.  A warp's partial for a unit is still
+    // one residue class summed in chunk order, and the finalize sums residues 0..15 in order:
+    // bitwise the same result as the unrotated dealing.
+#ifdef DBF_ROT
+    const int rot = (reuse && (nch & (kWarps - 1))) ? kWarps / 2 : 0;
+#else
+    const int rot = 0;
+#endif
+    if (rot) {
+#pragma unroll
+      for (int p = 0; p < kMaxUnits / 2; ++p) {
+        const int u0 = 2 * p;
+        if (u0 >= nunits) break;
+        const bool has1 = u0 + 1 < nunits;
+        const int res = (warp + p * rot) & (kWarps - 1);
+        const uint8_t* oxs = sm.xs + res * xs_bytes<NB>();
+        const int* oq = qft + res * xs_chunks<NB>() * NB * 2;
+        for (int c = res; c < nch; c += kWarps) {
+          const int qs = (c / kWarps) % xs_chunks<NB>();
+          const uint8_t* xq = oxs + qs * kChunkQ;
+          const int2 ftt = *(const int2*)(oq + (qs * NB + (tig < NB ? tig : 0)) * 2);
+          uint2 b[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * NB * 64 + xlane);
+          const float inv = __int_as_float((127 - ftt.x) << 23) * kQInv;
+          float v[2][2];
+          pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, ftt.y, inv, lane, v);
+          acc0[u0] += v[0][0];
+          acc1[u0] += v[0][1];
+          if (u0 + 1 < kMaxUnits && has1) {
+            acc0[u0 + 1] += v[1][0];
+            acc1[u0 + 1] += v[1][1];
+          }
+        }
+      }
+    } else
     for (int c = warp; c < nch; c += kWarps) {
       const int qs = (c / kWarps) % xs_chunks<NB>();
       uint8_t* xq = xs + qs * kChunkQ;
@@ -675,35 +758,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         const int u0 = 2 * p;
         if (u0 >= nunits) break;
         const bool has1 = u0 + 1 < nunits;
-        uint4 w[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int off = ((u0 + (h && has1 ? 1 : 0)) * nch + c) * kChunkBytes;
-          int slot = slot0 + (off >> 14);
-          if (slot >= ring_slots) slot -= ring_slots;
-          w[h] = *((const uint4*)(sm.ring + (size_t)slot * kSlotBytes + (off & (kSlotBytes - 1))) + lane);
-        }
-        int ac[2][DBF_CHAINS][4] = {};  // per unit: independent accumulator chains
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          // k-block r = 4s + t reads (word >> 4s) & (0x01010101 << t): A bytes 2^t * bit
-          const uint32_t m = 0x01010101u << (r & 3);
-          const int sh = 4 * (r >> 2);
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            imma(ac[h][r % DBF_CHAINS], (w[h].x >> sh) & m, (w[h].y >> sh) & m, (w[h].z >> sh) & m, (w[h].w >> sh) & m,
-                 b[r].x, b[r].y);
-        }
         float v[2][2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          // columns 2*tig, 2*tig+1 (token tig's digit planes) of rows g, g+8: s = 8 * sum bit X
-          int s0 = ac[h][0][0], s1 = ac[h][0][1], s2 = ac[h][0][2], s3 = ac[h][0][3];
-#pragma unroll
-          for (int q = 1; q < DBF_CHAINS; ++q) s0 += ac[h][q][0], s1 += ac[h][q][1], s2 += ac[h][q][2], s3 += ac[h][q][3];
-          v[h][0] = (float)(((s0 + 256 * s1) >> 2) - Tt) * inv;
-          v[h][1] = (float)(((s2 + 256 * s3) >> 2) - Tt) * inv;
-        }
+        pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, Tt, inv, lane, v);
         acc0[u0] += v[0][0];
         acc1[u0] += v[0][1];
         if (u0 + 1 < kMaxUnits && has1) {
@@ -748,7 +804,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         if (t < NB && t < batch && row < rows) {
           float v = 0.f;
 #pragma unroll
-          for (int w2 = 0; w2 < kWarps; ++w2) v += part[((w2 * kMaxUnits + fu) * NB + t) * 16 + (lane & 15)];
+          for (int r = 0; r < kWarps; ++r) {  // residue classes in order (warp = residue when rot == 0)
+            const int w2 = (r - (fu >> 1) * rot) & (kWarps - 1);
+            v += part[((w2 * kMaxUnits + fu) * NB + t) * 16 + (lane & 15)];
+          }
           v *= osc_row;
           const __half h = __float2half_rn(v);
           if (ll_out) st_ll16(ll_out + t * out_ll_stride + row, h, ep_out);

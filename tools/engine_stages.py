@@ -16,7 +16,8 @@ blocks = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
-plan = llama_decode_plan("llama2-7b", bpw=2.0, blocks=blocks, batch=batch, generator=g)
+import os
+plan = llama_decode_plan(os.environ.get("DBF_MODEL", "llama2-7b"), bpw=2.0, blocks=blocks, batch=batch, generator=g)
 plan.buffers[plan.input_buffer].normal_(generator=g)
 plan.use_engine()
 eng = plan.engine

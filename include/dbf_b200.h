@@ -296,6 +296,9 @@ int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t nsegments,
 
 /* Largest run the engine accepts at this batch: units per run and packed-sign bytes per run. */
 int dbf_engine_run_limits(int32_t batch, int32_t* max_units, int64_t* max_run_bytes);
+/* The same for a program whose widest segment has max_cols columns (at batch 1 the quantized-input
+ * store grows with max_cols and the sign ring shrinks accordingly). */
+int dbf_engine_run_limits_cols(int32_t max_cols, int32_t batch, int32_t* max_units, int64_t* max_run_bytes);
 /* Dynamic shared memory the engine needs for max_cols at this batch (1..4); DBF_ERR_UNSUPPORTED if
  * it cannot fit. */
 int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* bytes);

@@ -64,9 +64,17 @@ constexpr int kPartFloats1 = kWarps * kMaxUnits * 16;  // one partial buffer
 #ifndef DBF_XS_CHUNKS1
 #define DBF_XS_CHUNKS1 4  // 64 chunks: the 70B gate/up A stage (50 chunks, 3 runs per CTA) quantizes once
 #endif
-template <int NB> constexpr int xs_chunks() { return NB == 1 ? DBF_XS_CHUNKS1 : (NB == 2 ? 2 : 1); }
-inline int xs_chunks_of(int nb) { return nb == 1 ? DBF_XS_CHUNKS1 : (nb == 2 ? 2 : 1); }
-template <int NB> constexpr int xs_bytes() { return xs_chunks<NB>() * kChunkQBytes1 * NB; }
+#ifndef DBF_XS_CHUNKS1_MAX
+#define DBF_XS_CHUNKS1_MAX 7  // 112 chunks: the 70B down.B stage (m = 28672) quantizes its input once
+#endif
+// batch 1 sizes the quantized-chunk store from the program's widest input (one slot per 16
+// chunks, so a stage of any width up to 16 * DBF_XS_CHUNKS1_MAX chunks quantizes once per CTA);
+// the ring gets the rest of shared memory
+inline int xs_chunks_of(int nb, int max_cols = 0) {
+  if (nb != 1) return nb == 2 ? 2 : 1;
+  const int need = (int)((chunks(max_cols) + kWarps - 1) / kWarps);
+  return need <= DBF_XS_CHUNKS1 ? DBF_XS_CHUNKS1 : DBF_XS_CHUNKS1_MAX;  // the two batch-1 instantiations
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -502,9 +510,13 @@ __device__ __forceinline__ void pair_mma(const uint8_t* ring, int ring_slots, in
           for (int r = 0; r < 8; ++r) {
             const uint32_t m = 0x01010101u << (r & 3);
             const int sh = 4 * (r >> 2);
-            imma(ac[0][r % DBF_CHAINS], (w[0].x >> sh) & m, (w[0].y >> sh) & m, (w[0].z >> sh) & m,
-                 (w[0].w >> sh) & m, b[r].x, b[r].y);
+            // the idle second unit's accumulators carry a second chain (half the dependent MMA
+            // latency: single-unit runs are the widest segments' case)
+            imma(ac[r & 1][0], (w[0].x >> sh) & m, (w[0].y >> sh) & m, (w[0].z >> sh) & m, (w[0].w >> sh) & m,
+                 b[r].x, b[r].y);
           }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ac[0][0][e] += ac[1][0][e];
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -517,22 +529,25 @@ __device__ __forceinline__ void pair_mma(const uint8_t* ring, int ring_slots, in
         }
 }
 
-template <int NB>
+template <int NB, int XS>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program prog, int ring_slots) {
   constexpr int kChunkQ = kChunkQBytes1 * NB, kPartFloats = kPartFloats1 * NB;
+  // quantized chunks kept per warp (xs_chunks_of: sized by the program's widest input at batch 1)
+  constexpr int xsc = XS;
+  constexpr int xsb = xsc * kChunkQ;
   extern __shared__ __align__(128) uint8_t smem[];
   Smem sm;
   sm.ring = smem;
   sm.hdr = (dbf_engine_run*)(sm.ring + (size_t)ring_slots * kSlotBytes);
   sm.xs = (uint8_t*)(sm.hdr + ring_slots);
-  sm.part = (float*)(sm.xs + kWarps * xs_bytes<NB>());
+  sm.part = (float*)(sm.xs + kWarps * xsb);
   sm.full = (uint64_t*)(sm.part + 2 * kPartFloats);
   sm.empty = sm.full + ring_slots;
   // rarely-read per-warp / per-CTA scalars live in shared memory, not in (spilled) registers:
   // the quantized chunks' F and T for reuse across runs, the launch's epoch base, and each
   // warp's ring cursor {next first slot, full-barrier parities}
   int* qft = (int*)(sm.empty + ring_slots);  // [kWarps][xs_chunks][NB][2]
-  uint32_t* ep_base_s = (uint32_t*)(qft + kWarps * xs_chunks<NB>() * NB * 2);
+  uint32_t* ep_base_s = (uint32_t*)(qft + kWarps * xsc * NB * 2);
   // input key (vector, input scale) of the quantized chunks, double-buffered by run parity: run j
   // reads slot (j+1)&1 (written by warp 0 during run j-1, before that run's barrier) and writes j&1
   struct InKey { const void* iscale; int vec; int pad; };
@@ -596,12 +611,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kComputeRegs));
   const int g = lane >> 2, tig = lane & 3;
   const int batch = prog.batch < 1 ? 1 : prog.batch;  // tokens present (<= NB)
-  uint8_t* xs = sm.xs + warp * xs_bytes<NB>();
+  uint8_t* xs = sm.xs + warp * xsb;
   // this lane's B fragment in a k-block: column g = 2*token + plane (columns >= 2*NB mirror)
   const int xlane = ((lane >> 2) % (2 * NB)) * 32 + (lane & 3) * 8;
   // the quantized chunks stay valid for the next run when it reads the same vector with the same
   // input scale (a stage's units split over several runs of one CTA)
-  int* wq = qft + warp * xs_chunks<NB>() * NB * 2;  // this warp's [xs_chunks][NB][F, T]
+  int* wq = qft + warp * xsc * NB * 2;  // this warp's [xs_chunks][NB][F, T]
   if (lane == 0) cursor[warp] = make_int2(0, 0);  // {first slot of the next run, full parities}
   __syncwarp();
   for (int i = r0; i < r1; ++i) {
@@ -657,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       osc_bits = in.sdt == DBF_F16 ? (uint32_t)ld_nc_u16((const unsigned short*)oscale + r)
                                    : ld_nc_u32((const uint32_t*)oscale + r);
     }
-    constexpr int kReuseChunks = xs_chunks<NB>() * kWarps;
+    constexpr int kReuseChunks = xsc * kWarps;
     const InKey prev = inkey[buf ^ 1];
     const bool reuse = H.in_vec == prev.vec && in.iscale == prev.iscale && nch <= kReuseChunks;
     if (warp == 0 && lane == 0) {
@@ -684,10 +699,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         if (u0 >= nunits) break;
         const bool has1 = u0 + 1 < nunits;
         const int res = (warp + p * rot) & (kWarps - 1);
-        const uint8_t* oxs = sm.xs + res * xs_bytes<NB>();
-        const int* oq = qft + res * xs_chunks<NB>() * NB * 2;
+        const uint8_t* oxs = sm.xs + res * xsb;
+        const int* oq = qft + res * xsc * NB * 2;
         for (int c = res; c < nch; c += kWarps) {
-          const int qs = (c / kWarps) % xs_chunks<NB>();
+          const int qs = (c / kWarps) % xsc;
           const uint8_t* xq = oxs + qs * kChunkQ;
           const int2 ftt = *(const int2*)(oq + (qs * NB + (tig < NB ? tig : 0)) * 2);
           uint2 b[8];
@@ -706,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
       }
     } else
     for (int c = warp; c < nch; c += kWarps) {
-      const int qs = (c / kWarps) % xs_chunks<NB>();
+      const int qs = (c / kWarps) % xsc;
       uint8_t* xq = xs + qs * kChunkQ;
       // the chunk exponent F and quantized sum T of this lane's token tig (lanes tig >= NB hold
       // mirrored columns that are discarded); every token's pair is kept in shared memory (wq)
@@ -833,14 +848,18 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
 __global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; }
 
 // shared memory besides the per-slot parts (16 KB ring slot + 128 B record + 2 mbarriers)
-inline size_t fixed_smem(int nb) {
-  const int xs = xs_chunks_of(nb) * kChunkQBytes1 * nb;
-  return (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 + (size_t)kWarps * xs_chunks_of(nb) * nb * 2 * 4 + 48 +
+inline size_t fixed_smem(int nb, int xsc) {
+  const int xs = xsc * kChunkQBytes1 * nb;
+  return (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 + (size_t)kWarps * xsc * nb * 2 * 4 + 48 +
          (size_t)kWarps * 8 + 128;
 }
 constexpr size_t kPerSlot = kSlotBytes + sizeof(dbf_engine_run) + 2 * 8;
-inline int ring_slots(int nb = 1) { return std::min((int)((kMaxSmem - fixed_smem(nb)) / kPerSlot), kMaxSlots); }
-inline size_t smem_bytes(int slots, int nb = 1) { return (size_t)slots * kPerSlot + fixed_smem(nb); }
+inline int ring_slots(int nb, int max_cols) {
+  return std::min((int)((kMaxSmem - fixed_smem(nb, xs_chunks_of(nb, max_cols))) / kPerSlot), kMaxSlots);
+}
+inline size_t smem_bytes(int slots, int nb, int max_cols) {
+  return (size_t)slots * kPerSlot + fixed_smem(nb, xs_chunks_of(nb, max_cols));
+}
 inline int nb_for(int batch) { return batch <= 1 ? 1 : (batch <= 2 ? 2 : 4); }
 
 }  // namespace engine
@@ -857,6 +876,8 @@ extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t
     return DBF_ERR_INVALID_ARGUMENT;
   // units producing each vector (one segment writes each LL vector)
   std::vector<uint32_t> producers(nvectors, 0);
+  int max_cols = 1;
+  for (int s = 0; s < nsegments; ++s) max_cols = std::max(max_cols, (int)segments[s].cols);
   for (int s = 0; s < nsegments; ++s) {
     const dbf_engine_segment& g = segments[s];
     if (g.rows < 1 || g.cols < 1 || !g.tiled || g.in_vec < 0 || g.in_vec >= nvectors || g.out_vec >= nvectors)
@@ -874,8 +895,8 @@ extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t
       return DBF_ERR_SHAPE;
     if (n > engine::kMaxUnits ||
         (int64_t)n * chunks(g.cols) * kChunkBytes >
-            (int64_t)(engine::ring_slots(engine::nb_for(batch)) / 2) * engine::kSlotBytes)
-      return DBF_ERR_SHAPE;  // split longer runs (dbf_engine_run_limits)
+            (int64_t)(engine::ring_slots(engine::nb_for(batch), max_cols) / 2) * engine::kSlotBytes)
+      return DBF_ERR_SHAPE;  // split longer runs (dbf_engine_run_limits_cols)
     const dbf_engine_vector& vin = vectors[g.in_vec];
     if (vin.len != g.cols) return DBF_ERR_SHAPE;
     dbf_engine_run r;
@@ -909,20 +930,25 @@ extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t
 extern "C" int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* bytes) {
   if (max_cols < 1 || !bytes || batch < 1 || batch > 4) return DBF_ERR_INVALID_ARGUMENT;
   const int nb = engine::nb_for(batch);
-  const int slots = engine::ring_slots(nb);
+  const int slots = engine::ring_slots(nb, max_cols);
   // one 16-row unit of the widest segment must fit half the ring
   if (slots < engine::kMinSlots || chunks(max_cols) * kChunkBytes > (int64_t)(slots / 2) * engine::kSlotBytes)
     return DBF_ERR_UNSUPPORTED;
-  *bytes = engine::smem_bytes(slots, nb);
+  *bytes = engine::smem_bytes(slots, nb, max_cols);
+  return DBF_OK;
+}
+
+extern "C" int dbf_engine_run_limits_cols(int32_t max_cols, int32_t batch, int32_t* max_units,
+                                          int64_t* max_run_bytes) {
+  if (!max_units || !max_run_bytes || batch < 1 || batch > 4 || max_cols < 0) return DBF_ERR_INVALID_ARGUMENT;
+  *max_units = engine::kMaxUnits;
+  // a run's signs stay resident until every compute warp is done with it; leave room to prefetch
+  *max_run_bytes = (int64_t)(engine::ring_slots(engine::nb_for(batch), max_cols) / 2) * engine::kSlotBytes;
   return DBF_OK;
 }
 
 extern "C" int dbf_engine_run_limits(int32_t batch, int32_t* max_units, int64_t* max_run_bytes) {
-  if (!max_units || !max_run_bytes || batch < 1 || batch > 4) return DBF_ERR_INVALID_ARGUMENT;
-  *max_units = engine::kMaxUnits;
-  // a run's signs stay resident until every compute warp is done with it; leave room to prefetch
-  *max_run_bytes = (int64_t)(engine::ring_slots(engine::nb_for(batch)) / 2) * engine::kSlotBytes;
-  return DBF_OK;
+  return dbf_engine_run_limits_cols(0, batch, max_units, max_run_bytes);
 }
 
 template <typename K>
@@ -945,18 +971,20 @@ extern "C" int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, in
   size_t smem = 0;
   int st = dbf_engine_smem_bytes(max_cols, 1, &smem);
   if (st != DBF_OK) return st;
-  return engine_occupancy_of(engine::engine_kernel<1>, smem, blocks_per_sm, regs_per_thread);
+  return engine::xs_chunks_of(1, max_cols) == DBF_XS_CHUNKS1
+             ? engine_occupancy_of(engine::engine_kernel<1, DBF_XS_CHUNKS1>, smem, blocks_per_sm, regs_per_thread)
+             : engine_occupancy_of(engine::engine_kernel<1, DBF_XS_CHUNKS1_MAX>, smem, blocks_per_sm, regs_per_thread);
 }
 
-template <int NB>
+template <int NB, int XS>
 static int engine_launch_nb(const dbf_engine_program* program, cudaStream_t s) {
   size_t smem = 0;
   int st = dbf_engine_smem_bytes(program->max_cols, NB, &smem);
   if (st != DBF_OK) return st;
-  const int slots = engine::ring_slots(NB);
+  const int slots = engine::ring_slots(NB, program->max_cols);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel<NB, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          engine::kMaxSmem);
     if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
     configured = true;
@@ -972,7 +1000,7 @@ static int engine_launch_nb(const dbf_engine_program* program, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   dbf_engine_program prog = *program;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, engine::engine_kernel<NB>, prog, slots);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, engine::engine_kernel<NB, XS>, prog, slots);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   return DBF_OK;
 }
@@ -983,8 +1011,13 @@ extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream
     return DBF_ERR_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   const int nb = engine::nb_for(program->batch);
-  const int st = nb == 1 ? engine_launch_nb<1>(program, s)
-                         : (nb == 2 ? engine_launch_nb<2>(program, s) : engine_launch_nb<4>(program, s));
+  int st;
+  if (nb == 1)
+    st = engine::xs_chunks_of(1, program->max_cols) == DBF_XS_CHUNKS1
+             ? engine_launch_nb<1, DBF_XS_CHUNKS1>(program, s)
+             : engine_launch_nb<1, DBF_XS_CHUNKS1_MAX>(program, s);
+  else
+    st = nb == 2 ? engine_launch_nb<2, 2>(program, s) : engine_launch_nb<4, 1>(program, s);
   if (st != DBF_OK) return st;
   engine::advance_run_kernel<<<1, 1, 0, s>>>(program->run_counter);
   return check_launch();

@@ -74,10 +74,12 @@ def occupancy(max_cols: int) -> tuple[int, int]:
     return b.value, r.value
 
 
-def run_limits(batch: int = 1) -> tuple[int, int]:
-    """(units per run, packed-sign bytes per run) the engine accepts at this batch."""
+def run_limits(batch: int = 1, max_cols: int = 0) -> tuple[int, int]:
+    """(units per run, packed-sign bytes per run) the engine accepts at this batch for a program
+    whose widest segment has max_cols columns."""
     u, b = ctypes.c_int32(0), ctypes.c_int64(0)
-    _lib.check(_lib.lib.dbf_engine_run_limits(batch, ctypes.byref(u), ctypes.byref(b)), "dbf_engine_run_limits")
+    _lib.check(_lib.lib.dbf_engine_run_limits_cols(max_cols, batch, ctypes.byref(u), ctypes.byref(b)),
+               "dbf_engine_run_limits_cols")
     return u.value, b.value
 
 
@@ -206,7 +208,7 @@ class EngineProgram:
             rot = (rot + len(units)) % self.grid
         # compress each CTA's unit list into runs: consecutive row blocks of one segment, at most
         # max_units units / max_run_bytes of packed signs each (dbf_engine_run_limits)
-        max_units, max_bytes = run_limits(self.batch)
+        max_units, max_bytes = run_limits(self.batch, max(sg[2] for sg in segs))
         unit_bytes = {j: ((sg[2] + 255) // 256) * 512 for j, sg in enumerate(segs)}
         per_cta_runs: list[list[tuple[int, int, int]]] = []
         for lst in per_cta:

@@ -405,11 +405,23 @@ def sharded_bench(world: int, rank: int, steps: int, warmup: int, barrier, dist=
             g_n = graph_of(lambda: [s.forward(X) for s in shards])
             g_f = graph_of(lambda: [ar.forward(s, X) for s in shards])
             us = [mx(time_graph(gr, steps, warmup, barrier)) * 1e3 / inst for gr in (g_p, g_n, g_f)]
-            rows.append({"layer": name, "n": n, "k": k, "m": m, "batch": batch, "k_shard": [k0, k1],
-                         "instances": inst, "us_partial": us[0], "us_nccl_path": us[1], "us_fused": us[2],
-                         "us_allreduce_nccl": us[1] - us[0], "us_allreduce_fused": us[2] - us[0],
-                         "gbs_per_rank_fused": bytes_rank / (us[2] * 1e-6) / 1e9,
-                         "fused_vs_nccl_max_rel_diff": diff})
+            row = {"layer": name, "n": n, "k": k, "m": m, "batch": batch, "k_shard": [k0, k1],
+                   "instances": inst, "us_partial": us[0], "us_nccl_path": us[1], "us_fused": us[2],
+                   "us_allreduce_nccl": us[1] - us[0], "us_allreduce_fused": us[2] - us[0],
+                   "gbs_per_rank_fused": bytes_rank / (us[2] * 1e-6) / 1e9,
+                   "fused_vs_nccl_max_rel_diff": diff}
+            if batch <= 4:  # the partial through the decode engine (one launch per shard layer)
+                y_e = shards[0].forward(X, engine=True)
+                torch.cuda.synchronize()
+                row["engine_vs_nccl_max_rel_diff"] = float(
+                    ((y_e.float() - y_n.float()).abs().max() / y_n.float().abs().max().clamp_min(1e-30)).item())
+                g_pe = graph_of(lambda: [s.partial_engine(X) for s in shards])
+                g_ne = graph_of(lambda: [s.forward(X, engine=True) for s in shards])
+                ue = [mx(time_graph(gr, steps, warmup, barrier)) * 1e3 / inst for gr in (g_pe, g_ne)]
+                row.update({"us_partial_engine": ue[0], "us_nccl_path_engine": ue[1],
+                            "gbs_per_rank_partial_engine": bytes_rank / (ue[0] * 1e-6) / 1e9})
+                del g_pe, g_ne
+            rows.append(row)
             del g_p, g_n, g_f, shards, ar
             torch.cuda.empty_cache()
     return {"world": world, "model": "llama2-70b", "bpw": 2.0,

@@ -239,7 +239,8 @@ typedef struct {
   const void* iscale;   /* per-column input scale or NULL */
   const void* oscale;   /* per-row output scale or NULL */
   int32_t scale_dtype;  /* F16 / F32 */
-  int32_t out_dtype;    /* F16: LL values are rounded through fp16 (and out_plain is fp16); F32 */
+  int32_t out_dtype;    /* LL values are always rounded through fp16; out_plain is fp16 (F16) or the
+                           unrounded fp32 value (F32) */
   void* out_plain;      /* optional plain output (out_dtype), NULL if unused */
 } dbf_engine_segment;
 
@@ -283,6 +284,11 @@ typedef struct {
   int32_t grid;                       /* CTAs (<= number of SMs; one per SM)                    */
   int32_t max_cols;                   /* largest segment `cols` (sizes shared memory)          */
   int32_t batch;                      /* tokens per step, 1..4 (vectors hold batch rows each)   */
+  /* per-launch I/O (NULL = as built): x_override replaces the data of vector 0 (a plain input,
+   * batch x len contiguous) and y_override the out_plain pointer of every segment that has one,
+   * so one program serves calls on different input / output buffers without rebuilding runs */
+  const void* x_override;
+  void* y_override;
 } dbf_engine_program;
 
 /*

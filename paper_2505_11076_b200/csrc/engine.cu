@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     const dbf_engine_run& H = sm.hdr[slot0];
     const int cols = H.cols, nunits = H.nunits;
     InSpec in;
-    in.x = H.x;
+    in.x = (H.in_vec == 0 && prog.x_override) ? prog.x_override : H.x;
     in.iscale = H.iscale;
     in.kind = H.in_kind;
     in.dtype = H.in_dtype;
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     const int rows = H.rows, rb = H.rb, odt = H.out_dtype;
     const int64_t out_ll_stride = (int64_t)((rows + kChunkCols - 1) / kChunkCols) * kChunkCols;
     const void* oscale = H.oscale;
-    void* out_plain = H.out_plain;
+    void* out_plain = (H.out_plain && prog.y_override) ? prog.y_override : H.out_plain;
     uint32_t* ll_out = (uint32_t*)H.ll_out;
     const uint32_t ep_out = epoch16(*ep_base_s, H.out_vec);
     const int nch = (cols + kChunkCols - 1) / kChunkCols;
@@ -828,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           if (ll_out) st_ll16(ll_out + t * out_ll_stride + row, h, ep_out);
           if (out_plain) {
             if (odt == DBF_F16) ((__half*)out_plain)[(int64_t)t * rows + row] = h;
-            else ((float*)out_plain)[(int64_t)t * rows + row] = __half2float(h);
+            else ((float*)out_plain)[(int64_t)t * rows + row] = v;  // fp32 output: unrounded
           }
         }
       }

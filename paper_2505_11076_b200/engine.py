@@ -52,6 +52,8 @@ class _Program(ctypes.Structure):
         ("grid", ctypes.c_int32),
         ("max_cols", ctypes.c_int32),
         ("batch", ctypes.c_int32),
+        ("x_override", ctypes.c_void_p),
+        ("y_override", ctypes.c_void_p),
     ]
 
 
@@ -179,7 +181,7 @@ class EngineProgram:
         stage_units: dict[int, list[tuple[int, int]]] = {}
         for i, op in enumerate(plan.ops):
             layer = plan.layers[op.layer]
-            sd = _lib.dtype_code(layer.a.dtype)
+            sd = _lib.dtype_code(layer.mid.dtype)
             if sd not in (_lib.F16, _lib.F32):
                 raise ValueError("engine scales must be float16 or float32")
             if op.src not in latest:  # read before any op wrote it: an external (plain) input
@@ -192,8 +194,12 @@ class EngineProgram:
             segs.append((layer.B.tiled.data_ptr(), layer.k, layer.m_dim, src_vec, t_vec, layer.b.data_ptr(),
                          layer.mid.data_ptr(), sd, _lib.F32, 0))
             out_plain = plan.buffers[op.dst].data_ptr() if i == final_op else 0
-            segs.append((layer.A.tiled.data_ptr(), layer.n, layer.k, t_vec, y_vec, 0, layer.a.data_ptr(), sd,
-                         act_code, out_plain))
+            out_code = _lib.dtype_code(plan.buffers[op.dst].dtype) if i == final_op else act_code
+            if out_code not in (_lib.F16, _lib.F32):
+                raise ValueError("engine outputs must be float16 or float32")
+            # layer.a None: no output scale (a k-shard's partial; the scale follows the all-reduce)
+            segs.append((layer.A.tiled.data_ptr(), layer.n, layer.k, t_vec, y_vec, 0,
+                         layer.a.data_ptr() if layer.a is not None else 0, sd, out_code, out_plain))
             latest[op.dst] = y_vec
             for stage, seg_idx, rows in ((2 * lv[i], len(segs) - 2, layer.k), (2 * lv[i] + 1, len(segs) - 1, layer.n)):
                 stage_units.setdefault(stage, []).extend((seg_idx, rb) for rb in range((rows + 15) // 16))
@@ -281,6 +287,19 @@ class EngineProgram:
 
     def launch(self, stream=None):
         _lib.check(_lib.lib.dbf_engine_launch(ctypes.byref(self._prog), _lib.stream_ptr(stream)), "dbf_engine_launch")
+
+    def launch_io(self, x, y, stream=None):
+        """Launch on caller buffers: x replaces the step input (vector 0: batch x len, contiguous,
+        the dtype the program was built for) and y the final plain output."""
+        inp = self.plan.buffers[self.plan.input_buffer]
+        out = self.plan.buffers[self.plan.output_buffer]
+        if x.shape != inp.shape or x.dtype != inp.dtype or not x.is_contiguous():
+            raise ValueError(f"x must be a contiguous {tuple(inp.shape)} {inp.dtype} tensor")
+        if y.shape != out.shape or y.dtype != out.dtype or not y.is_contiguous():
+            raise ValueError(f"y must be a contiguous {tuple(out.shape)} {out.dtype} tensor")
+        prog = _Program.from_buffer_copy(self._prog)
+        prog.x_override, prog.y_override = x.data_ptr(), y.data_ptr()
+        _lib.check(_lib.lib.dbf_engine_launch(ctypes.byref(prog), _lib.stream_ptr(stream)), "dbf_engine_launch")
 
     def kernel_launches_per_step(self) -> int:
         return 2  # the engine kernel + the one-thread epoch advance

@@ -97,6 +97,20 @@ def shard_layer(layer, rank: int, world: int, align: int = 32) -> LayerShard:
 
 
 @dataclass(frozen=True)
+class _LayerView:
+    """The fields EngineProgram reads from a layer (a = None: no output scale)."""
+
+    A: object
+    B: object
+    a: object
+    mid: object
+    b: object
+    n: int
+    k: int
+    m_dim: int
+
+
+@dataclass(frozen=True)
 class _ShardShape:
     rank: int
     world: int
@@ -159,6 +173,36 @@ class DeviceShard:
         )
         return P
 
+    def partial_engine(self, X):
+        """The same fp32 partial through the persistent decode engine (batch <= 4, fp16 / fp32
+        input): one cooperative launch runs GEMV1 and GEMV2 with the LL handoff of t between them
+        (engine numerics: 13-bit input grid per 256-column chunk, t rounded to fp16; the partial
+        itself is not rounded).  The program is built once per (batch, dtype) and then reads X and
+        writes P through the launch-time I/O overrides, so calls cost one engine launch."""
+        import torch
+
+        from .engine import EngineProgram
+        from .plan import DecodePlan, PlanOp
+
+        X2 = X if X.ndim == 2 else X.unsqueeze(0)
+        X2 = X2.contiguous()
+        batch = X2.shape[0]
+        if not 1 <= batch <= 4 or X2.dtype not in (torch.float16, torch.float32):
+            raise ValueError("partial_engine runs 1..4 fp16/fp32 tokens (use partial for others)")
+        key = (batch, X2.dtype, X2.device)
+        progs = self.__dict__.setdefault("_engine_progs", {})
+        if key not in progs:
+            sh = self.shard
+            view = _LayerView(self.A, self.B, None, self.mid, self.b, sh.n, sh.k_shard, sh.m_dim)
+            bufs = [torch.zeros((batch, sh.m_dim), dtype=X2.dtype, device=X2.device),
+                    torch.zeros((batch, sh.n), dtype=torch.float32, device=X2.device)]
+            plan = DecodePlan([view], [PlanOp(0, 0, 1, "partial")], bufs, input_buffer=0, output_buffer=1)
+            progs[key] = (EngineProgram(plan), plan)
+        prog, _ = progs[key]
+        P = torch.empty((batch, self.shard.n), dtype=torch.float32, device=X2.device)
+        prog.launch_io(X2, P)
+        return P
+
     def finalize(self, P, out_dtype=None):
         import torch
 
@@ -174,11 +218,12 @@ class DeviceShard:
         )
         return Y
 
-    def forward(self, X, group=None, out_dtype=None):
-        """y = a * all_reduce_sum(P_g): one NCCL SUM all-reduce of n x batch fp32 values."""
+    def forward(self, X, group=None, out_dtype=None, engine: bool = False):
+        """y = a * all_reduce_sum(P_g): one NCCL SUM all-reduce of n x batch fp32 values
+        (engine=True computes P_g with partial_engine)."""
         import torch.distributed as dist
 
-        P = self.partial(X)
+        P = self.partial_engine(X) if engine else self.partial(X)
         if dist.is_initialized():  # a single process without a group has nothing to reduce
             dist.all_reduce(P, op=dist.ReduceOp.SUM, group=group)
         return self.finalize(P, out_dtype=out_dtype or X.dtype)

@@ -43,6 +43,30 @@ def test_simulated_shards_sum_to_the_full_forward(world, n, k, m, batch):
     assert rel_max(y, ref) <= 1e-2 and rel_norm(y, ref) <= 1e-2
 
 
+@pytest.mark.parametrize("world,n,k,m,batch", [(2, 1024, 1792, 8192, 1), (4, 2048, 3000, 4096, 3), (2, 1000, 600, 777, 4)])
+def test_engine_partials_sum_to_the_full_forward(world, n, k, m, batch):
+    """partial_engine (one decode-engine launch per shard, launch-time I/O buffers): the shards'
+    fp32 partials summed and finalized match the oracle forward within the fp16 tolerance, and a
+    second call on other buffers gives the same bits."""
+    import torch
+
+    rng = np.random.default_rng(world * 11 + batch)
+    layer = _host_layer(rng, n, k, m)
+    X = rng.standard_normal((batch, m)).astype(np.float16)
+    Xd = torch.from_numpy(X).cuda()
+    total = None
+    for r in range(world):
+        ds = sharded.DeviceShard(sharded.shard_layer(layer, r, world), scale_dtype=torch.float16)
+        p = ds.partial_engine(Xd)
+        assert torch.equal(ds.partial_engine(Xd.clone()), p)
+        q = ds.partial(Xd)
+        assert rel_max(p.cpu().numpy(), q.cpu().numpy()) <= 1e-2
+        total = p if total is None else total + p
+    y = ds.finalize(total, out_dtype=torch.float32).cpu().numpy()
+    ref = oracle.c_forward(X.astype(np.float64), layer.a, layer.A.bits, layer.mid, layer.B.bits, layer.b)
+    assert rel_max(y, ref) <= 1e-2 and rel_norm(y, ref) <= 1e-2
+
+
 def test_nccl_single_rank_group():
     import torch
     import torch.distributed as dist

@@ -332,6 +332,10 @@ int dbf_pair_signs(const uint32_t* words, int64_t rows, int64_t word_pitch, uint
 /* row pitch (elements) of the fp16 intermediate t in the prefill workspace */
 int64_t dbf_prefill_ld(int64_t cols);
 size_t dbf_prefill_workspace_bytes(int64_t k, int64_t tokens);
+/* Workspace that also holds the split-K fp32 partials used for tokens <= 256 (the two GEMMs then
+ * run over ~148 CTAs instead of rows/128; partials are summed in split order, deterministic).  A
+ * workspace of only dbf_prefill_workspace_bytes runs the same GEMMs without splitting K. */
+size_t dbf_prefill_workspace_bytes_nkm(int64_t n, int64_t k, int64_t m, int64_t tokens);
 
 /* Diagnostics: with DBF_PREFILL_TRACE set in the environment, the last sign GEMM launch records
  * per-K-block clock64 stamps of CTA (0,0); copies n int64 of them to host memory. */

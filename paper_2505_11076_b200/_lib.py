@@ -79,6 +79,7 @@ SIGNATURES: dict[str, tuple] = {
         [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _vp],
     ),
     "dbf_prefill_workspace_bytes": (_sz, [_i64, _i64]),
+    "dbf_prefill_workspace_bytes_nkm": (_sz, [_i64, _i64, _i64, _i64]),
     "dbf_sign_gemm": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
     "dbf_forward_prefill": (
         _int,

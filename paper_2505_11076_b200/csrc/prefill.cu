@@ -26,6 +26,7 @@
 //                rscale[row], fp16 store.
 // Ring stage s couples a smem activation tile and a TMEM A slot; both are released by the
 // tcgen05.commit of the MMAs that read them.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -72,6 +73,13 @@ struct Params {
   int rows, K, T;
   int num_kb;
   long long* trace;        // debug: per-K-block clock64 stamps of CTA (0,0), or nullptr
+  // small token counts (T <= 256): the MMA N and the activation box shrink to the tokens present
+  // (n_mma, act_bytes), and K may be split over gridDim.z CTAs (kb_per_split K blocks each) that
+  // store unscaled fp32 partials part[z][tok][row] for split_reduce_kernel (part == nullptr: no split)
+  int n_mma;
+  int act_bytes;
+  int kb_per_split;
+  float* part;
 };
 
 struct __align__(8) Barriers {
@@ -111,6 +119,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = blockIdx.x * BM;
   const int tok0 = blockIdx.y * BN;
+  const int kb0 = p.part ? (int)blockIdx.z * p.kb_per_split : 0;  // this CTA's K blocks [kb0, kb1)
+  const int kb1 = p.part ? min(p.num_kb, kb0 + p.kb_per_split) : p.num_kb;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -147,12 +157,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const int prod = warp == 0 ? 0 : warp - 1;
       const uint64_t pol = policy_evict_last();  // activations are re-read by every row tile
-      for (int kb = prod; kb < p.num_kb; kb += kNumProducers) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
+      for (int kb = kb0 + prod; kb < kb1; kb += kNumProducers) {
+        const int s = (kb - kb0) % STAGES;
+        const uint32_t ph = ((kb - kb0) / STAGES) & 1;
         mbar_wait(&bar.empty[s], ph ^ 1);
         if (tracing) p.trace[5 * p.num_kb + kb] = clock64();
-        mbar_arrive_expect_tx(&bar.full_act[s], kActStageBytes);
+        mbar_arrive_expect_tx(&bar.full_act[s], MC ? kActStageBytes : p.act_bytes);
         if constexpr (MC)
           tma_load_2d_mc(act + (size_t)s * kActStageBytes + rank * (kActStageBytes / 2), &act_map, kb * BK,
                          tok0 + (int)rank * (BN / 2), &bar.full_act[s], (uint16_t)0x3, pol);
@@ -163,10 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_f32(UM, BN);
-      for (int kb = 0; kb < p.num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
+      const uint32_t idesc = idesc_f16_f32(UM, MC ? BN : p.n_mma);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int s = (kb - kb0) % STAGES;
+        const uint32_t ph = ((kb - kb0) / STAGES) & 1;
         mbar_wait(&bar.full_act[s], ph);
         if (tracing) p.trace[4 * kb + 3] = clock64();
         mbar_wait(&bar.full_a[s], ph);
@@ -180,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int h = 0; h < MH; ++h)
             mma_f16_ts(tmem + kAccCol + h * BN, a_base + h * kAColsPerHalf + kk * (UK / 2), bd, idesc,
-                       (kb | kk) != 0);
+                       (kb != kb0) || (kk != 0));
         }
         if constexpr (MC) mma_commit_mc(&bar.empty[s], (uint16_t)0x3);
         else mma_commit(&bar.empty[s]);
@@ -197,52 +207,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool live = grow < p.rows;
     const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
     const uint4* wrow = reinterpret_cast<const uint4*>(p.words + (int64_t)(live ? grow : 0) * p.pitch);
-    // one uint4 = words 4i..4i+3 = K blocks 2i (.x/.y) and 2i+1 (.z/.w); prefetched one ahead
+    // one uint4 = words 4i..4i+3 = K blocks 2i (.x/.y) and 2i+1 (.z/.w).  Groups of 8 K blocks
+    // (4 quads): the next group's quads are loaded when a group starts, so each load has 8 K blocks
+    // of MMA time to arrive (one quad ahead was too short for N = 64 tiles: HBM latency-bound)
     const int nquads = (p.num_kb + 1) >> 1;
-    uint4 cur = make_uint4(0, 0, 0, 0), nxt = live ? __ldg(wrow) : make_uint4(0, 0, 0, 0);
+    uint4 q[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      q[i] = (live && (kb0 >> 1) + i < nquads) ? __ldg(wrow + (kb0 >> 1) + i) : make_uint4(0, 0, 0, 0);
     const bool tr = tracing && threadIdx.x == 32 * kExpWarp0;
-    for (int kb = 0; kb < p.num_kb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      if ((kb & 1) == 0) {
-        cur = nxt;
-        if (live && (kb >> 1) + 1 < nquads) nxt = __ldg(wrow + (kb >> 1) + 1);
-      }
-      const uint32_t w = (kb & 1) ? (half ? cur.w : cur.z) : (half ? cur.y : cur.x);
-      uint32_t ks[16];
-      if constexpr (KSCALE) {
-        const uint4* src = reinterpret_cast<const uint4*>(ks_smem + kb * (BK / 2) + half * 16);
+    for (int kg = kb0; kg < kb1; kg += 8) {  // kb0 is even (splits are whole quads)
+      uint4 nq[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint4 u = src[i];
-          ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
+      for (int i = 0; i < 4; ++i) {
+        const int qi = (kg >> 1) + 4 + i;
+        nq[i] = (live && qi < nquads && 2 * qi < kb1) ? __ldg(wrow + qi) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int kb = kg + j;
+        if (kb >= kb1) break;
+        const int s = (kb - kb0) % STAGES;
+        const uint32_t ph = ((kb - kb0) / STAGES) & 1;
+        const uint32_t w = (j & 1) ? (half ? q[j >> 1].w : q[j >> 1].z) : (half ? q[j >> 1].y : q[j >> 1].x);
+        uint32_t ks[16];
+        if constexpr (KSCALE) {
+          const uint4* src = reinterpret_cast<const uint4*>(ks_smem + kb * (BK / 2) + half * 16);
+  #pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint4 u = src[i];
+            ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
+          }
+        } else {
+  #pragma unroll
+          for (int i = 0; i < 16; ++i) ks[i] = 0x3C003C00u;
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) ks[i] = 0x3C003C00u;
+        uint32_t v[16];
+        expand_word(w, ks, v);
+        if (tr) p.trace[4 * kb] = clock64();
+        if (lane == 0) mbar_wait(&bar.empty[s], ph ^ 1);  // one poller per warp
+        __syncwarp();
+        if (tr) p.trace[4 * kb + 1] = clock64();
+        tc_fence_after();
+        tmem_st16(tmem + lane_addr + kACol0 + s * kAColsPerStage + mh * kAColsPerHalf + half * 16, v);
+        tmem_wait_st();
+        tc_fence_before();
+        if (tr) p.trace[4 * kb + 2] = clock64();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar.full_a[s]);
       }
-      uint32_t v[16];
-      expand_word(w, ks, v);
-      if (tr) p.trace[4 * kb] = clock64();
-      if (lane == 0) mbar_wait(&bar.empty[s], ph ^ 1);  // one poller per warp
-      __syncwarp();
-      if (tr) p.trace[4 * kb + 1] = clock64();
-      tc_fence_after();
-      tmem_st16(tmem + lane_addr + kACol0 + s * kAColsPerStage + mh * kAColsPerHalf + half * 16, v);
-      tmem_wait_st();
-      tc_fence_before();
-      if (tr) p.trace[4 * kb + 2] = clock64();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar.full_a[s]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) q[i] = nq[i];
     }
     // epilogue: this warp stores tokens [half*64, half*64+64) of its 32 rows (accumulator mh)
     if (lane == 0) mbar_wait(&bar.acc_full, 0);
     __syncwarp();
     tc_fence_after();
     const float rs = (live && p.rscale) ? __half2float(p.rscale[grow]) : 1.f;
+    float* part = p.part ? p.part + (size_t)blockIdx.z * p.T * p.rows : nullptr;
 #pragma unroll 1
     for (int c = 0; c < BN / 64; ++c) {
       const int col = half * (BN / 2) + c * 32;
+      if (tok0 + col >= p.T) break;  // columns past the tokens present (the MMA N may be smaller)
       uint32_t acc[32];
       tmem_ld32(tmem + lane_addr + kAccCol + mh * BN + col, acc);
       tmem_wait_ld();
@@ -250,7 +276,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int tok = tok0 + col + j;
-          if (tok < p.T) p.out[(int64_t)tok * p.ldo + grow] = __float2half_rn(__uint_as_float(acc[j]) * rs);
+          if (tok < p.T) {
+            if (part) part[(size_t)tok * p.rows + grow] = __uint_as_float(acc[j]);
+            else p.out[(int64_t)tok * p.ldo + grow] = __float2half_rn(__uint_as_float(acc[j]) * rs);
+          }
         }
       }
     }
@@ -298,9 +327,40 @@ static int make_act_map(CUtensorMap* map, const void* act, int64_t T, int64_t K,
 
 static long long* trace_buf = nullptr;
 
+// out[tok][row] = fp16(rscale[row] * sum_z part[z][tok][row]), splits summed in order (deterministic)
+__global__ void split_reduce_kernel(const float* __restrict__ part, int splits, int T, int rows,
+                                    const __half* __restrict__ rscale, __half* __restrict__ out, int64_t ldo) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)T * rows) return;
+  const int row = (int)(i % rows);
+  const int64_t tok = i / rows;
+  float v = 0.f;
+  for (int z = 0; z < splits; ++z) v += __ldcs(part + (size_t)z * T * rows + i);
+  out[tok * ldo + row] = __float2half_rn(v * (rscale ? __half2float(rscale[row]) : 1.f));
+}
+
+// K splits for a launch of `tiles` output tiles: enough CTAs to cover the SMs once, each split a
+// whole number of K-block pairs and at least kMinSplitKb K blocks.  1 = no split.
+constexpr int kMinSplitKb = 8;
+inline int split_count(int64_t tiles, int num_kb, int* kb_per_split) {
+  int S = (int)std::max<int64_t>(1, kNumSMs / std::max<int64_t>(tiles, 1));
+  S = std::min(S, std::max(1, num_kb / kMinSplitKb));
+  int kps = (int)ceil_div(num_kb, S);
+  kps += kps & 1;
+  S = (int)ceil_div(num_kb, kps);
+  *kb_per_split = kps;
+  return S;
+}
+inline size_t split_bytes(int64_t T, int64_t K, int64_t rows) {
+  if (T > BN) return 0;  // large token counts fill the GPU with token tiles
+  int kps = 0;
+  const int S = split_count(ceil_div(rows, BM), (int)ceil_div(K, BK), &kps);
+  return S > 1 ? (size_t)S * T * rows * sizeof(float) : 0;
+}
+
 static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_act, const uint32_t* words,
                             int64_t pitch, int64_t rows, const __half* kscale, const __half* rscale, __half* out,
-                            int64_t ldo, cudaStream_t stream) {
+                            int64_t ldo, cudaStream_t stream, float* split_ws = nullptr, size_t split_ws_bytes = 0) {
   if (T < 1 || K < 1 || rows < 1) return DBF_ERR_INVALID_ARGUMENT;
   if ((ld_act * 2) % 16 != 0 || ((uintptr_t)act & 15) != 0 || ld_act < K) return DBF_ERR_UNSUPPORTED;
   if (((uintptr_t)words & 15) != 0 || pitch % 4 != 0) return DBF_ERR_UNSUPPORTED;
@@ -308,8 +368,10 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   if (T > INT32_MAX || rows > INT32_MAX || K > INT32_MAX) return DBF_ERR_UNSUPPORTED;
   if (kscale && K > kMaxKScale) return DBF_ERR_UNSUPPORTED;
   static const bool mc = getenv("DBF_PREFILL_MULTICAST") != nullptr;  // measured slower
+  // T <= BN: one token tile whose MMA N / activation box cover only the tokens present
+  const int n_mma = T >= BN ? BN : (int)ceil_div(T, 16) * 16;
   CUtensorMap map;
-  int st = make_act_map(&map, act, T, K, ld_act, mc ? BN / 2 : BN);
+  int st = make_act_map(&map, act, T, K, ld_act, mc ? BN / 2 : n_mma);
   if (st != DBF_OK) return st;
   Params p;
   p.words = words;
@@ -322,13 +384,27 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   p.K = (int)K;
   p.T = (int)T;
   p.num_kb = (int)ceil_div(K, BK);
+  p.n_mma = n_mma;
+  p.act_bytes = n_mma * BK * 2;
+  p.kb_per_split = p.num_kb;
+  p.part = nullptr;
+  int splits = 1;
+  if (!mc && T <= BN) {
+    int kps = 0;
+    const int S = split_count(ceil_div(rows, BM), p.num_kb, &kps);
+    if (S > 1 && split_ws && split_ws_bytes >= (size_t)S * T * rows * sizeof(float)) {
+      splits = S;
+      p.kb_per_split = kps;
+      p.part = split_ws;
+    }
+  }
   p.trace = nullptr;
   if (getenv("DBF_PREFILL_TRACE")) {
     if (!trace_buf) cudaMalloc(&trace_buf, 8 * 6 * 4096);
     p.trace = trace_buf;
   }
   const unsigned gx = (unsigned)ceil_div(rows, BM);
-  dim3 grid(mc ? (gx + 1) / 2 * 2 : gx, (unsigned)ceil_div(T, BN));
+  dim3 grid(mc ? (gx + 1) / 2 * 2 : gx, (unsigned)ceil_div(T, BN), (unsigned)splits);
   const size_t smem = smem_bytes(p.num_kb, kscale != nullptr);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -351,6 +427,11 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   if (mc) e = kscale ? go(sign_gemm_kernel<true, true>) : go(sign_gemm_kernel<false, true>);
   else e = kscale ? go(sign_gemm_kernel<true, false>) : go(sign_gemm_kernel<false, false>);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  st = check_launch();
+  if (st != DBF_OK || splits == 1) return st;
+  const int64_t total = T * rows;
+  split_reduce_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, stream>>>(p.part, splits, (int)T, (int)rows, rscale,
+                                                                          out, ldo);
   return check_launch();
 }
 
@@ -384,6 +465,12 @@ int dbf_sign_gemm(const void* act, int64_t tokens, int64_t K, int64_t ld_act, co
                                    (const __half*)rscale, (__half*)out, ldo, (cudaStream_t)stream);
 }
 
+size_t dbf_prefill_workspace_bytes_nkm(int64_t n, int64_t k, int64_t m, int64_t tokens) {
+  if (n < 1 || k < 1 || m < 1 || tokens < 1) return 0;
+  const size_t t = (dbf_prefill_workspace_bytes(k, tokens) + 255) & ~(size_t)255;
+  return t + std::max(prefill::split_bytes(tokens, m, k), prefill::split_bytes(tokens, k, n));
+}
+
 int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired, int64_t B_pitch,
                         const void* a, const void* mid, const void* b, int64_t n, int64_t k, int64_t m,
                         const void* X, int64_t tokens, int64_t ldx, void* Y, int64_t ldy, void* workspace,
@@ -396,11 +483,15 @@ int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_
   const int64_t ldt = dbf_prefill_ld(k);
   __half* t = (__half*)workspace;
   cudaStream_t s = (cudaStream_t)stream;
+  // split-K partials after t when the workspace has room (dbf_prefill_workspace_bytes_nkm)
+  const size_t tb = (dbf_prefill_workspace_bytes(k, tokens) + 255) & ~(size_t)255;
+  float* sw = workspace_bytes > tb ? (float*)((char*)workspace + tb) : nullptr;
+  const size_t swb = workspace_bytes > tb ? workspace_bytes - tb : 0;
   int st = prefill::launch_sign_gemm(X, tokens, m, ldx, B_paired, B_pitch, k, (const __half*)b,
-                                     (const __half*)mid, t, ldt, s);
+                                     (const __half*)mid, t, ldt, s, sw, swb);
   if (st != DBF_OK) return st;
   return prefill::launch_sign_gemm(t, tokens, k, ldt, A_paired, A_pitch, n, nullptr, (const __half*)a,
-                                   (__half*)Y, ldy, s);
+                                   (__half*)Y, ldy, s, sw, swb);
 }
 
 }  // extern "C"

@@ -122,7 +122,10 @@ def forward_prefill(X, layer: DeviceLayer, out=None):
     A, B = layer.A.paired, layer.B.paired
     fused = PREFILL_FUSED and Y.stride(0) % 8 == 0 and Y.data_ptr() % 16 == 0
     name = "dbf_forward_prefill_fused" if fused else "dbf_forward_prefill"
-    ws_bytes = (_lib.lib.dbf_prefill_fused_workspace_bytes if fused else _lib.lib.dbf_prefill_workspace_bytes)(layer.k, T)
+    if fused:
+        ws_bytes = _lib.lib.dbf_prefill_fused_workspace_bytes(layer.k, T)
+    else:  # room for the split-K partials of small token counts
+        ws_bytes = _lib.lib.dbf_prefill_workspace_bytes_nkm(layer.n, layer.k, layer.m_dim, T)
     ws = _workspace(ws_bytes, X.device)
     _lib.check(
         getattr(_lib.lib, name)(

@@ -39,6 +39,9 @@ def _host_layer(rng, n, k, m):
         (300, 200, 96, 130),      # ragged tokens / rows / K; m % 8 != 0 exercises the padded copy
         (257, 1000, 160, 1000),   # tails on every dimension
         (1024, 256, 2048, 256),   # long GEMM2 K
+        (64, 1024, 2048, 4096),   # small T: MMA N = 64, K split over ~148 CTAs (both GEMMs)
+        (100, 512, 1024, 3000),   # small ragged T, ragged split tail
+        (200, 2048, 512, 1000),   # GEMM1 split, GEMM2 (K = 512) too short to split
     ],
 )
 def test_prefill_matches_oracle(rng, T, n, k, m):
@@ -139,3 +142,26 @@ def test_fused_prefill_equals_two_launch_path(T, n, k, m):
             _lib.stream_ptr()), "fused")
         torch.cuda.synchronize()
         assert torch.equal(Y, ref)
+
+
+def test_small_batch_split_k_is_deterministic():
+    """T = 64 at the Llama-2-13B MLP shape (1.5 bpw): the split-K partials are summed in split
+    order, so two runs are bitwise identical; a workspace too small for the partials runs the
+    unsplit GEMMs, equal within the fp16 tolerance."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    n, k, m, T = 13824, 5600, 5120, 64
+    dl = P.random_device_layer(n, k, m, generator=g, keep_words=True)
+    X = torch.randn((T, m), generator=g, device="cuda").half()
+    Y1 = P.forward_prefill(X, dl)
+    Y2 = P.forward_prefill(X, dl)
+    assert torch.equal(Y1, Y2) and torch.isfinite(Y1).all()
+    ws = torch.empty(_lib.lib.dbf_prefill_workspace_bytes(k, T), dtype=torch.uint8, device="cuda")
+    Y0 = torch.empty_like(Y1)
+    A, B = dl.A.paired, dl.B.paired
+    _lib.check(_lib.lib.dbf_forward_prefill(
+        A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], dl.a.data_ptr(), dl.mid.data_ptr(), dl.b.data_ptr(),
+        n, k, m, X.data_ptr(), T, X.stride(0), Y0.data_ptr(), Y0.stride(0), ws.data_ptr(), ws.numel(),
+        _lib.stream_ptr()), "dbf_forward_prefill")
+    err = (Y0.float() - Y1.float()).abs().max().item() / Y0.float().abs().max().item()
+    assert err <= TOL

@@ -664,8 +664,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     WT(1);
     // the output scale is fetched now as RAW bits and converted only in the finalize: converting
     // here would stall the finalizing warps for a full L2 round trip before their first poll
-    const int fu = kWarps - 1 - warp;  // the unit this warp finalizes (warps 15, 14, ...: they own
-                                       // the fewest chunks when a run's chunks do not divide by 16)
+    // warp 15 - i finalizes item i = (unit fu, token pair fpair) (warps 15, 14, ...: they own the
+    // fewest chunks when a run's chunks do not divide by 16); 4 tokens = 2 pairs per unit, so the
+    // 16 warps cover 8 units in one pass
+    constexpr int kPairs = (NB + 1) / 2;
+    const int fu = (kWarps - 1 - warp) / kPairs, fpair = (kWarps - 1 - warp) % kPairs;
     uint32_t osc_bits = in.sdt == DBF_F16 ? 0x3C00u : 0x3F800000u;  // 1.0
     if (oscale && fu < nunits && lane < 16 && (rb + fu) * 16 + lane < rows) {
       const int r = (rb + fu) * 16 + lane;
@@ -682,44 +685,6 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     bool first = true;
     ChunkFetch nf;
     bool fetched = false;
-    // A run whose input chunks are all quantized already (reuse) deals the chunk residue classes
-    // rotated by `rot` per unit pair, so warps that own one chunk more than others (nch not a
-    // multiple of 16) alternate with those that own one less.  A warp's partial for a unit is still
-    // one residue class summed in chunk order, and the finalize sums residues 0..15 in order:
-    // bitwise the same result as the unrotated dealing.
-#ifdef DBF_ROT
-    const int rot = (reuse && (nch & (kWarps - 1))) ? kWarps / 2 : 0;
-#else
-    const int rot = 0;
-#endif
-    if (rot) {
-#pragma unroll
-      for (int p = 0; p < kMaxUnits / 2; ++p) {
-        const int u0 = 2 * p;
-        if (u0 >= nunits) break;
-        const bool has1 = u0 + 1 < nunits;
-        const int res = (warp + p * rot) & (kWarps - 1);
-        const uint8_t* oxs = sm.xs + res * xsb;
-        const int* oq = qft + res * xsc * NB * 2;
-        for (int c = res; c < nch; c += kWarps) {
-          const int qs = (c / kWarps) % xsc;
-          const uint8_t* xq = oxs + qs * kChunkQ;
-          const int2 ftt = *(const int2*)(oq + (qs * NB + (tig < NB ? tig : 0)) * 2);
-          uint2 b[8];
-#pragma unroll
-          for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * NB * 64 + xlane);
-          const float inv = __int_as_float((127 - ftt.x) << 23) * kQInv;
-          float v[2][2];
-          pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, ftt.y, inv, lane, v);
-          acc0[u0] += v[0][0];
-          acc1[u0] += v[0][1];
-          if (u0 + 1 < kMaxUnits && has1) {
-            acc0[u0 + 1] += v[1][0];
-            acc1[u0 + 1] += v[1][1];
-          }
-        }
-      }
-    } else
     for (int c = warp; c < nch; c += kWarps) {
       const int qs = (c / kWarps) % xsc;
       uint8_t* xq = xs + qs * kChunkQ;
@@ -813,16 +778,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
                                             : __uint_as_float(osc_raw);
     if (fu < nunits) {
       const int row = (rb + fu) * 16 + (lane & 15);
-#pragma unroll
-      for (int t0 = 0; t0 < NB; t0 += 2) {
-        const int t = t0 + (lane >> 4);
+      {
+        const int t = 2 * fpair + (lane >> 4);
         if (t < NB && t < batch && row < rows) {
           float v = 0.f;
 #pragma unroll
-          for (int r = 0; r < kWarps; ++r) {  // residue classes in order (warp = residue when rot == 0)
-            const int w2 = (r - (fu >> 1) * rot) & (kWarps - 1);
-            v += part[((w2 * kMaxUnits + fu) * NB + t) * 16 + (lane & 15)];
-          }
+          for (int w2 = 0; w2 < kWarps; ++w2) v += part[((w2 * kMaxUnits + fu) * NB + t) * 16 + (lane & 15)];
           v *= osc_row;
           const __half h = __float2half_rn(v);
           if (ll_out) st_ll16(ll_out + t * out_ll_stride + row, h, ep_out);

@@ -47,6 +47,14 @@ constexpr int kSlotBytes = 16384;             // one ring slot = 32 chunks of 51
 #define DBF_CHAINS 1  // accumulator chains per unit (1, 2, 4 measured within 1 %; 1 issues fewest)
 #endif
 constexpr int kMaxUnits = 8;                  // units per run (the host splits longer runs)
+// 4-token runs keep at most 4 units: their accumulators, token pairs and quantizer state would not
+// fit the 112 registers otherwise (spills on the run-start path), and the smaller partial buffer
+// leaves room for two quantized chunks per warp (inputs up to 32 chunks quantized once per CTA)
+#ifndef DBF_NB4_UNITS
+#define DBF_NB4_UNITS 4
+#endif
+template <int NB> constexpr int max_units() { return NB == 4 ? DBF_NB4_UNITS : kMaxUnits; }
+inline int max_units_of(int nb) { return nb == 4 ? DBF_NB4_UNITS : kMaxUnits; }
 #ifndef DBF_POLL_NS
 #define DBF_POLL_NS 32
 #endif
@@ -58,7 +66,7 @@ constexpr int kMaxSlots = 16;
 constexpr float kQScale = 4079.f / 4096.f;    // keeps 8 * |X| below the two-digit limit 32640
 constexpr float kQInv = 4096.f / 4079.f;
 constexpr int kChunkQBytes1 = 8 * 64;         // one quantized chunk: 8 k-blocks x (2 planes x 4 lanes x 8 B)
-constexpr int kPartFloats1 = kWarps * kMaxUnits * 16;  // one partial buffer
+inline int part_floats(int nb) { return kWarps * max_units_of(nb) * 16 * nb; }  // one partial buffer
 // chunks a warp keeps quantized for reuse by the next run on the same input (a stage split over
 // several runs of one CTA): inputs up to 16 * xs_chunks chunks
 #ifndef DBF_XS_CHUNKS1
@@ -71,7 +79,10 @@ constexpr int kPartFloats1 = kWarps * kMaxUnits * 16;  // one partial buffer
 // chunks, so a stage of any width up to 16 * DBF_XS_CHUNKS1_MAX chunks quantizes once per CTA);
 // the ring gets the rest of shared memory
 inline int xs_chunks_of(int nb, int max_cols = 0) {
-  if (nb != 1) return nb == 2 ? 2 : 1;
+  // 2 tokens: 64 chunks; 4 tokens: 32 chunks when the widest unit leaves a deep enough ring
+  // (<= 16384 columns: 7B, 13B), else 16 (the 70B's 57 KB units want the 10-slot ring)
+  if (nb == 2) return 4;
+  if (nb == 4) return chunks(max_cols) <= 64 ? 2 : 1;
   const int need = (int)((chunks(max_cols) + kWarps - 1) / kWarps);
   return need <= DBF_XS_CHUNKS1 ? DBF_XS_CHUNKS1 : DBF_XS_CHUNKS1_MAX;  // the two batch-1 instantiations
 }
@@ -161,7 +172,7 @@ struct Smem {
   uint8_t* ring;
   dbf_engine_run* hdr;  // [kMaxSlots] record of the run whose first piece is in that slot
   uint8_t* xs;          // [kWarps][kXsBytes]
-  float* part;          // [2][kWarps][kMaxUnits][16]
+  float* part;          // [2][kWarps][max_units][NB][16]
   uint64_t* full;
   uint64_t* empty;
 };
@@ -481,9 +492,12 @@ __device__ __forceinline__ void quantize_chunk_tokens(const InSpec& in, int c, u
 }
 
 // The MMAs of units u0 and u0 + 1 (has1) against chunk c of the run (signs resident in the ring),
-// as the two units' fp32 chunk sums v[unit][row g / g + 8] of this lane's token.
+// as the two units' exact chunk sums P = s/4 - T (as floats) v[unit][row g / g + 8] of this lane's
+// token; the caller accumulates acc = fma(P, 1 / (2^F kQScale), acc) with an explicit FMA (left
+// to the compiler, the multiply-add was contracted in some unrolled positions and not in others,
+// so a unit's sum depended on its place in a run, i.e. on the grid).
 __device__ __forceinline__ void pair_mma(const uint8_t* ring, int ring_slots, int slot0, int nch, int c, int u0,
-                                         bool has1, const uint2 (&b)[8], int Tt, float inv, int lane,
+                                         bool has1, const uint2 (&b)[8], int Tt, int lane,
                                          float (&v)[2][2]) {
         uint4 w[2];
 #pragma unroll
@@ -524,14 +538,15 @@ __device__ __forceinline__ void pair_mma(const uint8_t* ring, int ring_slots, in
           int s0 = ac[h][0][0], s1 = ac[h][0][1], s2 = ac[h][0][2], s3 = ac[h][0][3];
 #pragma unroll
           for (int q = 1; q < DBF_CHAINS; ++q) s0 += ac[h][q][0], s1 += ac[h][q][1], s2 += ac[h][q][2], s3 += ac[h][q][3];
-          v[h][0] = (float)(((s0 + 256 * s1) >> 2) - Tt) * inv;
-          v[h][1] = (float)(((s2 + 256 * s3) >> 2) - Tt) * inv;
+          v[h][0] = (float)(((s0 + 256 * s1) >> 2) - Tt);  // exact (|P| < 2^24)
+          v[h][1] = (float)(((s2 + 256 * s3) >> 2) - Tt);
         }
 }
 
 template <int NB, int XS>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program prog, int ring_slots) {
-  constexpr int kChunkQ = kChunkQBytes1 * NB, kPartFloats = kPartFloats1 * NB;
+  constexpr int kMaxUnits = max_units<NB>();
+  constexpr int kChunkQ = kChunkQBytes1 * NB, kPartFloats = kWarps * kMaxUnits * 16 * NB;
   // quantized chunks kept per warp (xs_chunks_of: sized by the program's widest input at batch 1)
   constexpr int xsc = XS;
   constexpr int xsb = xsc * kChunkQ;
@@ -739,12 +754,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         if (u0 >= nunits) break;
         const bool has1 = u0 + 1 < nunits;
         float v[2][2];
-        pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, Tt, inv, lane, v);
-        acc0[u0] += v[0][0];
-        acc1[u0] += v[0][1];
+        pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, Tt, lane, v);
+        acc0[u0] = __fmaf_rn(v[0][0], inv, acc0[u0]);
+        acc1[u0] = __fmaf_rn(v[0][1], inv, acc1[u0]);
         if (u0 + 1 < kMaxUnits && has1) {
-          acc0[u0 + 1] += v[1][0];
-          acc1[u0 + 1] += v[1][1];
+          acc0[u0 + 1] = __fmaf_rn(v[1][0], inv, acc0[u0 + 1]);
+          acc1[u0 + 1] = __fmaf_rn(v[1][1], inv, acc1[u0 + 1]);
         }
       }
       { const int jj = c / kWarps; if (jj < 3) WT(5 + jj); }
@@ -811,7 +826,7 @@ __global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; 
 // shared memory besides the per-slot parts (16 KB ring slot + 128 B record + 2 mbarriers)
 inline size_t fixed_smem(int nb, int xsc) {
   const int xs = xsc * kChunkQBytes1 * nb;
-  return (size_t)kWarps * xs + 2 * (size_t)kPartFloats1 * nb * 4 + (size_t)kWarps * xsc * nb * 2 * 4 + 48 +
+  return (size_t)kWarps * xs + 2 * (size_t)part_floats(nb) * 4 + (size_t)kWarps * xsc * nb * 2 * 4 + 48 +
          (size_t)kWarps * 8 + 128;
 }
 constexpr size_t kPerSlot = kSlotBytes + sizeof(dbf_engine_run) + 2 * 8;
@@ -854,7 +869,7 @@ extern "C" int dbf_engine_build_runs(const dbf_engine_segment* segments, int32_t
     const dbf_engine_segment& g = segments[seg];
     if ((int64_t)(rb + n) * kRowBlock > (int64_t)((g.rows + kRowBlock - 1) / kRowBlock) * kRowBlock)
       return DBF_ERR_SHAPE;
-    if (n > engine::kMaxUnits ||
+    if (n > engine::max_units_of(engine::nb_for(batch)) ||
         (int64_t)n * chunks(g.cols) * kChunkBytes >
             (int64_t)(engine::ring_slots(engine::nb_for(batch), max_cols) / 2) * engine::kSlotBytes)
       return DBF_ERR_SHAPE;  // split longer runs (dbf_engine_run_limits_cols)
@@ -902,7 +917,7 @@ extern "C" int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* by
 extern "C" int dbf_engine_run_limits_cols(int32_t max_cols, int32_t batch, int32_t* max_units,
                                           int64_t* max_run_bytes) {
   if (!max_units || !max_run_bytes || batch < 1 || batch > 4 || max_cols < 0) return DBF_ERR_INVALID_ARGUMENT;
-  *max_units = engine::kMaxUnits;
+  *max_units = engine::max_units_of(engine::nb_for(batch));
   // a run's signs stay resident until every compute warp is done with it; leave room to prefetch
   *max_run_bytes = (int64_t)(engine::ring_slots(engine::nb_for(batch), max_cols) / 2) * engine::kSlotBytes;
   return DBF_OK;
@@ -978,7 +993,9 @@ extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream
              ? engine_launch_nb<1, DBF_XS_CHUNKS1>(program, s)
              : engine_launch_nb<1, DBF_XS_CHUNKS1_MAX>(program, s);
   else
-    st = nb == 2 ? engine_launch_nb<2, 2>(program, s) : engine_launch_nb<4, 1>(program, s);
+    st = nb == 2 ? engine_launch_nb<2, 4>(program, s)
+                 : (engine::xs_chunks_of(4, program->max_cols) == 2 ? engine_launch_nb<4, 2>(program, s)
+                                                                     : engine_launch_nb<4, 1>(program, s));
   if (st != DBF_OK) return st;
   engine::advance_run_kernel<<<1, 1, 0, s>>>(program->run_counter);
   return check_launch();

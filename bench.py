@@ -508,14 +508,6 @@ def main():
            "d2h_bytes_per_step": host_y.numel() * host_y.element_size(),
            "ms_per_step": ms_e2e, "api": "paper_2505_11076_b200.plan.DecodePlan.run-equivalent (pinned H2D, graph replay, D2H)"}
 
-    # ---- k-sharded 70B layers: NCCL all-reduce vs the all-reduce fused into GEMV2 (all ranks) ---
-    shard = None
-    if not args.no_sharded:
-        try:
-            shard = sharded_bench(world, rank, max(args.steps // 2, 5), 3, barrier, dist)
-        except Exception as e:  # noqa: BLE001 - report, keep the headline line
-            shard = {"error": f"{type(e).__name__}: {e}"[:300]}
-
     # ---- cuBLAS fp16 GEMV over the same 224 shapes and dataflow -----------------------------
     cublas = None
     if not args.no_cublas:
@@ -556,6 +548,17 @@ def main():
         cpu = {"value": ref.bytes_per_block / t / 1e9, "unit": "GB/s", "cores": ref.procs, "kind": "port",
                "sample": cpu_desc(args.model, args.bpw, ref.procs) + f", median of {args.cpu_reps} blocks",
                "ms_per_layer": t * 1e3 / len(ref.order)}
+
+    # ---- k-sharded 70B layers: NCCL all-reduce vs the all-reduce fused into GEMV2 (all ranks) ---
+    # last, after every other number is in hand: a failure here (e.g. a peer-memory problem at
+    # N > 1) is reported in the line instead of losing it
+    shard = None
+    if not args.no_sharded:
+        barrier()
+        try:
+            shard = sharded_bench(world, rank, max(args.steps // 2, 5), 3, barrier, dist)
+        except Exception as e:  # noqa: BLE001 - report, keep the headline line
+            shard = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     if rank == 0:
         line = {

@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-layers", action="store_true")
     ap.add_argument("--no-sharded", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--layer-kernels", action="store_true", help="per-layer GEMV kernels instead of the engine")
@@ -264,6 +265,58 @@ def time_graph(g, steps, warmup, barrier=lambda: None):
     torch.cuda.synchronize()
     barrier()
     return e0.elapsed_time(e1) / steps  # ms per step
+
+
+def layer_bench(model: str, bpw: float, steps: int, warmup: int):
+    """The metric at layer level (SURVEY §8d timing method): per distinct Llama-2 linear shape at
+    `bpw`, batch 1 -- (1) throughput: N distinct layer instances (total > 2x L2) that all read the
+    same input, run as ONE engine program without dependencies between them, µs/layer = time / N;
+    (2) isolated latency: one layer alone as one engine launch (B stage -> LL handoff -> A stage);
+    (3) cuBLAS fp16 GEMV of the dense n x m layer, the same N distinct instances in a CUDA graph."""
+    import torch
+
+    import paper_2505_11076_b200 as P
+    from paper_2505_11076_b200.budget import middle_dim
+    from paper_2505_11076_b200.plan import DecodePlan, PlanOp, block_shapes
+
+    rows = []
+    seen = set()
+    for name, n, m in block_shapes(model):
+        if (n, m) in seen:
+            continue
+        seen.add((n, m))
+        k = middle_dim(n, m, bpw, 32)
+        g = torch.Generator(device="cuda")
+        g.manual_seed(7)
+        one = P.random_device_layer(n, k, m, generator=g)
+        lb = one.bytes_logical(batch=1, act_bytes=2)
+        inst = int(min(96, max(4, -(-260_000_000 // lb))))
+        layers = [one] + [P.random_device_layer(n, k, m, generator=g) for _ in range(inst - 1)]
+        x = torch.randn((1, m), generator=g, device="cuda").half()
+        bufs = [x] + [torch.zeros((1, n), dtype=torch.half, device="cuda") for _ in range(inst)]
+        ops = [PlanOp(i, 0, i + 1, name) for i in range(inst)]
+        tp = DecodePlan(layers, ops, bufs, input_buffer=0, output_buffer=inst).use_engine()
+        tp.capture()
+        ms_t = time_graph(tp._graph, steps, warmup)
+        iso = DecodePlan([one], [PlanOp(0, 0, 1, name)], [x, bufs[1]], input_buffer=0, output_buffer=1).use_engine()
+        iso.capture()
+        ms_i = time_graph(iso._graph, steps * 10, warmup)
+        ws = [torch.empty((n, m), dtype=torch.half, device="cuda").normal_(0, m ** -0.5, generator=g)
+              for _ in range(inst)]
+        ys = [torch.empty((1, n), dtype=torch.half, device="cuda") for _ in range(inst)]
+        gc = graph_of(lambda: [torch.matmul(x, w.t(), out=y) for w, y in zip(ws, ys)])
+        ms_c = time_graph(gc, steps, warmup)
+        dense = 2 * n * m + 2 * (n + m)
+        rows.append({"layer": name, "n": n, "k": k, "m": m, "bytes": lb, "instances": inst,
+                     "us_per_layer": ms_t * 1e3 / inst, "gbs": lb * inst / (ms_t * 1e-3) / 1e9,
+                     "us_isolated": ms_i * 1e3, "cublas_fp16_us_per_layer": ms_c * 1e3 / inst,
+                     "cublas_fp16_gbs": dense * inst / (ms_c * 1e-3) / 1e9,
+                     "speedup_vs_cublas": ms_c / ms_t})
+        del tp, iso, gc, ws, ys, layers
+        torch.cuda.empty_cache()
+    return {"model": model, "bpw": bpw, "batch": 1,
+            "note": "independent instances in one engine launch (throughput) / one layer per launch (isolated)",
+            "rows": rows}
 
 
 def prefill_bench(model: str, bpw: float, tokens: int, steps: int, warmup: int):
@@ -536,6 +589,10 @@ def main():
                                "unit": "TFLOP/s", "frac": prefill["tflops"] / bf16_peak,
                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense fp16 = bf16 rate)"}
 
+    layers = None
+    if rank == 0 and not args.no_layers:
+        layers = layer_bench(args.model, args.bpw, max(args.steps // 2, 5), 3)
+
     sweep = None
     if rank == 0 and not args.no_sweep:
         sweep = sweep_bench(max(args.steps // 4, 3))
@@ -592,6 +649,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "prefill": prefill,
+            "layers": layers,
             "sweep": sweep,
             "sharded": shard,
             "gpu_launches": launches * args.steps,

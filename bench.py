@@ -382,18 +382,21 @@ def sweep_bench(steps: int):
 
     rows = []
 
-    def one(model, bpw, batch, engine):
+    def one(model, bpw, batch, engine, prefill=False):
         g = torch.Generator(device="cuda")
         g.manual_seed(5)
-        plan = llama_decode_plan(model, bpw=bpw, batch=batch, generator=g)
+        plan = llama_decode_plan(model, bpw=bpw, batch=batch, generator=g, keep_words=prefill or None)
         plan.buffers[plan.input_buffer].normal_(generator=g)
-        plan.use_engine() if engine else plan.use_layer_kernels()
+        if prefill:
+            plan.use_prefill()
+        else:
+            plan.use_engine() if engine else plan.use_layer_kernels()
         plan.capture()
         ms = time_graph(plan._graph, steps, 3)
         b = plan.bytes_per_step()
         rows.append({"model": model, "bpw": bpw, "batch": batch,
                      "path": (("engine" if batch <= 4 else f"engine, {-(-batch // 4)} launches of <= 4 tokens")
-                              if engine else ("tcgen05 prefill chain" if batch >= 64 else
+                              if engine else ("tcgen05 prefill chain" if batch >= 64 or prefill else
                                               "int8 GEMV chain (pre-quantized batch)")),
                      "ms_per_step": ms, "gbs": b / (ms * 1e-3) / 1e9,
                      "tokens_per_s_linears_only": batch * 1e3 / ms, "layers": len(plan.ops)})
@@ -403,12 +406,14 @@ def sweep_bench(steps: int):
     one("llama2-70b", 2.0, 1, True)
     one("llama2-70b", 2.0, 4, True)
     one("llama2-70b", 2.0, 16, True)
+    one("llama2-70b", 2.0, 16, False, prefill=True)
     for bpw in (1.0, 1.5, 2.0, 2.3):
         one("llama2-13b", bpw, 1, True)
     one("llama2-7b", 2.0, 4, True)
     one("llama2-13b", 1.5, 4, True)
     one("llama2-13b", 1.5, 8, True)
     one("llama2-13b", 1.5, 8, False)
+    one("llama2-13b", 1.5, 8, False, prefill=True)
     one("llama2-13b", 1.5, 64, False)
     return rows
 

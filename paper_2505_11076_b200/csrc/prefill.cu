@@ -61,7 +61,8 @@ constexpr int kExpWarp0 = 4;
 constexpr int kNumProducers = 3;              // warps 0, 2, 3
 constexpr int kExpWarps = 8 * MH;
 constexpr int kThreads = (kExpWarp0 + kExpWarps) * 32;
-constexpr int kMaxKScale = 32768;             // K columns whose kscale fits the smem copy
+constexpr int kMaxKScale = 1 << 20;           // K columns a kscale may have (beyond the smem copy: global)
+constexpr int kMaxSmemOptin = 227 * 1024;
 
 struct Params {
   const uint32_t* words;   // rows x pitch PAIRED words
@@ -80,6 +81,7 @@ struct Params {
   int act_bytes;
   int kb_per_split;
   float* part;
+  int ks_global;           // kscale read from global memory (L1-cached) when the smem copy does not fit
 };
 
 struct __align__(8) Barriers {
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&act_map);
   }
   if (warp == 1) tmem_alloc<kTmemCols>(&bar.tmem_base);
-  if constexpr (KSCALE) {
+  if (KSCALE && !p.ks_global) {
     // kscale as fp16 pairs, zero beyond K (those columns meet TMA zero-fill anyway)
     const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
     for (int i = threadIdx.x; i < p.num_kb * (BK / 2); i += kThreads) {
@@ -232,11 +234,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t w = (j & 1) ? (half ? q[j >> 1].w : q[j >> 1].z) : (half ? q[j >> 1].y : q[j >> 1].x);
         uint32_t ks[16];
         if constexpr (KSCALE) {
-          const uint4* src = reinterpret_cast<const uint4*>(ks_smem + kb * (BK / 2) + half * 16);
+          const int c0 = kb * BK + half * 32;  // first of this word's 32 columns
+          if (!p.ks_global) {
+            const uint4* src = reinterpret_cast<const uint4*>(ks_smem + kb * (BK / 2) + half * 16);
   #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint4 u = src[i];
-            ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
+            for (int i = 0; i < 4; ++i) {
+              const uint4 u = src[i];
+              ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
+            }
+          } else if (c0 + 32 <= p.K) {  // wide K (e.g. 70B down, K = 28672): straight from L1/L2
+            const uint4* src = reinterpret_cast<const uint4*>(p.kscale + c0);
+  #pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint4 u = __ldg(src + i);
+              ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
+            }
+          } else {
+            const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
+  #pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int c = c0 + 2 * q;
+              ks[q] = (c < p.K ? (uint32_t)src[c] : 0u) | ((c + 1 < p.K ? (uint32_t)src[c + 1] : 0u) << 16);
+            }
           }
         } else {
   #pragma unroll
@@ -388,6 +407,8 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   p.act_bytes = n_mma * BK * 2;
   p.kb_per_split = p.num_kb;
   p.part = nullptr;
+  p.ks_global = kscale && smem_bytes(p.num_kb, true) > (size_t)kMaxSmemOptin ? 1 : 0;
+  if (p.ks_global && ((uintptr_t)kscale & 15) != 0) return DBF_ERR_UNSUPPORTED;
   int splits = 1;
   if (!mc && T <= BN) {
     int kps = 0;
@@ -405,7 +426,7 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   }
   const unsigned gx = (unsigned)ceil_div(rows, BM);
   dim3 grid(mc ? (gx + 1) / 2 * 2 : gx, (unsigned)ceil_div(T, BN), (unsigned)splits);
-  const size_t smem = smem_bytes(p.num_kb, kscale != nullptr);
+  const size_t smem = smem_bytes(p.num_kb, kscale != nullptr && !p.ks_global);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

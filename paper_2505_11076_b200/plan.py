@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 from . import _lib
 from .budget import middle_dim
 from .device import DeviceLayer
-from .kernel import forward_device, random_device_layer
+from .kernel import forward_device, forward_prefill, random_device_layer
 
 # Llama-2 linear shapes (n = out_features, m = in_features), SURVEY.md §8a
 LLAMA_SHAPES = {
@@ -89,6 +89,15 @@ class DecodePlan:
     def use_layer_kernels(self):
         """Run one dbf_forward (two GEMV launches) per layer instead of the engine."""
         self.engine = None
+        self._prefill = False
+        self._graph = None
+        return self
+
+    def use_prefill(self):
+        """Run every layer through the tcgen05 sign GEMMs (forward_prefill) whatever the batch:
+        one pass over the weights for all tokens (fp16 activations; layers built with keep_words)."""
+        self.engine = None
+        self._prefill = True
         self._graph = None
         return self
 
@@ -96,8 +105,9 @@ class DecodePlan:
         if self.engine is not None:
             self.engine.launch()
             return
+        run = forward_prefill if getattr(self, "_prefill", False) else forward_device
         for op in self.ops:
-            forward_device(self.buffers[op.src], self.layers[op.layer], out=self.buffers[op.dst])
+            run(self.buffers[op.src], self.layers[op.layer], out=self.buffers[op.dst])
 
     def capture(self):
         import torch

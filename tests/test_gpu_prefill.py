@@ -42,6 +42,8 @@ def _host_layer(rng, n, k, m):
         (64, 1024, 2048, 4096),   # small T: MMA N = 64, K split over ~148 CTAs (both GEMMs)
         (100, 512, 1024, 3000),   # small ragged T, ragged split tail
         (200, 2048, 512, 1000),   # GEMM1 split, GEMM2 (K = 512) too short to split
+        (64, 256, 128, 28672),    # GEMM1 K = 28672 (70B down): kscale read from global, split K
+        (260, 128, 64, 30000),    # wide K without split, ragged K tail through the global kscale
     ],
 )
 def test_prefill_matches_oracle(rng, T, n, k, m):

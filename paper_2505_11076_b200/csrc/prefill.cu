@@ -51,11 +51,9 @@ constexpr int UK = 16;           // K per tcgen05.mma (kind::f16)
 #define DBF_PREFILL_STAGES 6
 #endif
 constexpr int STAGES = DBF_PREFILL_STAGES;
-constexpr int kActStageBytes = BN * BK * 2;   // 32 KB
 constexpr int kAColsPerHalf = BK / 2;         // 32 TMEM columns (2 fp16 per 32-bit column)
 constexpr int kAColsPerStage = MH * kAColsPerHalf;
 constexpr int kAccCol = 0;                    // accumulator of M half h at column h * BN
-constexpr int kACol0 = MH * BN;               // A slots after the accumulators
 constexpr int kTmemCols = 512;
 constexpr int kExpWarp0 = 4;
 constexpr int kNumProducers = 3;              // warps 0, 2, 3
@@ -84,19 +82,29 @@ struct Params {
   int ks_global;           // kscale read from global memory (L1-cached) when the smem copy does not fit
 };
 
-struct __align__(8) Barriers {
-  uint64_t full_act[STAGES];
-  uint64_t full_a[STAGES];
-  uint64_t empty[STAGES];
+template <int NST>
+struct __align__(8) BarriersT {
+  uint64_t full_act[NST];
+  uint64_t full_a[NST];
+  uint64_t empty[NST];
   uint64_t acc_full;
   uint32_t tmem_base;
 };
 
-static_assert(kACol0 + STAGES * kAColsPerStage <= kTmemCols, "TMEM budget (A slots)");
-constexpr size_t kFixedSmem = 1024 /*align slack*/ + (size_t)STAGES * kActStageBytes + sizeof(Barriers) + 64;
-inline size_t smem_bytes(int num_kb, bool kscale) {
-  return kFixedSmem + (kscale ? (size_t)num_kb * BK * 2 : 0);
+// Small-token tiles (T <= kSmallBN): the accumulator needs only kSmallBN TMEM columns, so the ring
+// can be twice as deep with 8 KB activation boxes.  At N <= 64 a K block's MMAs take ~128 cycles
+// and the 6-stage ring left each K block bound by the activation TMA round trip (~3100 cycles
+// over 6 boxes in flight, tools/prefill_trace.py).
+constexpr int kSmallBN = 64, kSmallStages = 12;
+
+static_assert(MH * BN + STAGES * kAColsPerStage <= kTmemCols, "TMEM budget (A slots)");
+static_assert(MH * kSmallBN + kSmallStages * kAColsPerStage <= kTmemCols, "TMEM budget (small tiles)");
+template <int TBN, int NST>
+inline size_t smem_bytes_for(int num_kb, bool kscale) {
+  return 1024 /*align slack*/ + (size_t)NST * TBN * BK * 2 + sizeof(BarriersT<NST>) + 64 +
+         (kscale ? (size_t)num_kb * BK * 2 : 0);
 }
+inline size_t smem_bytes(int num_kb, bool kscale) { return smem_bytes_for<BN, STAGES>(num_kb, kscale); }
 
 // One paired word (bit q <-> column 2q, bit 16+q <-> column 2q+1 of a 32-column group) -> 16 words of
 // fp16 pairs +-ks.  (~w << (15-q)) moves the NEGATED signs of the pair to the fp16 sign positions
@@ -109,9 +117,14 @@ __device__ __forceinline__ void expand_word(uint32_t w, const uint32_t* ks, uint
 
 // MC: CTA pairs (cluster 2x1) that share a token tile; each loads half of the activation box and
 // multicasts it to both, so every SM pulls 16 KB instead of 32 KB per K block through TMA.
-template <bool KSCALE, bool MC>
+template <bool KSCALE, bool MC, int TBN = BN, int NST = STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     sign_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const Params p) {
+  // tile configuration: the namespace defaults, or the small-token tiles
+  constexpr int BN = TBN, STAGES = NST;
+  constexpr int kActStageBytes = BN * BK * 2;
+  constexpr int kACol0 = MH * BN;
+  using Barriers = BarriersT<STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* act = smem;
@@ -155,11 +168,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 || warp == 2 || warp == 3) {
     // ---------------- TMA producers ----------------
     // One thread's TMA loads complete one after another (~500 clk per box on B200, measured:
-    // tools/microbench/tma.cu); three issuing warps keep three boxes in flight.
-    if (lane == 0) {
-      const int prod = warp == 0 ? 0 : warp - 1;
+    // tools/microbench/tma.cu), so every ring stage gets its own issuing thread: lanes
+    // 0..kPerWarp-1 of the three producer warps (3 issuers for 6 stages left small-token tiles,
+    // whose MMAs are short, bound at ~600 cycles per K block).
+    constexpr int kPerWarp = (STAGES + kNumProducers - 1) / kNumProducers;
+    constexpr int kIssuers = kPerWarp * kNumProducers;
+    if (lane < kPerWarp) {
+      const int prod = (warp == 0 ? 0 : warp - 1) * kPerWarp + lane;
       const uint64_t pol = policy_evict_last();  // activations are re-read by every row tile
-      for (int kb = kb0 + prod; kb < kb1; kb += kNumProducers) {
+      for (int kb = kb0 + prod; kb < kb1; kb += kIssuers) {
         const int s = (kb - kb0) % STAGES;
         const uint32_t ph = ((kb - kb0) / STAGES) & 1;
         mbar_wait(&bar.empty[s], ph ^ 1);
@@ -388,6 +405,7 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   if (kscale && K > kMaxKScale) return DBF_ERR_UNSUPPORTED;
   static const bool mc = getenv("DBF_PREFILL_MULTICAST") != nullptr;  // measured slower
   // T <= BN: one token tile whose MMA N / activation box cover only the tokens present
+  const bool small = !mc && T <= kSmallBN;
   const int n_mma = T >= BN ? BN : (int)ceil_div(T, 16) * 16;
   CUtensorMap map;
   int st = make_act_map(&map, act, T, K, ld_act, mc ? BN / 2 : n_mma);
@@ -407,7 +425,8 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   p.act_bytes = n_mma * BK * 2;
   p.kb_per_split = p.num_kb;
   p.part = nullptr;
-  p.ks_global = kscale && smem_bytes(p.num_kb, true) > (size_t)kMaxSmemOptin ? 1 : 0;
+  const size_t ks_fit = small ? smem_bytes_for<kSmallBN, kSmallStages>(p.num_kb, true) : smem_bytes(p.num_kb, true);
+  p.ks_global = kscale && ks_fit > (size_t)kMaxSmemOptin ? 1 : 0;
   if (p.ks_global && ((uintptr_t)kscale & 15) != 0) return DBF_ERR_UNSUPPORTED;
   int splits = 1;
   if (!mc && T <= BN) {
@@ -425,8 +444,11 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
     p.trace = trace_buf;
   }
   const unsigned gx = (unsigned)ceil_div(rows, BM);
-  dim3 grid(mc ? (gx + 1) / 2 * 2 : gx, (unsigned)ceil_div(T, BN), (unsigned)splits);
-  const size_t smem = smem_bytes(p.num_kb, kscale != nullptr && !p.ks_global);
+  dim3 grid(mc ? (gx + 1) / 2 * 2 : gx, (unsigned)ceil_div(T, small ? kSmallBN : BN), (unsigned)splits);
+  const bool ks_smem = kscale != nullptr && !p.ks_global;
+  // the small configuration pads its shared memory so that one CTA per SM owns all of TMEM
+  const size_t smem = small ? std::max<size_t>(smem_bytes_for<kSmallBN, kSmallStages>(p.num_kb, ks_smem), 120 * 1024)
+                            : smem_bytes(p.num_kb, ks_smem);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -446,6 +468,9 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   };
   cudaError_t e;
   if (mc) e = kscale ? go(sign_gemm_kernel<true, true>) : go(sign_gemm_kernel<false, true>);
+  else if (small)
+    e = kscale ? go(sign_gemm_kernel<true, false, kSmallBN, kSmallStages>)
+               : go(sign_gemm_kernel<false, false, kSmallBN, kSmallStages>);
   else e = kscale ? go(sign_gemm_kernel<true, false>) : go(sign_gemm_kernel<false, false>);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   st = check_launch();

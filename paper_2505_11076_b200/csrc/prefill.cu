@@ -235,6 +235,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 4; ++i)
       q[i] = (live && (kb0 >> 1) + i < nquads) ? __ldg(wrow + (kb0 >> 1) + i) : make_uint4(0, 0, 0, 0);
     const bool tr = tracing && threadIdx.x == 32 * kExpWarp0;
+    // the 16 kscale pairs of this lane's word of K block kb (+1.0 pairs without a kscale)
+    auto load_ks = [&](int kb, uint32_t (&ks)[16]) {
+      if constexpr (KSCALE) {
+        const int c0 = kb * BK + half * 32;  // first of this word's 32 columns
+        if (!p.ks_global) {
+          const uint4* src = reinterpret_cast<const uint4*>(ks_smem + kb * (BK / 2) + half * 16);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint4 u = src[i];
+            ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
+          }
+        } else if (c0 + 32 <= p.K) {  // wide K (e.g. 70B down, K = 28672): straight from L1/L2
+          const uint4* src = reinterpret_cast<const uint4*>(p.kscale + c0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint4 u = __ldg(src + i);
+            ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
+          }
+        } else {
+          const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
+#pragma unroll
+          for (int qq = 0; qq < 16; ++qq) {
+            const int c = c0 + 2 * qq;
+            ks[qq] = (c < p.K ? (uint32_t)src[c] : 0u) | ((c + 1 < p.K ? (uint32_t)src[c + 1] : 0u) << 16);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ks[i] = 0x3C003C00u;
+      }
+    };
     for (int kg = kb0; kg < kb1; kg += 8) {  // kb0 is even (splits are whole quads)
       uint4 nq[4];
 #pragma unroll
@@ -243,54 +274,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         nq[i] = (live && qi < nquads && 2 * qi < kb1) ? __ldg(wrow + qi) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int kb = kg + j;
+      // two K blocks per iteration (one slot wait, one tcgen05 store wait and one arrive round per
+      // pair): at small token counts the per-K-block bookkeeping bounded the expanders
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        const int kb = kg + 2 * jp;
         if (kb >= kb1) break;
-        const int s = (kb - kb0) % STAGES;
+        const bool two = kb + 1 < kb1;
+        const int s = (kb - kb0) % STAGES;  // even (kb - kb0 and STAGES are even): s + 1 < STAGES
         const uint32_t ph = ((kb - kb0) / STAGES) & 1;
-        const uint32_t w = (j & 1) ? (half ? q[j >> 1].w : q[j >> 1].z) : (half ? q[j >> 1].y : q[j >> 1].x);
-        uint32_t ks[16];
-        if constexpr (KSCALE) {
-          const int c0 = kb * BK + half * 32;  // first of this word's 32 columns
-          if (!p.ks_global) {
-            const uint4* src = reinterpret_cast<const uint4*>(ks_smem + kb * (BK / 2) + half * 16);
-  #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint4 u = src[i];
-              ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
-            }
-          } else if (c0 + 32 <= p.K) {  // wide K (e.g. 70B down, K = 28672): straight from L1/L2
-            const uint4* src = reinterpret_cast<const uint4*>(p.kscale + c0);
-  #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint4 u = __ldg(src + i);
-              ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
-            }
-          } else {
-            const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
-  #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const int c = c0 + 2 * q;
-              ks[q] = (c < p.K ? (uint32_t)src[c] : 0u) | ((c + 1 < p.K ? (uint32_t)src[c + 1] : 0u) << 16);
-            }
-          }
-        } else {
-  #pragma unroll
-          for (int i = 0; i < 16; ++i) ks[i] = 0x3C003C00u;
+        uint32_t ks[16], v0[16], v1[16];
+        load_ks(kb, ks);
+        expand_word(half ? q[jp].y : q[jp].x, ks, v0);
+        if (two) {
+          load_ks(kb + 1, ks);
+          expand_word(half ? q[jp].w : q[jp].z, ks, v1);
         }
-        uint32_t v[16];
-        expand_word(w, ks, v);
         if (tr) p.trace[4 * kb] = clock64();
-        if (lane == 0) mbar_wait(&bar.empty[s], ph ^ 1);  // one poller per warp
+        if (lane == 0) {  // one poller per warp
+          mbar_wait(&bar.empty[s], ph ^ 1);
+          if (two) mbar_wait(&bar.empty[s + 1], ph ^ 1);
+        }
         __syncwarp();
         if (tr) p.trace[4 * kb + 1] = clock64();
         tc_fence_after();
-        tmem_st16(tmem + lane_addr + kACol0 + s * kAColsPerStage + mh * kAColsPerHalf + half * 16, v);
+        const uint32_t col = tmem + lane_addr + kACol0 + mh * kAColsPerHalf + half * 16;
+        tmem_st16(col + s * kAColsPerStage, v0);
+        if (two) tmem_st16(col + (s + 1) * kAColsPerStage, v1);
         tmem_wait_st();
         tc_fence_before();
         if (tr) p.trace[4 * kb + 2] = clock64();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar.full_a[s]);
+        if (lane == 0) {
+          mbar_arrive(&bar.full_a[s]);
+          if (two) mbar_arrive(&bar.full_a[s + 1]);
+        }
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) q[i] = nq[i];

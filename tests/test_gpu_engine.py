@@ -127,3 +127,32 @@ def test_engine_batch_8_runs_in_groups_of_4():
     g4.manual_seed(77)
     plan4 = llama_decode_plan("llama2-7b", bpw=2.0, batch=4, blocks=1, generator=g4).use_engine()
     assert torch.equal(_run(plan4, x[4:]), out[4:])
+
+
+@pytest.mark.parametrize("batch,n,k,m,act", [(3, 1000, 300, 777, "f32"), (4, 200, 64, 4100, "f16"),
+                                              (1, 17, 32, 29000, "f32"), (2, 5000, 2000, 300, "f16")])
+def test_engine_ragged_layers_vs_oracle(batch, n, k, m, act):
+    """Ragged shapes (rows not a multiple of 16, columns not of 256, inputs wider than 64 chunks),
+    fp32 or fp16 activations, 1-4 tokens; fp32 plain output is the unrounded sum.  Against the
+    float64 oracle on the same bytes, and launched again through the per-launch I/O overrides on
+    other buffers: bitwise the same."""
+    import torch
+    from paper_2505_11076_b200.plan import DecodePlan, PlanOp
+
+    dt = torch.float32 if act == "f32" else torch.float16
+    g = torch.Generator(device="cuda")
+    g.manual_seed(batch * 7 + n)
+    layer = P.random_device_layer(n, k, m, generator=g, keep_words=True)
+    x = torch.randn((batch, m), generator=g, device="cuda").to(dt)
+    bufs = [x.clone(), torch.zeros((batch, n), dtype=dt, device="cuda")]
+    plan = DecodePlan([layer], [PlanOp(0, 0, 1, "l")], bufs, input_buffer=0, output_buffer=1).use_engine()
+    plan._eager()
+    torch.cuda.synchronize()
+    y = bufs[1].double().cpu().numpy()
+    ref = oracle.c_forward(x.double().cpu().numpy(), layer.a.double().cpu().numpy(), layer.A.to_host().bits,
+                           layer.mid.double().cpu().numpy(), layer.B.to_host().bits, layer.b.double().cpu().numpy())
+    assert rel_max(y, ref) <= TOL and rel_norm(y, ref) <= TOL, (rel_max(y, ref), rel_norm(y, ref))
+    y2 = torch.empty_like(bufs[1])
+    plan.engine.launch_io(x.clone(), y2)
+    torch.cuda.synchronize()
+    assert torch.equal(y2, bufs[1])

@@ -278,7 +278,8 @@ typedef struct {
 typedef struct {
   const dbf_engine_run* runs;         /* device array of run records, per CTA in order         */
   const int32_t* cta_offsets;         /* device array, grid + 1 entries (indices into runs)     */
-  uint32_t* run_counter;              /* device uint32, advanced after every launch             */
+  uint32_t* run_counter;              /* device uint32[2], zeroed once: [0] launches so far (the
+                                         last CTA of a launch advances it), [1] CTAs done      */
   int64_t* trace;                     /* optional: 4 x int64 %globaltimer stamps per run / NULL */
   int32_t nvectors;
   int32_t grid;                       /* CTAs (<= number of SMs; one per SM)                    */
@@ -310,7 +311,7 @@ int dbf_engine_run_limits_cols(int32_t max_cols, int32_t batch, int32_t* max_uni
 int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* bytes);
 /* Resident engine CTAs per SM and registers per thread for max_cols (diagnostics). */
 int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, int32_t* regs_per_thread);
-/* Launch one run of the program (cooperative: all CTAs co-resident) + the epoch advance. */
+/* Launch one run of the program (cooperative: all CTAs co-resident; one kernel). */
 int dbf_engine_launch(const dbf_engine_program* program, void* stream);
 
 /* ---- prefill / batched path: tcgen05 + TMEM sign GEMMs (>= 64 tokens) ------------------ */

@@ -23,7 +23,7 @@
 // Inter-CTA dependencies use an LL ("low latency", as in NCCL's LL protocol) handoff: each value
 // is one 32-bit word {fp16 value, 16-bit epoch}; consumers poll the words themselves, so there is
 // no separate flag, fence or counter round trip.  Epochs are (launch * nvectors + vector) mod
-// 65535 + 1, advanced by a one-thread kernel after every launch, so LL buffers never need
+// 65535 + 1; the last CTA of a launch advances the launch counter, so LL buffers never need
 // clearing (a stale word always carries the previous launch's epoch).
 #include <algorithm>
 #include <cstring>
@@ -819,9 +819,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     }
     __syncwarp();
   }
+  // the last CTA to finish advances the launch counter (every CTA read it at its start, and the
+  // next launch is stream-ordered after this one): no separate advance kernel per step
+  if (warp == 0 && lane == 0 && atomicAdd(prog.run_counter + 1, 1u) == gridDim.x - 1) {
+    prog.run_counter[1] = 0u;
+    prog.run_counter[0] += 1u;
+  }
 }
-
-__global__ void advance_run_kernel(uint32_t* run_counter) { *run_counter += 1u; }
 
 // shared memory besides the per-slot parts (16 KB ring slot + 128 B record + 2 mbarriers)
 inline size_t fixed_smem(int nb, int xsc) {
@@ -997,6 +1001,5 @@ extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream
                  : (engine::xs_chunks_of(4, program->max_cols) == 2 ? engine_launch_nb<4, 2>(program, s)
                                                                      : engine_launch_nb<4, 1>(program, s));
   if (st != DBF_OK) return st;
-  engine::advance_run_kernel<<<1, 1, 0, s>>>(program->run_counter);
   return check_launch();
 }

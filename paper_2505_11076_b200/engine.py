@@ -247,7 +247,7 @@ class EngineProgram:
             vec_arr[j] = (ptr, ln, kind, dt, 0)
 
         self.max_cols = max(sg[2] for sg in segs)
-        self.run_counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.run_counter = torch.zeros(2, dtype=torch.int32, device=dev)  # [launches, CTAs done]
         self.ready = torch.zeros(len(vecs), dtype=torch.int32, device=dev)
         records = np.zeros(len(flat) * 128, dtype=np.uint8)
         _lib.check(
@@ -302,7 +302,7 @@ class EngineProgram:
         _lib.check(_lib.lib.dbf_engine_launch(ctypes.byref(prog), _lib.stream_ptr(stream)), "dbf_engine_launch")
 
     def kernel_launches_per_step(self) -> int:
-        return 2  # the engine kernel + the one-thread epoch advance
+        return 1  # the engine kernel (its last CTA advances the launch counter)
 
 
 class EngineGroups:

@@ -290,6 +290,11 @@ typedef struct {
    * so one program serves calls on different input / output buffers without rebuilding runs */
   const void* x_override;
   void* y_override;
+  /* batches of 2-4 tokens on inputs wider than the shared-memory store: a device buffer of
+   * grid x qscratch_cta_bytes (dbf_engine_qscratch_bytes) where each CTA keeps its quantized
+   * input chunks for the stage's later runs; NULL = re-quantize per run */
+  void* qscratch;
+  int64_t qscratch_cta_bytes;
 } dbf_engine_program;
 
 /*
@@ -306,6 +311,8 @@ int dbf_engine_run_limits(int32_t batch, int32_t* max_units, int64_t* max_run_by
 /* The same for a program whose widest segment has max_cols columns (at batch 1 the quantized-input
  * store grows with max_cols and the sign ring shrinks accordingly). */
 int dbf_engine_run_limits_cols(int32_t max_cols, int32_t batch, int32_t* max_units, int64_t* max_run_bytes);
+/* Per-CTA quantized-input scratch a program needs at this batch (0: none). */
+size_t dbf_engine_qscratch_bytes(int32_t max_cols, int32_t batch);
 /* Dynamic shared memory the engine needs for max_cols at this batch (1..4); DBF_ERR_UNSUPPORTED if
  * it cannot fit. */
 int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* bytes);

@@ -70,6 +70,7 @@ SIGNATURES: dict[str, tuple] = {
     "dbf_engine_launch": (_int, [_vp, _vp]),
     "dbf_engine_run_limits": (_int, [_c.c_int32, _c.POINTER(_c.c_int32), _c.POINTER(_c.c_int64)]),
     "dbf_engine_run_limits_cols": (_int, [_c.c_int32, _c.c_int32, _c.POINTER(_c.c_int32), _c.POINTER(_c.c_int64)]),
+    "dbf_engine_qscratch_bytes": (_sz, [_c.c_int32, _c.c_int32]),
     "dbf_pair_signs": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "dbf_prefill_debug_trace": (_int, [_vp, _int]),
     "dbf_prefill_ld": (_i64, [_i64]),

@@ -66,6 +66,7 @@ constexpr int kMaxSlots = 16;
 constexpr float kQScale = 4079.f / 4096.f;    // keeps 8 * |X| below the two-digit limit 32640
 constexpr float kQInv = 4096.f / 4079.f;
 constexpr int kChunkQBytes1 = 8 * 64;         // one quantized chunk: 8 k-blocks x (2 planes x 4 lanes x 8 B)
+constexpr int kQScrFT = 32;                   // scratch bytes per chunk for F, T of up to 4 tokens
 inline int part_floats(int nb) { return kWarps * max_units_of(nb) * 16 * nb; }  // one partial buffer
 // chunks a warp keeps quantized for reuse by the next run on the same input (a stage split over
 // several runs of one CTA): inputs up to 16 * xs_chunks chunks
@@ -692,9 +693,17 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     }
     constexpr int kReuseChunks = xsc * kWarps;
     const InKey prev = inkey[buf ^ 1];
-    const bool reuse = H.in_vec == prev.vec && in.iscale == prev.iscale && nch <= kReuseChunks;
+    // inputs wider than the shared-memory store (batches of 2-4 tokens on wide layers) keep their
+    // quantized chunks in the CTA's L2-resident scratch instead: a later run on the same input
+    // copies them back rather than polling and quantizing again
+    uint8_t* qscr = (NB > 1 && prog.qscratch && nch > kReuseChunks)
+                        ? (uint8_t*)prog.qscratch + (size_t)blockIdx.x * prog.qscratch_cta_bytes
+                        : nullptr;
+    const bool same_in = H.in_vec == prev.vec && in.iscale == prev.iscale;
+    const bool reuse = same_in && nch <= kReuseChunks;
+    const bool greuse = same_in && qscr != nullptr;
     if (warp == 0 && lane == 0) {
-      inkey[buf].vec = nch <= kReuseChunks ? H.in_vec : -1;
+      inkey[buf].vec = (nch <= kReuseChunks || qscr) ? H.in_vec : -1;
       inkey[buf].iscale = in.iscale;
     }
     bool first = true;
@@ -725,7 +734,19 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           if (fetched) fetch_issue(in, c + kWarps, lane, nf);
         }
       } else {
-        if (!reuse) {
+        // scratch slot of chunk c: the digits (kChunkQ bytes) then F, T per token (NB * 8 bytes)
+        uint8_t* qsc = qscr ? qscr + (size_t)c * (kChunkQ + kQScrFT) : nullptr;
+        if (greuse) {  // copy the chunk back from L2 (each lane its own digit bytes; lanes < 2 NB the F, T)
+          const uint4* src = (const uint4*)qsc + lane * (kChunkQ / 512);
+          uint4 d[kChunkQ / 512];
+#pragma unroll
+          for (int i = 0; i < kChunkQ / 512; ++i) d[i] = __ldcg(src + i);
+          const int ft = lane < 2 * NB ? __ldcg((const int*)(qsc + kChunkQ) + lane) : 0;
+#pragma unroll
+          for (int i = 0; i < kChunkQ / 512; ++i) ((uint4*)xq)[lane * (kChunkQ / 512) + i] = d[i];
+          if (lane < 2 * NB) wq[qs * NB * 2 + lane] = ft;
+          __syncwarp();
+        } else if (!reuse) {
           int F[NB], T[NB];
 #ifdef DBF_ENGINE_WARP_TRACE
           quantize_chunk_tokens<NB>(in, c, ep_in, xq, batch, F, T, (wt && c == warp) ? wt + 10 : nullptr);
@@ -736,6 +757,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           for (int t = 0; t < NB; ++t)
             if (lane == 0) wq[(qs * NB + t) * 2] = F[t], wq[(qs * NB + t) * 2 + 1] = T[t];
           __syncwarp();
+          if (qsc) {  // keep it for the stage's later runs
+            uint4* dst = (uint4*)qsc + lane * (kChunkQ / 512);
+#pragma unroll
+            for (int i = 0; i < kChunkQ / 512; ++i) __stcg(dst + i, ((const uint4*)xq)[lane * (kChunkQ / 512) + i]);
+            if (lane < 2 * NB) __stcg((int*)(qsc + kChunkQ) + lane, wq[qs * NB * 2 + lane]);
+          }
         }
         const int2 ftt = *(const int2*)(wq + (qs * NB + (tig < NB ? tig : 0)) * 2);
         Ft = ftt.x, Tt = ftt.y;
@@ -916,6 +943,14 @@ extern "C" int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* by
     return DBF_ERR_UNSUPPORTED;
   *bytes = engine::smem_bytes(slots, nb, max_cols);
   return DBF_OK;
+}
+
+extern "C" size_t dbf_engine_qscratch_bytes(int32_t max_cols, int32_t batch) {
+  if (max_cols < 1 || batch < 2 || batch > 4) return 0;
+  const int nb = engine::nb_for(batch);
+  const int64_t nch = chunks(max_cols);
+  if (nch <= (int64_t)engine::xs_chunks_of(nb, max_cols) * engine::kWarps) return 0;
+  return (size_t)nch * (engine::kChunkQBytes1 * nb + engine::kQScrFT);  // per CTA
 }
 
 extern "C" int dbf_engine_run_limits_cols(int32_t max_cols, int32_t batch, int32_t* max_units,

@@ -54,6 +54,8 @@ class _Program(ctypes.Structure):
         ("batch", ctypes.c_int32),
         ("x_override", ctypes.c_void_p),
         ("y_override", ctypes.c_void_p),
+        ("qscratch", ctypes.c_void_p),
+        ("qscratch_cta_bytes", ctypes.c_int64),
     ]
 
 
@@ -273,6 +275,11 @@ class EngineProgram:
         )
         self._offsets = offsets
         self._flat = flat
+        qb = _lib.lib.dbf_engine_qscratch_bytes(self.max_cols, self.batch)
+        if qb:  # quantized-input scratch for wide inputs at 2-4 tokens (L2-resident, per CTA)
+            qb = (qb + 255) // 256 * 256
+            self.qscratch = torch.empty(self.grid * qb, dtype=torch.uint8, device=dev)
+            self._prog.qscratch, self._prog.qscratch_cta_bytes = self.qscratch.data_ptr(), qb
         size = ctypes.c_size_t(0)
         _lib.check(_lib.lib.dbf_engine_smem_bytes(self.max_cols, self.batch, ctypes.byref(size)), "dbf_engine_smem_bytes")
         self.smem_bytes = size.value

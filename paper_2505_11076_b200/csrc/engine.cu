@@ -569,9 +569,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   struct InKey { const void* iscale; int vec; int pad; };
   InKey* inkey = (InKey*)(ep_base_s + 4);
   int2* cursor = (int2*)(inkey + 2);  // [kWarps]
-  // 4-token runs: the run's output fields live in shared memory (double-buffered by run parity,
-  // written by warp 0 at run start) instead of registers held across the MMA loop (48 -> 8 bytes
-  // of spills; 7B at 4 tokens 2531 -> 2292 us)
+  // the run's output fields live in shared memory (double-buffered by run parity, written by warp
+  // 0 at run start) instead of registers held across the MMA loop: 4 tokens 48 -> 8 bytes of
+  // spills (7B 2531 -> 2292 us), 1 token 1042 -> 1027 us; 2 tokens measured 1.6 % slower, kept off
+  constexpr bool kRunOutSmem = NB != 2;
   struct RunOut { void* out_plain; uint32_t* ll_out; int rows, rb, odt; uint32_t ep_out; };
   RunOut* runout = (RunOut*)(cursor + kWarps);  // [2]
 
@@ -676,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     const int nch = (cols + kChunkCols - 1) / kChunkCols;
     const int npieces = (nunits * nch * kChunkBytes + kSlotBytes - 1) / kSlotBytes;
     const uint32_t ep_in = H.in_kind == 1 ? epoch16(*ep_base_s, H.in_vec) : 0u;
-    if constexpr (NB > 2) {
+    if constexpr (kRunOutSmem) {
       if (warp == 0 && lane == 0) runout[buf] = RunOut{out_plain, ll_out, rows, rb, odt, ep_out};
     }
     float acc0[kMaxUnits], acc1[kMaxUnits];  // rows g, g+8 of each unit for token tig (tig < NB)
@@ -835,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
                                             : __uint_as_float(osc_raw);
     if (fu < nunits) {
       RunOut ro;
-      if constexpr (NB > 2) ro = runout[buf];
+      if constexpr (kRunOutSmem) ro = runout[buf];
       else ro = RunOut{out_plain, ll_out, rows, rb, odt, ep_out};
       const int row = (ro.rb + fu) * 16 + (lane & 15);
       {

@@ -680,6 +680,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     if constexpr (kRunOutSmem) {
       if (warp == 0 && lane == 0) runout[buf] = RunOut{out_plain, ll_out, rows, rb, odt, ep_out};
     }
+    // batch 1: the next run's ring cursor is stored now, so nothing of it stays live across the
+    // MMA loop (7B step 1024 -> 1017 us, 70B -3 %); 4 tokens measured 1 % slower, they store it at
+    // the end of the run
+    if (NB == 1 && lane == 0) {
+      int nx = slot0 + npieces;
+      if (nx >= ring_slots) nx -= ring_slots;
+      cursor[warp] = make_int2(nx, cur.y ^ (1 << slot0));
+    }
     float acc0[kMaxUnits], acc1[kMaxUnits];  // rows g, g+8 of each unit for token tig (tig < NB)
 #pragma unroll
     for (int u = 0; u < kMaxUnits; ++u) acc0[u] = acc1[u] = 0.f;
@@ -859,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     if (tr && threadIdx.x == 0) tr[3] = gtimer();
     WT(9);
 #undef WT
-    if (lane == 0) {
+    if (NB != 1 && lane == 0) {
       int nx = slot0 + npieces;
       if (nx >= ring_slots) nx -= ring_slots;
       cursor[warp] = make_int2(nx, cur.y ^ (1 << slot0));

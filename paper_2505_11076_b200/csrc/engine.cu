@@ -733,99 +733,154 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
         fetched = true;
       }
     }
-    for (int c = warp; c < nch; c += kWarps) {
-      const int qs = (c / kWarps) % xsc;
-      uint8_t* xq = xs + qs * kChunkQ;
-      // the chunk exponent F and quantized sum T of this lane's token tig (lanes tig >= NB hold
-      // mirrored columns that are discarded); every token's pair is kept in shared memory (wq)
-      // for reuse by the next run, and for NB > 1 the lanes pick theirs up from there
-      int Ft, Tt;
-      if constexpr (NB == 1) {
-        if (reuse) {
-          Ft = wq[2 * qs], Tt = wq[2 * qs + 1];
-        } else {
-          if (fetched) {
-            quantize_fetched(in, c, ep_in, xq, Ft, Tt, nf);
-          } else {
-#ifdef DBF_ENGINE_WARP_TRACE
-            quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt, (wt && c == warp) ? wt + 10 : nullptr);
-#else
-            quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt);
-#endif
-          }
-          if (lane == 0) wq[2 * qs] = Ft, wq[2 * qs + 1] = Tt;
-          fetched = in.kind == 1 && c + kWarps < nch;
-          if (fetched) fetch_issue(in, c + kWarps, lane, nf);
-        }
-      } else {
-        // scratch slot of chunk c: the digits (kChunkQ bytes) then F, T per token (NB * 8 bytes)
-        uint8_t* qsc = qscr ? qscr + (size_t)c * (kChunkQ + kQScrFT) : nullptr;
-        if (greuse) {  // copy the chunk back from L2 (each lane its own digit bytes; lanes < 2 NB the F, T)
-          const uint4* src = (const uint4*)qsc + lane * (kChunkQ / 512);
-          uint4 d[kChunkQ / 512];
-#pragma unroll
-          for (int i = 0; i < kChunkQ / 512; ++i) d[i] = __ldcg(src + i);
-          const int ft = lane < 2 * NB ? __ldcg((const int*)(qsc + kChunkQ) + lane) : 0;
-#pragma unroll
-          for (int i = 0; i < kChunkQ / 512; ++i) ((uint4*)xq)[lane * (kChunkQ / 512) + i] = d[i];
-          if (lane < 2 * NB) wq[qs * NB * 2 + lane] = ft;
-          __syncwarp();
-        } else if (!reuse) {
-          int F[NB], T[NB];
-#ifdef DBF_ENGINE_WARP_TRACE
-          quantize_chunk_tokens<NB>(in, c, ep_in, xq, batch, F, T, (wt && c == warp) ? wt + 10 : nullptr);
-#else
-          quantize_chunk_tokens<NB>(in, c, ep_in, xq, batch, F, T);
-#endif
-#pragma unroll
-          for (int t = 0; t < NB; ++t)
-            if (lane == 0) wq[(qs * NB + t) * 2] = F[t], wq[(qs * NB + t) * 2 + 1] = T[t];
-          __syncwarp();
-          if (qsc) {  // keep it for the stage's later runs
-            uint4* dst = (uint4*)qsc + lane * (kChunkQ / 512);
-#pragma unroll
-            for (int i = 0; i < kChunkQ / 512; ++i) __stcg(dst + i, ((const uint4*)xq)[lane * (kChunkQ / 512) + i]);
-            if (lane < 2 * NB) __stcg((int*)(qsc + kChunkQ) + lane, wq[qs * NB * 2 + lane]);
-          }
-        }
-        const int2 ftt = *(const int2*)(wq + (qs * NB + (tig < NB ? tig : 0)) * 2);
-        Ft = ftt.x, Tt = ftt.y;
-      }
-      if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
-      { const int jj = c / kWarps; if (jj < 3) WT(2 + jj); }
-      uint2 b[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * NB * 64 + xlane);
-      const float inv = __int_as_float((127 - Ft) << 23) * kQInv;  // 1 / (2^F * kQScale)
-      // units in pairs: two independent MMA streams per warp (the second repeats the last unit
-      // when nunits is odd and is then discarded)
+    float* part = sm.part + buf * kPartFloats;
+    if constexpr (NB == 1 && XS > DBF_XS_CHUNKS1) {
+      // batch 1 on wide programs (the 7-chunk store, e.g. 70B): unit pairs outer, the warp's chunks
+      // inner -- the first pass quantizes every owned chunk (kept in shared memory: the store
+      // covers the widest input), later passes reuse them, and each pair's sums go to shared
+      // memory as soon as its pass ends, so only one pair's accumulators are live at a time.
+      // Per-unit chunk order is unchanged (bitwise).  70B 16 blocks 1743 -> 1579 us; on 7B
+      // (4-chunk store, mostly one chunk per warp) chunk-outer stays 0.6 % faster.
 #pragma unroll
       for (int p = 0; p < kMaxUnits / 2; ++p) {
         const int u0 = 2 * p;
         if (u0 >= nunits) break;
         const bool has1 = u0 + 1 < nunits;
-        float v[2][2];
-        pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, Tt, lane, v);
-        acc0[u0] = __fmaf_rn(v[0][0], inv, acc0[u0]);
-        acc1[u0] = __fmaf_rn(v[0][1], inv, acc1[u0]);
-        if (u0 + 1 < kMaxUnits && has1) {
-          acc0[u0 + 1] = __fmaf_rn(v[1][0], inv, acc0[u0 + 1]);
-          acc1[u0 + 1] = __fmaf_rn(v[1][1], inv, acc1[u0 + 1]);
+        float a0[2] = {0.f, 0.f}, a1[2] = {0.f, 0.f};  // units u0, u0 + 1: rows g, g + 8
+        for (int c = warp; c < nch; c += kWarps) {
+          const int qs = (c / kWarps) % xsc;
+          uint8_t* xq = xs + qs * kChunkQ;
+          int Ft, Tt;
+          if (p > 0 || reuse) {
+            Ft = wq[2 * qs], Tt = wq[2 * qs + 1];
+          } else {
+            if (fetched) {
+              quantize_fetched(in, c, ep_in, xq, Ft, Tt, nf);
+            } else {
+              quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt);
+            }
+            if (lane == 0) wq[2 * qs] = Ft, wq[2 * qs + 1] = Tt;
+            fetched = in.kind == 1 && c + kWarps < nch;
+            if (fetched) fetch_issue(in, c + kWarps, lane, nf);
+            if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
+            first = false;
+          }
+          uint2 b[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * 64 + xlane);
+          const float inv = __int_as_float((127 - Ft) << 23) * kQInv;
+          float v[2][2];
+          pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, Tt, lane, v);
+          a0[0] = __fmaf_rn(v[0][0], inv, a0[0]);
+          a1[0] = __fmaf_rn(v[0][1], inv, a1[0]);
+          a0[1] = __fmaf_rn(v[1][0], inv, a0[1]);
+          a1[1] = __fmaf_rn(v[1][1], inv, a1[1]);
+        }
+        if (tig == 0) {
+          float* pu = part + (warp * kMaxUnits + u0) * 16;
+          pu[g] = a0[0];
+          pu[g + 8] = a1[0];
+          if (has1) {
+            pu[16 + g] = a0[1];
+            pu[16 + g + 8] = a1[1];
+          }
         }
       }
-      { const int jj = c / kWarps; if (jj < 3) WT(5 + jj); }
-      first = false;
-    }
-    if (tr && warp == 0 && lane == 0) tr[2] = gtimer();
-    // partials -> shared memory (double-buffered by run parity), then the compute warps meet once
-    float* part = sm.part + buf * kPartFloats;
-    if (tig < NB) {
-#pragma unroll
-      for (int u = 0; u < kMaxUnits; ++u) {
-        if (u < nunits) {
-          float* pu = part + ((warp * kMaxUnits + u) * NB + tig) * 16;
-          pu[g] = acc0[u];
-          pu[g + 8] = acc1[u];
+      if (tr && warp == 0 && lane == 0) tr[2] = gtimer();
+    } else {
+    for (int c = warp; c < nch; c += kWarps) {
+        const int qs = (c / kWarps) % xsc;
+        uint8_t* xq = xs + qs * kChunkQ;
+        // the chunk exponent F and quantized sum T of this lane's token tig (lanes tig >= NB hold
+        // mirrored columns that are discarded); every token's pair is kept in shared memory (wq)
+        // for reuse by the next run, and for NB > 1 the lanes pick theirs up from there
+        int Ft, Tt;
+        if constexpr (NB == 1) {
+          if (reuse) {
+            Ft = wq[2 * qs], Tt = wq[2 * qs + 1];
+          } else {
+            if (fetched) {
+              quantize_fetched(in, c, ep_in, xq, Ft, Tt, nf);
+            } else {
+  #ifdef DBF_ENGINE_WARP_TRACE
+              quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt, (wt && c == warp) ? wt + 10 : nullptr);
+  #else
+              quantize_chunk(in, c, ep_in, xq, 64, Ft, Tt);
+  #endif
+            }
+            if (lane == 0) wq[2 * qs] = Ft, wq[2 * qs + 1] = Tt;
+            fetched = in.kind == 1 && c + kWarps < nch;
+            if (fetched) fetch_issue(in, c + kWarps, lane, nf);
+          }
+        } else {
+          // scratch slot of chunk c: the digits (kChunkQ bytes) then F, T per token (NB * 8 bytes)
+          uint8_t* qsc = qscr ? qscr + (size_t)c * (kChunkQ + kQScrFT) : nullptr;
+          if (greuse) {  // copy the chunk back from L2 (each lane its own digit bytes; lanes < 2 NB the F, T)
+            const uint4* src = (const uint4*)qsc + lane * (kChunkQ / 512);
+            uint4 d[kChunkQ / 512];
+  #pragma unroll
+            for (int i = 0; i < kChunkQ / 512; ++i) d[i] = __ldcg(src + i);
+            const int ft = lane < 2 * NB ? __ldcg((const int*)(qsc + kChunkQ) + lane) : 0;
+  #pragma unroll
+            for (int i = 0; i < kChunkQ / 512; ++i) ((uint4*)xq)[lane * (kChunkQ / 512) + i] = d[i];
+            if (lane < 2 * NB) wq[qs * NB * 2 + lane] = ft;
+            __syncwarp();
+          } else if (!reuse) {
+            int F[NB], T[NB];
+  #ifdef DBF_ENGINE_WARP_TRACE
+            quantize_chunk_tokens<NB>(in, c, ep_in, xq, batch, F, T, (wt && c == warp) ? wt + 10 : nullptr);
+  #else
+            quantize_chunk_tokens<NB>(in, c, ep_in, xq, batch, F, T);
+  #endif
+  #pragma unroll
+            for (int t = 0; t < NB; ++t)
+              if (lane == 0) wq[(qs * NB + t) * 2] = F[t], wq[(qs * NB + t) * 2 + 1] = T[t];
+            __syncwarp();
+            if (qsc) {  // keep it for the stage's later runs
+              uint4* dst = (uint4*)qsc + lane * (kChunkQ / 512);
+  #pragma unroll
+              for (int i = 0; i < kChunkQ / 512; ++i) __stcg(dst + i, ((const uint4*)xq)[lane * (kChunkQ / 512) + i]);
+              if (lane < 2 * NB) __stcg((int*)(qsc + kChunkQ) + lane, wq[qs * NB * 2 + lane]);
+            }
+          }
+          const int2 ftt = *(const int2*)(wq + (qs * NB + (tig < NB ? tig : 0)) * 2);
+          Ft = ftt.x, Tt = ftt.y;
+        }
+        if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
+        { const int jj = c / kWarps; if (jj < 3) WT(2 + jj); }
+        uint2 b[8];
+  #pragma unroll
+        for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * NB * 64 + xlane);
+        const float inv = __int_as_float((127 - Ft) << 23) * kQInv;  // 1 / (2^F * kQScale)
+        // units in pairs: two independent MMA streams per warp (the second repeats the last unit
+        // when nunits is odd and is then discarded)
+  #pragma unroll
+        for (int p = 0; p < kMaxUnits / 2; ++p) {
+          const int u0 = 2 * p;
+          if (u0 >= nunits) break;
+          const bool has1 = u0 + 1 < nunits;
+          float v[2][2];
+          pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, Tt, lane, v);
+          acc0[u0] = __fmaf_rn(v[0][0], inv, acc0[u0]);
+          acc1[u0] = __fmaf_rn(v[0][1], inv, acc1[u0]);
+          if (u0 + 1 < kMaxUnits && has1) {
+            acc0[u0 + 1] = __fmaf_rn(v[1][0], inv, acc0[u0 + 1]);
+            acc1[u0 + 1] = __fmaf_rn(v[1][1], inv, acc1[u0 + 1]);
+          }
+        }
+        { const int jj = c / kWarps; if (jj < 3) WT(5 + jj); }
+        first = false;
+      }
+      if (tr && warp == 0 && lane == 0) tr[2] = gtimer();
+      // partials -> shared memory (double-buffered by run parity), then the compute warps meet once
+      if (tig < NB) {
+  #pragma unroll
+        for (int u = 0; u < kMaxUnits; ++u) {
+          if (u < nunits) {
+            float* pu = part + ((warp * kMaxUnits + u) * NB + tig) * 16;
+            pu[g] = acc0[u];
+            pu[g + 8] = acc1[u];
+          }
         }
       }
     }

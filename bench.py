@@ -423,7 +423,8 @@ def sharded_bench(world: int, rank: int, steps: int, warmup: int, barrier, dist=
     k sharded over the `world` GPUs of the run (word-aligned uneven shards).  Per shape and batch:
     the local partial alone, the NCCL path (partial -> NCCL all-reduce -> finalize) and the fused
     path (dbf_forward_allreduce: partials pushed to every peer's symmetric-memory buffer from the
-    GEMV2 epilogue).  Each timing replays a CUDA graph over enough distinct layer instances to
+    GEMV2 epilogue); at batch <= 4 also the decode-engine partial, its NCCL path and the engine with
+    the same all-reduce fused into its last stage (forward_allreduce_engine).  Each timing replays a CUDA graph over enough distinct layer instances to
     exceed 2x L2; µs are per layer, max over ranks."""
     import torch
 
@@ -473,12 +474,19 @@ def sharded_bench(world: int, rank: int, steps: int, warmup: int, barrier, dist=
                 torch.cuda.synchronize()
                 row["engine_vs_nccl_max_rel_diff"] = float(
                     ((y_e.float() - y_n.float()).abs().max() / y_n.float().abs().max().clamp_min(1e-30)).item())
+                y_fe = ar.forward(shards[0], X, engine=True)
+                torch.cuda.synchronize()
+                row["fused_engine_vs_engine_nccl_max_rel_diff"] = float(
+                    ((y_fe.float() - y_e.float()).abs().max() / y_e.float().abs().max().clamp_min(1e-30)).item())
                 g_pe = graph_of(lambda: [s.partial_engine(X) for s in shards])
                 g_ne = graph_of(lambda: [s.forward(X, engine=True) for s in shards])
-                ue = [mx(time_graph(gr, steps, warmup, barrier)) * 1e3 / inst for gr in (g_pe, g_ne)]
-                row.update({"us_partial_engine": ue[0], "us_nccl_path_engine": ue[1],
-                            "gbs_per_rank_partial_engine": bytes_rank / (ue[0] * 1e-6) / 1e9})
-                del g_pe, g_ne
+                g_fe = graph_of(lambda: [ar.forward(s, X, engine=True) for s in shards])
+                ue = [mx(time_graph(gr, steps, warmup, barrier)) * 1e3 / inst for gr in (g_pe, g_ne, g_fe)]
+                row.update({"us_partial_engine": ue[0], "us_nccl_path_engine": ue[1], "us_fused_engine": ue[2],
+                            "us_allreduce_nccl_engine": ue[1] - ue[0], "us_allreduce_fused_engine": ue[2] - ue[0],
+                            "gbs_per_rank_partial_engine": bytes_rank / (ue[0] * 1e-6) / 1e9,
+                            "gbs_per_rank_fused_engine": bytes_rank / (ue[2] * 1e-6) / 1e9})
+                del g_pe, g_ne, g_fe
             rows.append(row)
             del g_p, g_n, g_f, shards, ar
             torch.cuda.empty_cache()

@@ -295,6 +295,23 @@ typedef struct {
    * input chunks for the stage's later runs; NULL = re-quantize per run */
   void* qscratch;
   int64_t qscratch_cta_bytes;
+  /* k-sharded layers: one-shot all-reduce fused into the program's last stage, the
+   * engine counterpart of dbf_forward_allreduce (ar_world == 0: off).  Every segment with a plain
+   * output pushes its unscaled fp32 rows into slot ar_rank of every peer's receive buffer
+   * ([2][ar_world][ar_bt][rows] fp32, dbf_allreduce_recv_bytes), raises its row blocks in every
+   * peer's flag array (group 0 of [16][ar_world][nrb] u32, dbf_allreduce_flag_bytes) after one
+   * system-scope fence, waits for every rank's flags of those row blocks and writes
+   * y[t, r] = ar_a[r] * sum over ranks in rank order (fp64, rounded once to fp32) to the plain
+   * output (y_override or out_plain) as dtype ar_ydt, row stride ar_ldy.  The call's epoch is
+   * *ar_epoch + 1 (the counter dbf_forward_allreduce also uses; the launch's last CTA advances
+   * it), so calls of both paths may share one set of buffers. */
+  const uint64_t* ar_recv;            /* device array [ar_world] of receive-buffer addresses    */
+  const uint64_t* ar_flags;           /* device array [ar_world] of flag-array addresses        */
+  uint32_t* ar_epoch;                 /* device call counter                                    */
+  const void* ar_a;                   /* output scale a (n), dtype ar_sdt                       */
+  int32_t ar_world, ar_rank, ar_bt, ar_sdt;
+  int32_t ar_ydt, ar_pad;
+  int64_t ar_ldy;
 } dbf_engine_program;
 
 /*

@@ -144,6 +144,15 @@ __device__ __forceinline__ uint4 ld_ll16x4(const uint32_t* p) {
                : "memory");
   return v;
 }
+__device__ __forceinline__ void st_relaxed_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -492,6 +501,101 @@ __device__ __forceinline__ void quantize_chunk_tokens(const InSpec& in, int c, u
   }
 }
 
+// Fused one-shot all-reduce (dbf_engine_program.ar_*), once per CTA after its last run: every
+// finalize already pushed this rank's partial rows to every peer, so the 16 compute warps meet,
+// thread 0 issues ONE system-scope fence and raises the row blocks of the CTA's plain-output runs
+// in every peer's flags (a fence per run cost ~10 us per layer: measured), the (row block, rank)
+// flags are polled in parallel (20 s watchdog), then y = a * sum over ranks in rank order (fp64,
+// rounded once to fp32) -- the same bits on every rank, and the same formula as
+// dbf_forward_allreduce's combine (csrc/decode.cu).
+struct ArArgs {
+  const uint64_t* recv;
+  const uint64_t* flags;
+  const void* a;
+  uint32_t* epoch;
+  int world, rank, bt, sdt, ydt;
+  int64_t ldy;
+  void* y_override;
+};
+
+// the kernel's view of dbf_engine_program without the ar_* tail (which travels as a separate,
+// trailing kernel parameter, so the plain engine's parameter layout is unchanged)
+struct EngineCore {
+  const dbf_engine_run* runs;
+  const int32_t* cta_offsets;
+  uint32_t* run_counter;
+  int64_t* trace;
+  int32_t nvectors, grid, max_cols, batch;
+  const void* x_override;
+  void* y_override;
+  void* qscratch;
+  int64_t qscratch_cta_bytes;
+};
+
+__device__ __noinline__ void allreduce_cta(const ArArgs ar, const dbf_engine_run* R, int r0, int r1, int batch,
+                                           uint32_t ep) {
+  asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");  // every push of the CTA issued
+  if (threadIdx.x == 0) {
+#ifdef DBF_AR_FENCE_GPU  // experiment only (not valid across GPUs): the fence's own cost at world 1
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
+    for (int i = r0; i < r1; ++i) {
+      if (!R[i].out_plain) continue;
+      const int nrb = (R[i].rows + kRowBlock - 1) / kRowBlock, rb = R[i].rb;
+      for (int u = 0; u < R[i].nunits; ++u)
+        for (int g2 = 0; g2 < ar.world; ++g2)
+          st_relaxed_sys_u32((uint32_t*)ar.flags[g2] + (size_t)ar.rank * nrb + rb + u, ep);
+    }
+  }
+  const uint32_t* myflags = (const uint32_t*)ar.flags[ar.rank];
+  for (int i = r0; i < r1; ++i) {
+    if (!R[i].out_plain) continue;
+    const int nrb = (R[i].rows + kRowBlock - 1) / kRowBlock, rb = R[i].rb, nunits = R[i].nunits;
+    for (int j = threadIdx.x; j < nunits * ar.world; j += kWarps * 32) {
+      const uint32_t* f = myflags + (size_t)(j % ar.world) * nrb + rb + j / ar.world;
+      const long long t0 = gtimer();
+      // epochs only grow: a peer already on its next call has also pushed this one
+      while ((int32_t)(ld_acquire_sys_u32(f) - ep) < 0) {
+        __nanosleep(32);
+        if (gtimer() - t0 > 20ll * 1000 * 1000 * 1000) __trap();  // 20 s watchdog: a peer is gone
+      }
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+  for (int i = r0; i < r1; ++i) {
+    if (!R[i].out_plain) continue;
+    void* y = ar.y_override ? ar.y_override : R[i].out_plain;
+    const int rows = R[i].rows, rb = R[i].rb, nunits = R[i].nunits;
+    const float* recv = (const float*)ar.recv[ar.rank] + (size_t)(ep & 1u) * ar.world * ar.bt * rows;
+    for (int j = threadIdx.x; j < nunits * 16 * batch; j += kWarps * 32) {
+      const int t = (j >> 4) % batch, row = (rb + j / (16 * batch)) * 16 + (j & 15);
+      if (row >= rows) continue;
+      double acc = 0.0;
+      for (int src = 0; src < ar.world; ++src)
+        acc += (double)__ldcg(recv + ((size_t)src * ar.bt + t) * rows + row);
+      double a = 1.0;
+      if (ar.a) {
+        switch (ar.sdt) {
+          case DBF_F16: a = (double)__half2float(((const __half*)ar.a)[row]); break;
+          case DBF_F32: a = (double)((const float*)ar.a)[row]; break;
+          case DBF_F64: a = ((const double*)ar.a)[row]; break;
+          default: a = (double)__bfloat162float(((const __nv_bfloat16*)ar.a)[row]); break;
+        }
+      }
+      const double v = (double)(float)acc * a;
+      const int64_t o = (int64_t)t * ar.ldy + row;
+      switch (ar.ydt) {
+        case DBF_F16: ((__half*)y)[o] = __float2half_rn((float)v); break;
+        case DBF_F32: ((float*)y)[o] = (float)v; break;
+        case DBF_F64: ((double*)y)[o] = v; break;
+        default: ((__nv_bfloat16*)y)[o] = __float2bfloat16_rn((float)v); break;
+      }
+    }
+  }
+}
+
 // The MMAs of units u0 and u0 + 1 (has1) against chunk c of the run (signs resident in the ring),
 // as the two units' exact chunk sums P = s/4 - T (as floats) v[unit][row g / g + 8] of this lane's
 // token; the caller accumulates acc = fma(P, 1 / (2^F kQScale), acc) with an explicit FMA (left
@@ -544,8 +648,10 @@ __device__ __forceinline__ void pair_mma(const uint8_t* ring, int ring_slots, in
         }
 }
 
-template <int NB, int XS>
-__global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program prog, int ring_slots) {
+// AR: the program's last stage carries the fused all-reduce (dbf_engine_program.ar_*); a separate
+// instantiation, so the plain engine carries none of its code (measured +1.3-7 % when shared)
+template <int NB, int XS, bool AR>
+__global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, int ring_slots, ArArgs ar) {
   constexpr int kMaxUnits = max_units<NB>();
   constexpr int kChunkQ = kChunkQBytes1 * NB, kPartFloats = kWarps * kMaxUnits * 16 * NB;
   // quantized chunks kept per warp (xs_chunks_of: sized by the program's widest input at batch 1)
@@ -589,6 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
   const int r0 = prog.cta_offsets[blockIdx.x], r1 = prog.cta_offsets[blockIdx.x + 1];
   if (threadIdx.x == 0) {
     *ep_base_s = (uint32_t)(((uint64_t)*prog.run_counter * (uint64_t)prog.nvectors) % 65535ull);
+    if (AR) ep_base_s[1] = *ar.epoch + 1u;  // this call's all-reduce epoch
     inkey[0].vec = inkey[1].vec = -1;
     inkey[0].iscale = inkey[1].iscale = nullptr;
   }
@@ -913,8 +1020,17 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
           const int64_t ll_stride = (int64_t)((ro.rows + kChunkCols - 1) / kChunkCols) * kChunkCols;
           if (ro.ll_out) st_ll16(ro.ll_out + t * ll_stride + row, h, ro.ep_out);
           if (ro.out_plain) {
-            if (ro.odt == DBF_F16) ((__half*)ro.out_plain)[(int64_t)t * ro.rows + row] = h;
-            else ((float*)ro.out_plain)[(int64_t)t * ro.rows + row] = v;  // fp32 output: unrounded
+            if (AR) {
+              // fused all-reduce, push half: the unrounded fp32 partial into slot ar_rank of every
+              // peer's receive buffer (NVLink P2P stores through the mapped peer addresses)
+              const size_t idx = (size_t)(ep_base_s[1] & 1u) * ar.world * ar.bt * ro.rows +
+                                 ((size_t)ar.rank * ar.bt + t) * ro.rows + row;
+              for (int g2 = 0; g2 < ar.world; ++g2) ((float*)ar.recv[g2])[idx] = v;
+            } else if (ro.odt == DBF_F16) {
+              ((__half*)ro.out_plain)[(int64_t)t * ro.rows + row] = h;
+            } else {
+              ((float*)ro.out_plain)[(int64_t)t * ro.rows + row] = v;  // fp32 output: unrounded
+            }
           }
         }
       }
@@ -929,11 +1045,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(dbf_engine_program 
     }
     __syncwarp();
   }
+  if constexpr (AR)
+    allreduce_cta(ar, R, r0, r1, batch, ep_base_s[1]);
   // the last CTA to finish advances the launch counter (every CTA read it at its start, and the
   // next launch is stream-ordered after this one): no separate advance kernel per step
   if (warp == 0 && lane == 0 && atomicAdd(prog.run_counter + 1, 1u) == gridDim.x - 1) {
     prog.run_counter[1] = 0u;
     prog.run_counter[0] += 1u;
+    if (AR) *ar.epoch += 1u;  // every CTA read it at its start
   }
 }
 
@@ -1070,11 +1189,11 @@ extern "C" int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, in
   int st = dbf_engine_smem_bytes(max_cols, 1, &smem);
   if (st != DBF_OK) return st;
   return engine::xs_chunks_of(1, max_cols) == DBF_XS_CHUNKS1
-             ? engine_occupancy_of(engine::engine_kernel<1, DBF_XS_CHUNKS1>, smem, blocks_per_sm, regs_per_thread)
-             : engine_occupancy_of(engine::engine_kernel<1, DBF_XS_CHUNKS1_MAX>, smem, blocks_per_sm, regs_per_thread);
+             ? engine_occupancy_of(engine::engine_kernel<1, DBF_XS_CHUNKS1, false>, smem, blocks_per_sm, regs_per_thread)
+             : engine_occupancy_of(engine::engine_kernel<1, DBF_XS_CHUNKS1_MAX, false>, smem, blocks_per_sm, regs_per_thread);
 }
 
-template <int NB, int XS>
+template <int NB, int XS, bool AR>
 static int engine_launch_nb(const dbf_engine_program* program, cudaStream_t s) {
   size_t smem = 0;
   int st = dbf_engine_smem_bytes(program->max_cols, NB, &smem);
@@ -1082,7 +1201,7 @@ static int engine_launch_nb(const dbf_engine_program* program, cudaStream_t s) {
   const int slots = engine::ring_slots(NB, program->max_cols);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel<NB, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel<NB, XS, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          engine::kMaxSmem);
     if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
     configured = true;
@@ -1097,27 +1216,43 @@ static int engine_launch_nb(const dbf_engine_program* program, cudaStream_t s) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  dbf_engine_program prog = *program;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, engine::engine_kernel<NB, XS>, prog, slots);
+  const dbf_engine_program& p = *program;
+  const engine::EngineCore core{p.runs, p.cta_offsets, p.run_counter, p.trace, p.nvectors, p.grid, p.max_cols,
+                                p.batch, p.x_override, p.y_override, p.qscratch, p.qscratch_cta_bytes};
+  const engine::ArArgs ar{p.ar_recv, p.ar_flags, p.ar_a, p.ar_epoch, p.ar_world, p.ar_rank, p.ar_bt, p.ar_sdt,
+                          p.ar_ydt, p.ar_ldy, p.y_override};
+  cudaError_t e = cudaLaunchKernelEx(&cfg, engine::engine_kernel<NB, XS, AR>, core, slots, ar);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   return DBF_OK;
+}
+
+template <bool AR>
+static int engine_launch_ar(const dbf_engine_program* program, cudaStream_t s) {
+  const int nb = engine::nb_for(program->batch);
+  int st;
+  if (nb == 1)
+    st = engine::xs_chunks_of(1, program->max_cols) == DBF_XS_CHUNKS1
+             ? engine_launch_nb<1, DBF_XS_CHUNKS1, AR>(program, s)
+             : engine_launch_nb<1, DBF_XS_CHUNKS1_MAX, AR>(program, s);
+  else
+    st = nb == 2 ? engine_launch_nb<2, 4, AR>(program, s)
+                 : (engine::xs_chunks_of(4, program->max_cols) == 2 ? engine_launch_nb<4, 2, AR>(program, s)
+                                                                     : engine_launch_nb<4, 1, AR>(program, s));
+  if (st != DBF_OK) return st;
+  return check_launch();
 }
 
 extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream) {
   if (!program || !program->runs || !program->cta_offsets || !program->run_counter || program->grid < 1 ||
       program->max_cols < 1 || program->batch < 1 || program->batch > 4)
     return DBF_ERR_INVALID_ARGUMENT;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int nb = engine::nb_for(program->batch);
-  int st;
-  if (nb == 1)
-    st = engine::xs_chunks_of(1, program->max_cols) == DBF_XS_CHUNKS1
-             ? engine_launch_nb<1, DBF_XS_CHUNKS1>(program, s)
-             : engine_launch_nb<1, DBF_XS_CHUNKS1_MAX>(program, s);
-  else
-    st = nb == 2 ? engine_launch_nb<2, 4>(program, s)
-                 : (engine::xs_chunks_of(4, program->max_cols) == 2 ? engine_launch_nb<4, 2>(program, s)
-                                                                     : engine_launch_nb<4, 1>(program, s));
-  if (st != DBF_OK) return st;
-  return check_launch();
+  if (program->ar_world &&
+      (program->ar_world < 0 || program->ar_world > 64 || program->ar_rank < 0 ||
+       program->ar_rank >= program->ar_world || !program->ar_recv || !program->ar_flags || !program->ar_epoch ||
+       program->ar_bt < program->batch || program->ar_ldy < 1 || program->ar_ydt < DBF_F16 || program->ar_ydt > DBF_BF16 ||
+       (program->ar_a && (program->ar_sdt < DBF_F16 || program->ar_sdt > DBF_BF16))))
+    return DBF_ERR_INVALID_ARGUMENT;
+  return program->ar_world ? engine_launch_ar<true>(program, (cudaStream_t)stream)
+                           : engine_launch_ar<false>(program, (cudaStream_t)stream);
 }
+

@@ -56,6 +56,17 @@ class _Program(ctypes.Structure):
         ("y_override", ctypes.c_void_p),
         ("qscratch", ctypes.c_void_p),
         ("qscratch_cta_bytes", ctypes.c_int64),
+        ("ar_recv", ctypes.c_void_p),
+        ("ar_flags", ctypes.c_void_p),
+        ("ar_epoch", ctypes.c_void_p),
+        ("ar_a", ctypes.c_void_p),
+        ("ar_world", ctypes.c_int32),
+        ("ar_rank", ctypes.c_int32),
+        ("ar_bt", ctypes.c_int32),
+        ("ar_sdt", ctypes.c_int32),
+        ("ar_ydt", ctypes.c_int32),
+        ("ar_pad", ctypes.c_int32),
+        ("ar_ldy", ctypes.c_int64),
     ]
 
 
@@ -306,6 +317,27 @@ class EngineProgram:
             raise ValueError(f"y must be a contiguous {tuple(out.shape)} {out.dtype} tensor")
         prog = _Program.from_buffer_copy(self._prog)
         prog.x_override, prog.y_override = x.data_ptr(), y.data_ptr()
+        _lib.check(_lib.lib.dbf_engine_launch(ctypes.byref(prog), _lib.stream_ptr(stream)), "dbf_engine_launch")
+
+    def launch_allreduce(self, x, y, peer_recv, peer_flags, epoch_counter, world: int, rank: int, a,
+                         stream=None):
+        """Launch on caller buffers with the one-shot all-reduce fused into the last stage
+        (dbf_engine_program.ar_*): the final plain output is pushed to every rank's receive
+        buffer and y = a * (sum over ranks) is written to ``y`` (batch x n, any io dtype)."""
+        inp = self.plan.buffers[self.plan.input_buffer]
+        out = self.plan.buffers[self.plan.output_buffer]
+        if x.shape != inp.shape or x.dtype != inp.dtype or not x.is_contiguous():
+            raise ValueError(f"x must be a contiguous {tuple(inp.shape)} {inp.dtype} tensor")
+        if y.shape != out.shape or y.stride(1) != 1:
+            raise ValueError(f"y must be a {tuple(out.shape)} tensor with unit column stride")
+        if not 1 <= world <= 8 or not 0 <= rank < world:
+            raise ValueError("world must be 1..8 and 0 <= rank < world")
+        prog = _Program.from_buffer_copy(self._prog)
+        prog.x_override, prog.y_override = x.data_ptr(), y.data_ptr()
+        prog.ar_recv, prog.ar_flags, prog.ar_epoch = peer_recv.data_ptr(), peer_flags.data_ptr(), epoch_counter.data_ptr()
+        prog.ar_a, prog.ar_sdt = a.data_ptr(), _lib.dtype_code(a.dtype)
+        prog.ar_world, prog.ar_rank, prog.ar_bt = world, rank, x.shape[0]
+        prog.ar_ydt, prog.ar_ldy = _lib.dtype_code(y.dtype), y.stride(0)
         _lib.check(_lib.lib.dbf_engine_launch(ctypes.byref(prog), _lib.stream_ptr(stream)), "dbf_engine_launch")
 
     def kernel_launches_per_step(self) -> int:

@@ -181,11 +181,19 @@ class DeviceShard:
         writes P through the launch-time I/O overrides, so calls cost one engine launch."""
         import torch
 
+        X2 = X if X.ndim == 2 else X.unsqueeze(0)
+        X2 = X2.contiguous()
+        prog = self._engine_program(X2)
+        P = torch.empty((X2.shape[0], self.shard.n), dtype=torch.float32, device=X2.device)
+        prog.launch_io(X2, P)
+        return P
+
+    def _engine_program(self, X2):
+        import torch
+
         from .engine import EngineProgram
         from .plan import DecodePlan, PlanOp
 
-        X2 = X if X.ndim == 2 else X.unsqueeze(0)
-        X2 = X2.contiguous()
         batch = X2.shape[0]
         if not 1 <= batch <= 4 or X2.dtype not in (torch.float16, torch.float32):
             raise ValueError("partial_engine runs 1..4 fp16/fp32 tokens (use partial for others)")
@@ -198,10 +206,23 @@ class DeviceShard:
                     torch.zeros((batch, sh.n), dtype=torch.float32, device=X2.device)]
             plan = DecodePlan([view], [PlanOp(0, 0, 1, "partial")], bufs, input_buffer=0, output_buffer=1)
             progs[key] = (EngineProgram(plan), plan)
-        prog, _ = progs[key]
-        P = torch.empty((batch, self.shard.n), dtype=torch.float32, device=X2.device)
-        prog.launch_io(X2, P)
-        return P
+        return progs[key][0]
+
+    def forward_allreduce_engine(self, X, peer_recv, peer_flags, epoch_counter, out_dtype=None):
+        """The layer through the decode engine with the one-shot all-reduce fused into its last
+        stage (one launch per call): GEMV1 -> LL t -> GEMV2, whose finalize pushes the fp32 partial
+        rows into every rank's receive buffer, raises the row blocks' flags, waits for every rank's
+        and writes y = a * sum over ranks.  Same buffers, flags and call counter as
+        ``forward_allreduce`` (``FusedAllReduce``); batch 1..4, fp16 / fp32 X."""
+        import torch
+
+        sh = self.shard
+        X2 = X if X.ndim == 2 else X.unsqueeze(0)
+        X2 = X2.contiguous()
+        prog = self._engine_program(X2)
+        Y = torch.empty((X2.shape[0], sh.n), dtype=out_dtype or X2.dtype, device=X2.device)
+        prog.launch_allreduce(X2, Y, peer_recv, peer_flags, epoch_counter, sh.world, sh.rank, self.a)
+        return Y
 
     def finalize(self, P, out_dtype=None):
         import torch
@@ -300,12 +321,14 @@ class FusedAllReduce:
         self._handles = (hr, hf)
         dist.barrier(group=grp)  # every rank's flags are zero before anyone pushes
 
-    def forward(self, shard: "DeviceShard", X, out_dtype=None):
+    def forward(self, shard: "DeviceShard", X, out_dtype=None, engine: bool = False):
+        """engine=True: the decode-engine path (``forward_allreduce_engine``, batch <= 4)."""
         if (X.shape[0] if X.ndim == 2 else 1) > self.batch or shard.shard.n != self.n:
             raise ValueError("layer/batch larger than this FusedAllReduce was sized for")
         if shard.shard.world != self.world or shard.shard.rank != self.rank:
             raise ValueError("shard rank/world do not match the process group")
-        return shard.forward_allreduce(X, self.peer_recv, self.peer_flags, self.counter, out_dtype=out_dtype)
+        fwd = shard.forward_allreduce_engine if engine else shard.forward_allreduce
+        return fwd(X, self.peer_recv, self.peer_flags, self.counter, out_dtype=out_dtype)
 
 
 def reduce_partials_host(partials, a) -> np.ndarray:

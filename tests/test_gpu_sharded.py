@@ -210,3 +210,123 @@ def test_fused_allreduce_symmetric_memory_single_rank():
         assert int(ar.counter.item()) == 3 + 1 + 4  # eager calls, warm-up call, replays (capture runs nothing)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [1, 3, 4])
+def test_engine_fused_allreduce_single_rank_equals_engine_partial(batch):
+    """world = 1 through the decode engine: the fused push / flag / combine in the last stage gives
+    the same bits as partial_engine + dbf_finalize_partial, over several calls (both buffer
+    parities); the call counter and this rank's flags advance once per call."""
+    import torch
+
+    from paper_2505_11076_b200 import _lib
+
+    rng = np.random.default_rng(30 + batch)
+    n, k, m = 1000, 640, 1024
+    layer = _host_layer(rng, n, k, m)
+    ds = sharded.DeviceShard(sharded.shard_layer(layer, 0, 1), scale_dtype=torch.float16)
+    recv = torch.empty(_lib.lib.dbf_allreduce_recv_bytes(n, batch, 1) // 4, dtype=torch.float32, device="cuda")
+    flags = torch.zeros(_lib.lib.dbf_allreduce_flag_bytes(n, 1) // 4, dtype=torch.int32, device="cuda")
+    counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for epoch in range(1, 5):
+        X = torch.from_numpy(rng.standard_normal((batch, m)).astype(np.float16)).cuda()
+        ref = ds.finalize(ds.partial_engine(X), out_dtype=torch.float16)
+        y = ds.forward_allreduce_engine(X, _ptrs([recv]), _ptrs([flags]), counter)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref), epoch
+        assert int(counter.item()) == epoch
+        assert int(flags.view(16, 1, -1)[0].min()) == epoch
+    # the per-layer fused path shares the counter / flags / buffers: calls of both paths interleave
+    y2 = ds.forward_allreduce(X, _ptrs([recv]), _ptrs([flags]), counter)
+    y3 = ds.forward_allreduce_engine(X, _ptrs([recv]), _ptrs([flags]), counter)
+    torch.cuda.synchronize()
+    assert int(counter.item()) == 6 and torch.equal(y3, ref)
+    out = oracle.c_forward(X.double().cpu().numpy(), layer.a, layer.A.bits, layer.mid, layer.B.bits, layer.b)
+    for v in (y, y2, y3):
+        assert rel_max(v.float().cpu().numpy(), out) <= 1e-2 and rel_norm(v.float().cpu().numpy(), out) <= 1e-2
+
+
+@pytest.mark.parametrize("world,rank,batch", [(2, 1, 1), (4, 0, 4), (8, 5, 2)])
+def test_engine_fused_allreduce_combines_pushed_peer_partials(world, rank, batch):
+    """One rank of a `world`-GPU group through the engine, the other ranks' pushes staged
+    beforehand (no kernel waits on another): y = a * (sum of all ranks' engine partials in rank
+    order) bit for bit, and this rank's partial lands in slot `rank` of every peer buffer."""
+    import torch
+
+    from paper_2505_11076_b200 import _lib
+
+    rng = np.random.default_rng(world * 100 + rank)
+    n, k, m = 1000, 1792, 2048
+    layer = _host_layer(rng, n, k, m)
+    X = torch.from_numpy(rng.standard_normal((batch, m)).astype(np.float16)).cuda()
+    shards = [sharded.DeviceShard(sharded.shard_layer(layer, g, world), scale_dtype=torch.float16) for g in range(world)]
+    parts = [s.partial_engine(X) for s in shards]
+    nrb = -(-n // 16)
+    recvs = [torch.zeros(_lib.lib.dbf_allreduce_recv_bytes(n, batch, world) // 4, dtype=torch.float32, device="cuda")
+             for _ in range(world)]
+    flags = [torch.zeros(_lib.lib.dbf_allreduce_flag_bytes(n, world) // 4, dtype=torch.int32, device="cuda")
+             for _ in range(world)]
+    counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for epoch in (1, 2, 3):
+        mine = recvs[rank].view(2, world, batch, n)[epoch & 1]
+        fl = flags[rank].view(16, world, nrb)
+        for g in range(world):
+            if g != rank:
+                mine[g].copy_(parts[g])
+                fl[0, g, :] = epoch
+        torch.cuda.synchronize()
+        y = shards[rank].forward_allreduce_engine(X, _ptrs(recvs), _ptrs(flags), counter, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        acc = np.zeros((batch, n))
+        for g in range(world):
+            acc += parts[g].double().cpu().numpy()
+        a = shards[rank].a.double().cpu().numpy()
+        want = (acc.astype(np.float32).astype(np.float64) * a[None, :]).astype(np.float32)
+        np.testing.assert_array_equal(y.cpu().numpy(), want)
+        for g in range(world):
+            assert torch.equal(recvs[g].view(2, world, batch, n)[epoch & 1][rank], parts[rank])
+            assert int(flags[g].view(16, world, nrb)[0, rank].min()) == epoch
+    ref = oracle.c_forward(X.double().cpu().numpy(), layer.a, layer.A.bits, layer.mid, layer.B.bits, layer.b)
+    assert rel_max(y.cpu().numpy(), ref) <= 1e-2 and rel_norm(y.cpu().numpy(), ref) <= 1e-2
+
+
+def test_engine_fused_allreduce_symmetric_memory_single_rank():
+    """FusedAllReduce.forward(engine=True) over a 1-rank NCCL group (symmetric-memory buffers):
+    equal to the engine partial + NCCL all-reduce path, eager and graph-replayed."""
+    import torch
+    import torch.distributed as dist
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(19)
+        layer = _host_layer(rng, 512, 640, 1024)
+        ds = sharded.DeviceShard(sharded.shard_layer(layer, 0, 1), scale_dtype=torch.float16)
+        try:
+            ar = sharded.FusedAllReduce(512, 4)
+        except Exception as e:  # noqa: BLE001 - symmetric memory needs driver/fabric support
+            pytest.skip(f"torch symmetric memory unavailable: {e}")
+        for _ in range(3):
+            X = torch.from_numpy(rng.standard_normal((4, 1024)).astype(np.float16)).cuda()
+            assert torch.equal(ar.forward(ds, X, engine=True), ds.forward(X, engine=True))
+        X = torch.from_numpy(rng.standard_normal((4, 1024)).astype(np.float16)).cuda()
+        ref = ds.forward(X, engine=True)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            ar.forward(ds, X, engine=True)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            yg = ar.forward(ds, X, engine=True)
+        for _ in range(4):
+            yg.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(yg, ref)
+        assert int(ar.counter.item()) == 3 + 1 + 4
+    finally:
+        dist.destroy_process_group()

@@ -532,9 +532,23 @@ struct EngineCore {
   int64_t qscratch_cta_bytes;
 };
 
+struct ArRun {
+  void* out_plain;
+  int rows, rb, nunits, pad;
+};
+
 __device__ __noinline__ void allreduce_cta(const ArArgs ar, const dbf_engine_run* R, int r0, int r1, int batch,
-                                           uint32_t ep) {
+                                           uint32_t ep, ArRun* rs, int rs_cap) {
   asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");  // every push of the CTA issued
+  // the CTA's run records, fetched once in parallel into shared memory (rs: the partial-sum area,
+  // free now): walking them from global memory one by one cost ~1 us per run and loop (measured)
+  const int nr = min(r1 - r0, rs_cap);
+  for (int i = threadIdx.x; i < nr; i += kWarps * 32)
+    rs[i] = ArRun{R[r0 + i].out_plain, R[r0 + i].rows, R[r0 + i].rb, R[r0 + i].nunits, 0};
+  asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+  auto run = [&](int i) -> ArRun {
+    return i - r0 < nr ? rs[i - r0] : ArRun{R[i].out_plain, R[i].rows, R[i].rb, R[i].nunits, 0};
+  };
   if (threadIdx.x == 0) {
 #ifdef DBF_AR_FENCE_GPU  // experiment only (not valid across GPUs): the fence's own cost at world 1
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -542,19 +556,21 @@ __device__ __noinline__ void allreduce_cta(const ArArgs ar, const dbf_engine_run
     asm volatile("fence.acq_rel.sys;" ::: "memory");
 #endif
     for (int i = r0; i < r1; ++i) {
-      if (!R[i].out_plain) continue;
-      const int nrb = (R[i].rows + kRowBlock - 1) / kRowBlock, rb = R[i].rb;
-      for (int u = 0; u < R[i].nunits; ++u)
+      const ArRun r = run(i);
+      if (!r.out_plain) continue;
+      const int nrb = (r.rows + kRowBlock - 1) / kRowBlock;
+      for (int u = 0; u < r.nunits; ++u)
         for (int g2 = 0; g2 < ar.world; ++g2)
-          st_relaxed_sys_u32((uint32_t*)ar.flags[g2] + (size_t)ar.rank * nrb + rb + u, ep);
+          st_relaxed_sys_u32((uint32_t*)ar.flags[g2] + (size_t)ar.rank * nrb + r.rb + u, ep);
     }
   }
   const uint32_t* myflags = (const uint32_t*)ar.flags[ar.rank];
   for (int i = r0; i < r1; ++i) {
-    if (!R[i].out_plain) continue;
-    const int nrb = (R[i].rows + kRowBlock - 1) / kRowBlock, rb = R[i].rb, nunits = R[i].nunits;
-    for (int j = threadIdx.x; j < nunits * ar.world; j += kWarps * 32) {
-      const uint32_t* f = myflags + (size_t)(j % ar.world) * nrb + rb + j / ar.world;
+    const ArRun r = run(i);
+    if (!r.out_plain) continue;
+    const int nrb = (r.rows + kRowBlock - 1) / kRowBlock;
+    for (int j = threadIdx.x; j < r.nunits * ar.world; j += kWarps * 32) {
+      const uint32_t* f = myflags + (size_t)(j % ar.world) * nrb + r.rb + j / ar.world;
       const long long t0 = gtimer();
       // epochs only grow: a peer already on its next call has also pushed this one
       while ((int32_t)(ld_acquire_sys_u32(f) - ep) < 0) {
@@ -565,9 +581,10 @@ __device__ __noinline__ void allreduce_cta(const ArArgs ar, const dbf_engine_run
   }
   asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
   for (int i = r0; i < r1; ++i) {
-    if (!R[i].out_plain) continue;
-    void* y = ar.y_override ? ar.y_override : R[i].out_plain;
-    const int rows = R[i].rows, rb = R[i].rb, nunits = R[i].nunits;
+    const ArRun r = run(i);
+    if (!r.out_plain) continue;
+    void* y = ar.y_override ? ar.y_override : r.out_plain;
+    const int rows = r.rows, rb = r.rb, nunits = r.nunits;
     const float* recv = (const float*)ar.recv[ar.rank] + (size_t)(ep & 1u) * ar.world * ar.bt * rows;
     for (int j = threadIdx.x; j < nunits * 16 * batch; j += kWarps * 32) {
       const int t = (j >> 4) % batch, row = (rb + j / (16 * batch)) * 16 + (j & 15);
@@ -1046,7 +1063,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
     __syncwarp();
   }
   if constexpr (AR)
-    allreduce_cta(ar, R, r0, r1, batch, ep_base_s[1]);
+    allreduce_cta(ar, R, r0, r1, batch, ep_base_s[1], (ArRun*)sm.part,
+                  (int)(2 * kPartFloats * sizeof(float) / sizeof(ArRun)));
   // the last CTA to finish advances the launch counter (every CTA read it at its start, and the
   // next launch is stream-ordered after this one): no separate advance kernel per step
   if (warp == 0 && lane == 0 && atomicAdd(prog.run_counter + 1, 1u) == gridDim.x - 1) {

@@ -86,3 +86,40 @@ def test_engine_run_records_resolve_everything_on_the_host():
     assert i32[32 + 27] == 3  # in_producers of vec1 = ceil(40/16) units of segment 0
     bad = np.array([[1, 4, 2]], dtype=np.int32)  # rows 64..95 of a 70-row segment: out of range
     assert _lib.lib.dbf_engine_build_runs(segs.ctypes.data, 2, vecs.ctypes.data, 3, bad.ctypes.data, 1, 1, ready, out.ctypes.data) == _lib.ERR_SHAPE
+
+
+def test_python_struct_mirrors_match_the_c_layout(tmp_path):
+    """The ctypes / numpy mirrors of the engine structs (engine.py) have the C header's size and
+    field offsets (gcc compiles a probe against include/dbf_b200.h; no CUDA needed)."""
+    import shutil
+    import subprocess
+
+    from paper_2505_11076_b200 import engine
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    prog = [f[0] for f in engine._Program._fields_]
+    probes = [("dbf_engine_program", n) for n in prog]
+    probes += [("dbf_engine_segment", n) for n in engine.SEG_DTYPE.names]
+    probes += [("dbf_engine_vector", n) for n in engine.VEC_DTYPE.names]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dbf_b200.h"', "int main(void) {"]
+    for t in ("dbf_engine_program", "dbf_engine_segment", "dbf_engine_vector"):
+        lines.append(f'  printf("{t} size %zu\\n", sizeof({t}));')
+    for t, n in probes:
+        lines.append(f'  printf("{t} {n} %zu\\n", offsetof({t}, {n}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-std=c11", f"-I{HEADER.parent}", str(src), "-o", str(exe)], check=True)
+    c = {}
+    for line in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines():
+        t, n, v = line.split()
+        c[(t, n)] = int(v)
+    assert c[("dbf_engine_program", "size")] == ctypes.sizeof(engine._Program)
+    for f in engine._Program._fields_:
+        assert c[("dbf_engine_program", f[0])] == getattr(engine._Program, f[0]).offset, f[0]
+    for t, dt in (("dbf_engine_segment", engine.SEG_DTYPE), ("dbf_engine_vector", engine.VEC_DTYPE)):
+        assert c[(t, "size")] == dt.itemsize, t
+        for n in dt.names:
+            assert c[(t, n)] == dt.fields[n][1], (t, n)

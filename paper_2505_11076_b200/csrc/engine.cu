@@ -41,7 +41,13 @@ constexpr int kProdWarp = kWarps;             // producer warp index (first warp
 // sub-partition).  120 would fit the register file on paper but setmaxnreg.inc never returns
 // with it on B200 (measured); 112 does.
 constexpr int kThreads = (kWarps + 4) * 32;
-constexpr int kProdRegs = 24, kComputeRegs = 112;
+#ifndef DBF_COMPUTE_REGS
+#define DBF_COMPUTE_REGS 112  // setmaxnreg for the 16 compute warps (the producer warpgroup drops to 24)
+#endif
+constexpr int kProdRegs = 24, kComputeRegs = DBF_COMPUTE_REGS;
+// setmaxnreg.inc only draws on registers the producer warpgroup released (launch allocation 96 per
+// thread at 640 threads): asking for more blocks the compute warps forever (120 measured: hang)
+static_assert(16 * (kComputeRegs - 96) <= 4 * (96 - kProdRegs), "compute warps would wait for registers forever");
 constexpr int kSlotBytes = 16384;             // one ring slot = 32 chunks of 512 B
 #ifndef DBF_CHAINS
 #define DBF_CHAINS 1  // accumulator chains per unit (1, 2, 4 measured within 1 %; 1 issues fewest)

@@ -101,6 +101,41 @@ class DecodePlan:
         self._graph = None
         return self
 
+    def use_fastest(self, steps: int = 5, grid: int | None = None):
+        """Time the decode engine (groups of <= 4 tokens) against the tcgen05 prefill chain on
+        this plan's own buffers (CUDA graph replays, CUDA events) and keep the faster one -- the
+        crossover depends on model and batch (bench.py sweep: 13B at 8 tokens the engine 6.9 ms vs
+        the chain 11.7 ms; 70B at 16 tokens 85 ms vs 62 ms).  The chain is a candidate only for
+        fp16 activations on fp16-scaled layers that kept their sign words (keep_words=True).  The
+        input buffer is restored afterwards; the choice is in ``self.choice`` / ``self.choice_ms``."""
+        import torch
+
+        _lib.require_cuda()
+        cands = [("engine", lambda: self.use_engine(grid))]
+        if self.buffers[self.input_buffer].dtype == torch.float16 and all(
+                l.scale_dtype == torch.float16 and l.A.words is not None and l.B.words is not None
+                for l in self.layers):
+            cands.append(("prefill", self.use_prefill))
+        saved = self.buffers[self.input_buffer].clone()
+        timings = {}
+        for name, select in cands:
+            select()
+            self.capture()
+            for _ in range(2):
+                self.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                self.replay()
+            e1.record()
+            e1.synchronize()
+            timings[name] = e0.elapsed_time(e1) / steps
+        self.choice = min(timings, key=timings.get)
+        self.choice_ms = timings
+        dict(cands)[self.choice]()
+        self.buffers[self.input_buffer].copy_(saved)
+        return self
+
     def _eager(self):
         if self.engine is not None:
             self.engine.launch()

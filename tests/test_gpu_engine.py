@@ -156,3 +156,24 @@ def test_engine_ragged_layers_vs_oracle(batch, n, k, m, act):
     plan.engine.launch_io(x.clone(), y2)
     torch.cuda.synchronize()
     assert torch.equal(y2, bufs[1])
+
+
+def test_use_fastest_keeps_the_faster_path_and_its_numbers():
+    """DecodePlan.use_fastest times the engine (two launches of 4 tokens) against the tcgen05
+    prefill chain on the plan's buffers and keeps the faster; the kept path gives exactly its own
+    numbers, the two paths agree within the fp16 tolerance, and the input buffer is restored."""
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(61)
+    plan = llama_decode_plan("llama2-7b", bpw=2.0, batch=8, blocks=1, generator=g, keep_words=True)
+    x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
+    ref_e = _run(plan.use_engine(), x)
+    ref_p = _run(plan.use_prefill(), x)
+    ok, err = _close(ref_e, ref_p)
+    assert ok, err
+    plan.buffers[plan.input_buffer].copy_(x)
+    plan.use_fastest(steps=2)
+    assert set(plan.choice_ms) == {"engine", "prefill"} and plan.choice in plan.choice_ms
+    assert torch.equal(plan.buffers[plan.input_buffer], x)
+    assert torch.equal(_run(plan, x), ref_e if plan.choice == "engine" else ref_p)

@@ -40,6 +40,44 @@ sys.path.insert(0, str(ROOT))
 METRIC = "DBF layer µs & HBM GB/s (Llama2-7B shapes, bs=1); speedup vs fp16 cuBLAS GEMV"
 WORKLOAD = "llama2-7b linears, DBF 2.0 bpw, decode bs=1 (224 layers/step)"
 
+# Llama-2 linear shapes (n = out_features, m = in_features), kept here so that the reference arm
+# never imports the product package (it must not load libdbf_b200.so)
+LLAMA = {"llama2-7b": (4096, 11008, 4096, 32), "llama2-13b": (5120, 13824, 5120, 40),
+         "llama2-70b": (8192, 28672, 1024, 80)}
+
+
+def block_shapes(model: str) -> list[tuple[str, int, int]]:
+    h, i, kv, _ = LLAMA[model]
+    return [("q", h, h), ("k", kv, h), ("v", kv, h), ("o", h, h), ("gate", i, h), ("up", i, h), ("down", h, i)]
+
+
+def middle_dim(n: int, m: int, bits: float, granularity: int = 32) -> int:
+    """/root/reference/pkg/src/dbf/budget.py:113-132"""
+    return max(int(bits * n * m / (n + m) // granularity) * granularity, granularity)
+
+
+def layer_bytes(n: int, k: int, m: int, batch: int = 1, scale_bytes: int = 2, act_bytes: int = 2) -> int:
+    """Algorithmic HBM bytes of one decode forward: packed signs of A and B, the
+    three scale vectors, the input and output activations."""
+    return n * ((k + 7) // 8) + k * ((m + 7) // 8) + scale_bytes * (n + k + m) + act_bytes * batch * (m + n)
+
+
+def step_layers(model: str, bpw: float) -> list[tuple[str, int, int, int]]:
+    """(name, n, k, m) of every linear of one decode step of `model`, in dataflow order."""
+    blocks = LLAMA[model][3]
+    return [(nm, n, middle_dim(n, m, bpw), m) for _ in range(blocks) for nm, n, m in block_shapes(model)]
+
+
+def base_config(args, world: int) -> dict:
+    """The workload as BOTH arms report it (same dict, so the driver can pair the lines)."""
+    layers = step_layers(args.model, args.bpw)
+    return {"workload": WORKLOAD if (args.model, args.bpw, args.batch) == ("llama2-7b", 2.0, 1) else
+            f"{args.model} linears, DBF {args.bpw} bpw, decode bs={args.batch} ({len(layers)} layers/step)",
+            "model": args.model, "bpw": args.bpw, "global_batch": args.batch * world, "seq_len": 1,
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU", "layers_per_step": len(layers),
+            "bytes_per_step": sum(layer_bytes(n, k, m, args.batch) for _, n, k, m in layers),
+            "l2": "working set > 2x126 MB L2 per step; no flush"}
+
 
 # ---------------------------------------------------------------------------------------------
 def parse():
@@ -133,7 +171,6 @@ class CpuReference:
 
     def __init__(self, model: str, bpw: float, procs: int | None = None):
         from oracle import dbf_oracle as npo
-        from paper_2505_11076_b200.plan import block_shapes
 
         rng = np.random.default_rng(0)
         shapes = block_shapes(model)
@@ -170,9 +207,11 @@ class CpuReference:
 
 
 def cpu_desc(model, bpw, procs):
-    return (f"one {model} decoder block (7 layers: q,k,v,o 4096x4096 k=4096; gate,up 11008x4096 k=5952; "
-            f"down 4096x11008 k=5952 at {bpw} bpw), bs=1, dbf.forward algorithm (oracle restatement, "
-            f"bit-identical to the reference), rows split over {procs} processes")
+    shapes = ", ".join(f"{nm} {n}x{m} k={middle_dim(n, m, bpw)}" for nm, n, m in block_shapes(model))
+    return (f"bounded sample: one {model} decoder block per step (7 of the step's layers: {shapes}; "
+            f"{bpw} bpw), bs=1, GB/s = that block's algorithmic bytes / its time; dbf.forward algorithm "
+            f"(oracle restatement, bit-identical to the reference on its golden vectors), rows split over "
+            f"{procs} processes")
 
 
 # ---------------------------------------------------------------------------------------------
@@ -201,11 +240,10 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (uniform signs, U(0.5,1.5)-scaled vectors, N(0,1) input)",
-        "config": {"workload": WORKLOAD, "model": args.model, "bpw": args.bpw, "global_batch": 1,
-                   "step": "one decoder block (7 of the 224 layers) per step, bounded CPU sample",
-                   "us_per_layer": t * 1e6 / len(ref.order)},
+        "config": base_config(args, args.gpus),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": ref.procs, "kind": "port",
-                         "sample": cpu_desc(args.model, args.bpw, ref.procs)},
+                         "sample": cpu_desc(args.model, args.bpw, ref.procs),
+                         "us_per_layer": t * 1e6 / len(ref.order)},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -276,8 +314,7 @@ def layer_bench(model: str, bpw: float, steps: int, warmup: int):
     import torch
 
     import paper_2505_11076_b200 as P
-    from paper_2505_11076_b200.budget import middle_dim
-    from paper_2505_11076_b200.plan import DecodePlan, PlanOp, block_shapes
+    from paper_2505_11076_b200.plan import DecodePlan, PlanOp
 
     rows = []
     seen = set()
@@ -326,8 +363,6 @@ def prefill_bench(model: str, bpw: float, tokens: int, steps: int, warmup: int):
     import torch
 
     import paper_2505_11076_b200 as P
-    from paper_2505_11076_b200.budget import middle_dim
-    from paper_2505_11076_b200.plan import block_shapes
 
     g = torch.Generator(device="cuda")
     g.manual_seed(77)
@@ -528,6 +563,8 @@ def main():
     plan.capture()
     bytes_step = plan.bytes_per_step()
     launches = plan.kernel_launches_per_step()
+    cfg = base_config(args, world)
+    assert cfg["bytes_per_step"] == bytes_step, (cfg["bytes_per_step"], bytes_step)
 
     clocks = ClockSampler(local).start()
     ms = time_graph(plan._graph, args.steps, max(args.warmup, 3), barrier)
@@ -597,10 +634,11 @@ def main():
     prefill = None
     if rank == 0 and not args.no_prefill:
         prefill = prefill_bench(args.model, 1.0, 2048, max(args.steps // 2, 5), 3)
-        _, bf16_peak = tensor_peaks()
+        bf16_peak, _ = tensor_peaks()
         prefill["roofline"] = {"bound": "tensor", "achieved": prefill["tflops"], "peak": bf16_peak,
                                "unit": "TFLOP/s", "frac": prefill["tflops"] / bf16_peak,
-                               "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense fp16 = bf16 rate)"}
+                               "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: every layer is timed alone; "
+                                              "dense fp16 = bf16 rate)"}
 
     layers = None
     if rank == 0 and not args.no_layers:
@@ -644,12 +682,9 @@ def main():
             "vs_baseline": None,
             "dtype": "int8-tc (exact i32 per 256-col chunk) / fp16 io",
             "data": "synthetic random-init DBF factors of Llama-2-7B shapes (uniform signs, fp16 scales)",
-            "config": {
-                "workload": WORKLOAD, "model": args.model, "bpw": args.bpw, "global_batch": args.batch * world,
-                "seq_len": 1, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                "layers_per_step": len(plan.ops), "us_per_layer": ms * 1e3 / len(plan.ops),
-                "tokens_per_s_linears_only": 1e3 / ms * world,
-                "bytes_per_step": bytes_step, "l2": "working set 1.63 GB/step > 2x126 MB L2; no flush",
+            "config": cfg,
+            "detail": {
+                "us_per_layer": ms * 1e3 / len(plan.ops), "tokens_per_s_linears_only": 1e3 / ms * world,
                 "cublas_fp16": cublas,
                 "path": "layer kernels (2 GEMV launches per layer)" if args.layer_kernels else
                         "decode engine: 1 persistent kernel per step (bulk-copy sign ring + int8 mma.sync + fp16 LL handoff)",

@@ -278,8 +278,13 @@ typedef struct {
 typedef struct {
   const dbf_engine_run* runs;         /* device array of run records, per CTA in order         */
   const int32_t* cta_offsets;         /* device array, grid + 1 entries (indices into runs)     */
-  uint32_t* run_counter;              /* device uint32[2], zeroed once: [0] launches so far (the
-                                         last CTA of a launch advances it), [1] CTAs done      */
+  uint32_t* run_counter;              /* device uint32[4], zeroed once: [0] epoch base =
+                                         (launches * nvectors) mod 65535 (the last CTA of a
+                                         launch advances it; nvectors % 65535 != 0), [1] CTAs
+                                         done, [2] sticky status bits: 1 = an input chunk held
+                                         inf/NaN (the outputs it feeds are NaN), 2 = a value
+                                         published in fp16 overflowed (|v| > 65504); the host
+                                         reads and clears them, [3] reserved                    */
   int64_t* trace;                     /* optional: 4 x int64 %globaltimer stamps per run / NULL */
   int32_t nvectors;
   int32_t grid;                       /* CTAs (<= number of SMs; one per SM)                    */
@@ -379,15 +384,6 @@ int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_
                         int64_t k, int64_t m, const void* X, int64_t tokens, int64_t ldx, void* Y,
                         int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
 
-/* The same forward as ONE persistent kernel (GEMM1 and GEMM2 tiles scheduled dynamically over the
- * SMs, GEMM2 tiles of a token block start as soon as that block's t is published).  Workspace:
- * dbf_prefill_fused_workspace_bytes (t + scheduling counters, 256-byte aligned); X, Y need 16-byte
- * aligned rows.  Same numerics as dbf_forward_prefill. */
-size_t dbf_prefill_fused_workspace_bytes(int64_t k, int64_t tokens);
-int dbf_forward_prefill_fused(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired,
-                              int64_t B_pitch, const void* a, const void* mid, const void* b, int64_t n,
-                              int64_t k, int64_t m, const void* X, int64_t tokens, int64_t ldx, void* Y,
-                              int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

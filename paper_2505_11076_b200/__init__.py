@@ -6,7 +6,7 @@ Everything computes on an sm_100a GPU through the C ABI in ``include/dbf_b200.h`
 calls fail without a CUDA device -- there is no CPU fallback.
 """
 
-from ._lib import DbfNativeError
+from ._lib import DbfNativeError, DbfOverflowError
 from .bitcore import (
     DbfFormatError,
     DbfLayer,
@@ -48,6 +48,7 @@ __all__ = [
     "DbfFormatError",
     "DbfLayer",
     "DbfNativeError",
+    "DbfOverflowError",
     "DeviceLayer",
     "DeviceSignMatrix",
     "SignMatrix",

@@ -74,11 +74,6 @@ SIGNATURES: dict[str, tuple] = {
     "dbf_pair_signs": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "dbf_prefill_debug_trace": (_int, [_vp, _int]),
     "dbf_prefill_ld": (_i64, [_i64]),
-    "dbf_prefill_fused_workspace_bytes": (_sz, [_i64, _i64]),
-    "dbf_forward_prefill_fused": (
-        _int,
-        [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _vp],
-    ),
     "dbf_prefill_workspace_bytes": (_sz, [_i64, _i64]),
     "dbf_prefill_workspace_bytes_nkm": (_sz, [_i64, _i64, _i64, _i64]),
     "dbf_sign_gemm": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
@@ -87,6 +82,10 @@ SIGNATURES: dict[str, tuple] = {
         [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _vp],
     ),
 }
+
+
+class DbfOverflowError(FloatingPointError):
+    """The decode engine saw a non-finite input or overflowed fp16 (EngineProgram.check)."""
 
 
 class DbfNativeError(RuntimeError):

@@ -1,5 +1,6 @@
 // Shared helpers for the DBF B200 kernels (sm_100a).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
@@ -20,6 +21,21 @@ void set_cuda_error(cudaError_t e);
 inline int check_launch() {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  return DBF_OK;
+}
+
+// Opt a kernel into `bytes` of dynamic shared memory once per DEVICE (the attribute is per device
+// context: a process driving two GPUs must set it on each); lock-free, idempotent if raced.
+template <auto Kern> inline int ensure_smem_attr(int bytes) {
+  static std::atomic<uint64_t> done{0};  // one per kernel (the template argument is the kernel itself)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return DBF_OK;
+  e = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  done.fetch_or(bit, std::memory_order_acq_rel);
   return DBF_OK;
 }
 

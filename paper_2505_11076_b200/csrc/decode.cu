@@ -22,6 +22,7 @@ namespace dbf {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
+constexpr int kBadF = -(1 << 20);  // exponent marking a row that held inf / NaN
 constexpr int kQuantBits = 22;  // |X| <= 2^22; X * 2^7 fits 4 balanced int8 digits with room
 
 struct GemvParams {
@@ -122,10 +123,12 @@ __device__ void quantize_row(const GemvParams& p, int slot, int nkb, int lpk, ui
   const void* xr = (const char*)p.x + (int64_t)slot * p.ldx * (int64_t)(p.x_dtype == DBF_F64 ? 8 : (p.x_dtype == DBF_F32 ? 4 : 2));
   // pass 1: max |x * iscale|
   AT mx = 0;
+  int nonfinite = 0;
   for (int j = tid; j < p.cols; j += kThreads) {
     AT u = (AT)load_any(xr, p.x_dtype, j);
     if (p.iscale) u *= (AT)load_any(p.iscale, p.scale_dtype, j);
     mx = fmax(mx, fabs(u));
+    nonfinite |= !isfinite((double)u);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -134,12 +137,19 @@ __device__ void quantize_row(const GemvParams& p, int slot, int nkb, int lpk, ui
   if (tid == 0) {
     AT m = 0;
     for (int w = 0; w < kWarps; ++w) m = fmax(m, red_max[w]);
+    // an inf max: F = kBadF (zero digits, NaN outputs); a NaN is caught by the vote below
     int F = (m > 0) ? kQuantBits - frexp_exp((double)m) : 0;
+    if (!isfinite((double)m)) F = kBadF;
     *sF = F;
   }
   __syncthreads();
+  // any NaN in the row (fmax drops NaN operands, so the max alone cannot see it)
+  if (__syncthreads_or(nonfinite)) {
+    if (tid == 0) *sF = kBadF;
+  }
+  __syncthreads();
   const int F = *sF;
-  const AT scale = (AT)pow2(F);
+  const AT scale = F == kBadF ? (AT)0 : (AT)pow2(F);
   // pass 2: groups of 4 consecutive columns -> 4 digit planes of 4 bytes each
   const int pair = slot >> 1, bsub = slot & 1;
   const int ngroups = nkb * 8;
@@ -307,7 +317,8 @@ __global__ void __launch_bounds__(kThreads) gemv_i8_kernel(GemvParams p, const u
 #pragma unroll
         for (int w2 = 0; w2 < kWarps; ++w2) s128 += red[(w2 * 16 + row) * 2 * NP + slot];
         const long long P = 2 * (s128 >> 7) - sT[slot];
-        double v = (double)P * pow2(-sF[slot]);
+        // a row with a non-finite input (F = kBadF, zero digits) gives NaN, never a finite value
+        double v = sF[slot] == kBadF ? __longlong_as_double(0x7FF8000000000000ll) : (double)P * pow2(-sF[slot]);
         if (p.oscale) v *= load_any(p.oscale, p.scale_dtype, grow);
         if (p.ar_world) {
           // one-shot all-reduce, push half: this rank's fp32 partial into slot `ar_rank` of every
@@ -374,13 +385,8 @@ template <int NP, bool SINGLE, bool PRE = false>
 int launch_gemv_t(const GemvParams& p, cudaStream_t s, const uint8_t* gfrag = nullptr, const int* gF = nullptr,
                   const long long* gT = nullptr) {
   const size_t smem = gemv_smem_bytes(NP, SINGLE, p.nchunks);
-  static bool configured = false;  // attribute set once per instantiation (max opt-in smem)
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_i8_kernel<NP, SINGLE, PRE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
-    configured = true;
-  }
+  const int st = ensure_smem_attr<gemv_i8_kernel<NP, SINGLE, PRE>>(227 * 1024);
+  if (st != DBF_OK) return st;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemv_i8_kernel<NP, SINGLE, PRE>, kThreads, smem);
   per_sm = std::max(per_sm, 1);

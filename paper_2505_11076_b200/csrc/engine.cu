@@ -71,6 +71,11 @@ constexpr int kMaxSlots = 16;
 // Per token of a batch (NB tokens share every MMA: B column n = 2*token + digit plane):
 constexpr float kQScale = 4079.f / 4096.f;    // keeps 8 * |X| below the two-digit limit 32640
 constexpr float kQInv = 4096.f / 4079.f;
+// chunk exponent of a chunk holding inf / NaN: 1 / (2^F kQScale) = 2^(127 - F) overflows to inf
+constexpr int kBadF = -128;
+// status bits of a launch (run_counter[2], sticky until the host clears them)
+constexpr uint32_t kStatusNonFinite = 1u;  // an input chunk held inf / NaN (its outputs are NaN)
+constexpr uint32_t kStatusOverflow = 2u;   // a value rounded to fp16 overflowed (|v| > 65504)
 constexpr int kChunkQBytes1 = 8 * 64;         // one quantized chunk: 8 k-blocks x (2 planes x 4 lanes x 8 B)
 constexpr int kQScrFT = 32;                   // scratch bytes per chunk for F, T of up to 4 tokens
 inline int part_floats(int nb) { return kWarps * max_units_of(nb) * 16 * nb; }  // one partial buffer
@@ -159,6 +164,11 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -272,30 +282,60 @@ __device__ __forceinline__ bool load_group(const InSpec& in, int col0, uint32_t 
   return true;
 }
 
+// Experiment builds (DBF_POLL_CANARY = n): before re-reading a whole chunk (1 KB of LL words per
+// warp per poll), wait until n canary words (the last row of units 15, 14, ...) carry the epoch.
+__device__ __forceinline__ void ll_canary(const InSpec& in, int c0, uint32_t epoch) {
+#ifdef DBF_POLL_CANARY
+  if (in.kind != 1) return;
+  const int lane = threadIdx.x & 31;
+  const int row = c0 + 255 - 16 * lane;
+  for (;;) {
+    bool ok = true;
+    if (lane < DBF_POLL_CANARY && row < in.cols) {
+      uint32_t w;
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(w) : "l"((const uint32_t*)in.x + row) : "memory");
+      ok = (w >> 16) == epoch;
+    }
+    if (__all_sync(0xffffffffu, ok)) return;
+    __nanosleep(kPollSleepNs);
+  }
+#endif
+}
+
 // Scale and quantize one chunk (this lane: groups lane and lane + 32) into the warp's
 // B-fragment scratch; see quantize_chunk.  Returns F and T = sum_j X_j.
 __device__ __forceinline__ void emit_digits(float (&u)[2][4], const float (&sc)[2][4], uint8_t* xs, int kb_stride,
                                             int lane, int& F_out, int& T_out) {
+  // max |u| with NaN propagation (max.NaN: a NaN anywhere makes the max NaN; fmaxf would drop it)
   float mx = 0.f;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       u[h][e] *= sc[h][e];
-      mx = fmaxf(mx, fabsf(u[h][e]));
+      mx = fmax_nan(mx, fabsf(u[h][e]));
     }
   }
-  // |u| >= 0: the float bits order like unsigned integers, so one REDUX gives the warp max
+  // |u| >= 0 (or NaN): the float bits order like unsigned integers, inf / NaN >= 0x7F800000
   const uint32_t mxb = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
   int F = 0;
-  if (mxb != 0u) {
-    // mx in [2^(e-1), 2^e) with e = biased exponent - 126 (mx is a normal float: fp16 inputs
-    // times fp16/fp32 scales stay far above 2^-126)  ->  |X| <= 4096 * kQScale <= 4079
-    const int e = (int)(mxb >> 23) - 126;
-    F = 12 - e;
-    F = F > 125 ? 125 : (F < -125 ? -125 : F);
+  float scale;
+  if (mxb >= 0x7F800000u) {
+    // a non-finite input (or an fp16 overflow upstream): the chunk's digits are zero and
+    // F = kBadF makes 1 / (2^F kQScale) = inf, so every output this chunk feeds is NaN instead of
+    // a finite value computed from garbage digits; the launch's status word records it
+    F = kBadF;
+    scale = 0.f;
+  } else {
+    if (mxb != 0u) {
+      // mx in [2^(e-1), 2^e) with e = biased exponent - 126 (mx is a normal float: fp16 inputs
+      // times fp16/fp32 scales stay far above 2^-126)  ->  |X| <= 4096 * kQScale <= 4079
+      const int e = (int)(mxb >> 23) - 126;
+      F = 12 - e;
+      F = F > 125 ? 125 : (F < -125 ? -125 : F);
+    }
+    scale = __int_as_float((F + 127) << 23) * kQScale;
   }
-  const float scale = __int_as_float((F + 127) << 23) * kQScale;
   int ts = 0;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -349,6 +389,7 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
   }
   int npoll = 0;
   if (dbg && lane == 0) dbg[0] = gtimer();
+  ll_canary(in, c0, epoch);
   for (;;) {
     const bool ok0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
     const bool ok1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
@@ -390,6 +431,7 @@ __device__ __forceinline__ void quantize_fetched(const InSpec& in, int c, uint32
   const bool ok0 = ll_group(f.v[0], c0 + 4 * lane, in.cols, epoch, u[0]);
   const bool ok1 = ll_group(f.v[1], c0 + 4 * (lane + 32), in.cols, epoch, u[1]);
   if (!__all_sync(0xffffffffu, ok0 && ok1)) {
+    ll_canary(in, c0, epoch);
     for (;;) {  // not all published when prefetched: poll as usual
       const bool p0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
       const bool p1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
@@ -504,6 +546,45 @@ __device__ __forceinline__ void quantize_chunk_tokens(const InSpec& in, int c, u
     if (dbg && lane == 0) dbg[6] = gtimer();
   } else {
     emit_tokens<NB>(u, sc, xq, 0, batch, lane, F, T);
+  }
+}
+
+// The producer lane: stream each run's packed signs (contiguous in HBM) and its 128-byte record into
+// the shared-memory ring with cp.async.bulk, L2 evict_first.  Every piece of a run completes on the
+// FIRST slot's full barrier (armed once with the run's total bytes), so the compute warps wait on
+// one barrier per run.  It never waits on activations: later layers stream while a stage waits.
+__device__ __forceinline__ void stream_runs(const dbf_engine_run* R, int r0, int r1, uint8_t* ring,
+                                            dbf_engine_run* hdr, uint64_t* full, uint64_t* empty,
+                                            int ring_slots, const volatile int* run_now = nullptr) {
+  const uint64_t pol = evict_first_policy();
+  int slot = 0;
+  uint32_t phase = 0;
+  const void* n_tiled = nullptr;
+  int n_cols = 1, n_units = 0;
+  if (r0 < r1) { n_tiled = R[r0].tiled; n_cols = R[r0].cols; n_units = R[r0].nunits; }
+  for (int i = r0; i < r1; ++i) {
+    const uint8_t* src = (const uint8_t*)n_tiled;
+    const int cols = n_cols, nunits = n_units;
+    if (i + 1 < r1) { n_tiled = R[i + 1].tiled; n_cols = R[i + 1].cols; n_units = R[i + 1].nunits; }
+    const int total = nunits * ((cols + kChunkCols - 1) / kChunkCols) * kChunkBytes;
+    int slot0 = slot;
+    for (int off = 0; off < total; off += kSlotBytes) {
+      const int n = min(kSlotBytes, total - off);
+      mbar_wait(&empty[slot], phase ^ 1u);
+      if (off == 0) {
+        slot0 = slot;
+        mbar_arrive_expect_tx(&full[slot0], total + (int)sizeof(dbf_engine_run));
+        bulk_g2s(&hdr[slot0], R + i, sizeof(dbf_engine_run), &full[slot0], pol);
+      }
+      bulk_g2s(ring + (size_t)slot * kSlotBytes, src + off, n, &full[slot0], pol);
+#ifdef DBF_PACE_NS
+#ifndef DBF_PACE_AHEAD
+#define DBF_PACE_AHEAD 1
+#endif
+      if (!run_now || i - r0 > *run_now + DBF_PACE_AHEAD) __nanosleep(DBF_PACE_NS);
+#endif
+      if (++slot == ring_slots) { slot = 0; phase ^= 1u; }
+    }
   }
 }
 
@@ -704,6 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
   constexpr bool kRunOutSmem = NB != 2;
   struct RunOut { void* out_plain; uint32_t* ll_out; int rows, rb, odt; uint32_t ep_out; };
   RunOut* runout = (RunOut*)(cursor + kWarps);  // [2]
+  volatile int* run_now = (volatile int*)(runout + 2);  // the compute warps' current run (producer pacing)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -717,8 +799,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
 
   const int r0 = prog.cta_offsets[blockIdx.x], r1 = prog.cta_offsets[blockIdx.x + 1];
   if (threadIdx.x == 0) {
-    *ep_base_s = (uint32_t)(((uint64_t)*prog.run_counter * (uint64_t)prog.nvectors) % 65535ull);
+    *ep_base_s = *prog.run_counter;  // (launches * nvectors) mod 65535, advanced below
     if (AR) ep_base_s[1] = *ar.epoch + 1u;  // this call's all-reduce epoch
+    *run_now = 0;
     inkey[0].vec = inkey[1].vec = -1;
     inkey[0].iscale = inkey[1].iscale = nullptr;
   }
@@ -728,34 +811,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
   if (warp >= kProdWarp) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
     // ---------------- producer: stream each run's packed signs (contiguous) into the ring -----
-    if (warp == kProdWarp && lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      int slot = 0;
-      uint32_t phase = 0;
-      const void* n_tiled = nullptr;
-      int n_cols = 1, n_units = 0;
-      if (r0 < r1) { n_tiled = R[r0].tiled; n_cols = R[r0].cols; n_units = R[r0].nunits; }
-      for (int i = r0; i < r1; ++i) {
-        const uint8_t* src = (const uint8_t*)n_tiled;
-        const int cols = n_cols, nunits = n_units;
-        if (i + 1 < r1) { n_tiled = R[i + 1].tiled; n_cols = R[i + 1].cols; n_units = R[i + 1].nunits; }
-        const int total = nunits * ((cols + kChunkCols - 1) / kChunkCols) * kChunkBytes;
-        // every piece of the run completes on the FIRST slot's full barrier (armed once with the
-        // run's total bytes), so the compute warps wait on one barrier instead of one per piece
-        int slot0 = slot;
-        for (int off = 0; off < total; off += kSlotBytes) {
-          const int n = min(kSlotBytes, total - off);
-          mbar_wait(&sm.empty[slot], phase ^ 1u);
-          if (off == 0) {
-            slot0 = slot;
-            mbar_arrive_expect_tx(&sm.full[slot0], total + (int)sizeof(dbf_engine_run));
-            bulk_g2s(&sm.hdr[slot0], R + i, sizeof(dbf_engine_run), &sm.full[slot0], pol);
-          }
-          bulk_g2s(sm.ring + (size_t)slot * kSlotBytes, src + off, n, &sm.full[slot0], pol);
-          if (++slot == ring_slots) { slot = 0; phase ^= 1u; }
-        }
-      }
-    }
+    if (warp == kProdWarp && lane == 0)
+      stream_runs(R, r0, r1, sm.ring, sm.hdr, sm.full, sm.empty, ring_slots, run_now);
     return;
   }
 
@@ -784,6 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
 #else
 #define WT(k) do { } while (0)
 #endif
+    if (warp == 0 && lane == 0) *run_now = j;
     const int2 cur = cursor[warp];
     const int slot0 = cur.x;
     mbar_wait(&sm.full[slot0], ((uint32_t)cur.y >> slot0) & 1u);  // the run's record and ALL its pieces
@@ -929,6 +987,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
           if (reuse) {
             Ft = wq[2 * qs], Tt = wq[2 * qs + 1];
           } else {
+#ifdef DBF_LL_TRACE  // debug build: [4 nruns][nvectors x 2048 publish stamps][nruns x 16 x (start, arrival)]
+            int64_t* llt = prog.trace ? prog.trace + 4 * (size_t)prog.cta_offsets[gridDim.x] +
+                                             (size_t)prog.nvectors * 2048 + ((size_t)i * kWarps + warp) * 2
+                                      : nullptr;
+            if (llt && lane == 0 && c == warp) llt[0] = gtimer();
+#endif
             if (fetched) {
               quantize_fetched(in, c, ep_in, xq, Ft, Tt, nf);
             } else {
@@ -939,6 +1003,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
   #endif
             }
             if (lane == 0) wq[2 * qs] = Ft, wq[2 * qs + 1] = Tt;
+#ifdef DBF_LL_TRACE
+            if (llt && lane == 0 && c == warp) llt[1] = gtimer();
+#endif
             fetched = in.kind == 1 && c + kWarps < nch;
             if (fetched) fetch_issue(in, c + kWarps, lane, nf);
           }
@@ -1040,8 +1107,17 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
           for (int w2 = 0; w2 < kWarps; ++w2) v += part[((w2 * kMaxUnits + fu) * NB + t) * 16 + (lane & 15)];
           v *= osc_row;
           const __half h = __float2half_rn(v);
+          // status: a NaN / inf output (from a non-finite input) or an fp16 overflow of a value
+          // that is published in fp16 (LL handoff or fp16 plain output); rare, so one atomic
           const int64_t ll_stride = (int64_t)((ro.rows + kChunkCols - 1) / kChunkCols) * kChunkCols;
           if (ro.ll_out) st_ll16(ro.ll_out + t * ll_stride + row, h, ro.ep_out);
+#ifdef DBF_LL_TRACE
+          if (prog.trace && ro.ll_out && (lane & 15) == 0 && t == 0) {
+            const dbf_engine_run& H2 = sm.hdr[0];  // unused: out_vec comes from the run record below
+            (void)H2;
+            prog.trace[4 * (size_t)prog.cta_offsets[gridDim.x] + (size_t)R[i].out_vec * 2048 + ro.rb + fu] = gtimer();
+          }
+#endif
           if (ro.out_plain) {
             if (AR) {
               // fused all-reduce, push half: the unrounded fp32 partial into slot ar_rank of every
@@ -1055,6 +1131,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
               ((float*)ro.out_plain)[(int64_t)t * ro.rows + row] = v;  // fp32 output: unrounded
             }
           }
+          // status (after the stores: the publish is on every stage's critical path): a NaN / inf
+          // output (from a non-finite input) or an fp16 overflow of a value published in fp16
+          if (!(fabsf(v) <= 65504.f) &&
+              (!isfinite(v) || ro.ll_out || (ro.out_plain && !AR && ro.odt == DBF_F16)))
+            atomicOr(prog.run_counter + 2, isfinite(v) ? kStatusOverflow : kStatusNonFinite);
         }
       }
     }
@@ -1075,7 +1156,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
   // next launch is stream-ordered after this one): no separate advance kernel per step
   if (warp == 0 && lane == 0 && atomicAdd(prog.run_counter + 1, 1u) == gridDim.x - 1) {
     prog.run_counter[1] = 0u;
-    prog.run_counter[0] += 1u;
+    // the epoch base itself advances by nvectors mod 65535 (nvectors % 65535 != 0, checked at
+    // launch), so consecutive launches never share an epoch for any vector, however many run
+    prog.run_counter[0] = (prog.run_counter[0] + (uint32_t)prog.nvectors) % 65535u;
     if (AR) *ar.epoch += 1u;  // every CTA read it at its start
   }
 }
@@ -1087,11 +1170,12 @@ inline size_t fixed_smem(int nb, int xsc) {
          (size_t)kWarps * 8 + 128;
 }
 constexpr size_t kPerSlot = kSlotBytes + sizeof(dbf_engine_run) + 2 * 8;
+inline size_t fixed_smem_of(int nb, int max_cols) { return fixed_smem(nb, xs_chunks_of(nb, max_cols)); }
 inline int ring_slots(int nb, int max_cols) {
-  return std::min((int)((kMaxSmem - fixed_smem(nb, xs_chunks_of(nb, max_cols))) / kPerSlot), kMaxSlots);
+  return std::min((int)((kMaxSmem - fixed_smem_of(nb, max_cols)) / kPerSlot), kMaxSlots);
 }
 inline size_t smem_bytes(int slots, int nb, int max_cols) {
-  return (size_t)slots * kPerSlot + fixed_smem(nb, xs_chunks_of(nb, max_cols));
+  return (size_t)slots * kPerSlot + fixed_smem_of(nb, max_cols);
 }
 inline int nb_for(int batch) { return batch <= 1 ? 1 : (batch <= 2 ? 2 : 4); }
 
@@ -1223,13 +1307,8 @@ static int engine_launch_nb(const dbf_engine_program* program, cudaStream_t s) {
   int st = dbf_engine_smem_bytes(program->max_cols, NB, &smem);
   if (st != DBF_OK) return st;
   const int slots = engine::ring_slots(NB, program->max_cols);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(engine::engine_kernel<NB, XS, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         engine::kMaxSmem);
-    if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
-    configured = true;
-  }
+  st = ensure_smem_attr<engine::engine_kernel<NB, XS, AR>>(engine::kMaxSmem);
+  if (st != DBF_OK) return st;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(program->grid);
   cfg.blockDim = dim3(engine::kThreads);
@@ -1268,7 +1347,8 @@ static int engine_launch_ar(const dbf_engine_program* program, cudaStream_t s) {
 
 extern "C" int dbf_engine_launch(const dbf_engine_program* program, void* stream) {
   if (!program || !program->runs || !program->cta_offsets || !program->run_counter || program->grid < 1 ||
-      program->max_cols < 1 || program->batch < 1 || program->batch > 4)
+      program->max_cols < 1 || program->batch < 1 || program->batch > 4 || program->nvectors < 1 ||
+      program->nvectors % 65535 == 0)
     return DBF_ERR_INVALID_ARGUMENT;
   if (program->ar_world &&
       (program->ar_world < 0 || program->ar_world > 64 || program->ar_rank < 0 ||

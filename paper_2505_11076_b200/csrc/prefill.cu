@@ -115,9 +115,7 @@ __device__ __forceinline__ void expand_word(uint32_t w, const uint32_t* ks, uint
   for (int q = 0; q < 16; ++q) v[q] = ((nw << (15 - q)) & 0x80008000u) ^ ks[q];
 }
 
-// MC: CTA pairs (cluster 2x1) that share a token tile; each loads half of the activation box and
-// multicasts it to both, so every SM pulls 16 KB instead of 32 KB per K block through TMA.
-template <bool KSCALE, bool MC, int TBN = BN, int NST = STAGES>
+template <bool KSCALE, int TBN = BN, int NST = STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     sign_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const Params p) {
   // tile configuration: the namespace defaults, or the small-token tiles
@@ -141,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bar.full_act[s], 1);
       mbar_init(&bar.full_a[s], kExpWarps);
-      mbar_init(&bar.empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs must be done with the slot
+      mbar_init(&bar.empty[s], 1);
     }
     mbar_init(&bar.acc_full, 1);
     fence_mbar_init();
@@ -159,10 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (MC) cluster_sync();  // the peer's barriers exist before any multicast reaches them
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
-  const uint32_t rank = MC ? cluster_ctarank() : 0u;
   const bool tracing = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
 
   if (warp == 0 || warp == 2 || warp == 3) {
@@ -181,18 +177,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph = ((kb - kb0) / STAGES) & 1;
         mbar_wait(&bar.empty[s], ph ^ 1);
         if (tracing) p.trace[5 * p.num_kb + kb] = clock64();
-        mbar_arrive_expect_tx(&bar.full_act[s], MC ? kActStageBytes : p.act_bytes);
-        if constexpr (MC)
-          tma_load_2d_mc(act + (size_t)s * kActStageBytes + rank * (kActStageBytes / 2), &act_map, kb * BK,
-                         tok0 + (int)rank * (BN / 2), &bar.full_act[s], (uint16_t)0x3, pol);
-        else
-          tma_load_2d(act + (size_t)s * kActStageBytes, &act_map, kb * BK, tok0, &bar.full_act[s], pol);
+        mbar_arrive_expect_tx(&bar.full_act[s], p.act_bytes);
+        tma_load_2d(act + (size_t)s * kActStageBytes, &act_map, kb * BK, tok0, &bar.full_act[s], pol);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      const uint32_t idesc = idesc_f16_f32(UM, MC ? BN : p.n_mma);
+      const uint32_t idesc = idesc_f16_f32(UM, p.n_mma);
       for (int kb = kb0; kb < kb1; ++kb) {
         const int s = (kb - kb0) % STAGES;
         const uint32_t ph = ((kb - kb0) / STAGES) & 1;
@@ -211,8 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_f16_ts(tmem + kAccCol + h * BN, a_base + h * kAColsPerHalf + kk * (UK / 2), bd, idesc,
                        (kb != kb0) || (kk != 0));
         }
-        if constexpr (MC) mma_commit_mc(&bar.empty[s], (uint16_t)0x3);
-        else mma_commit(&bar.empty[s]);
+        mma_commit(&bar.empty[s]);
       }
       mma_commit(&bar.acc_full);
     }
@@ -340,7 +331,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (MC) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -421,12 +411,11 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   if (pitch * 32 < ceil_div(K, BK) * BK) return DBF_ERR_SHAPE;  // a K block would read past the row
   if (T > INT32_MAX || rows > INT32_MAX || K > INT32_MAX) return DBF_ERR_UNSUPPORTED;
   if (kscale && K > kMaxKScale) return DBF_ERR_UNSUPPORTED;
-  static const bool mc = getenv("DBF_PREFILL_MULTICAST") != nullptr;  // measured slower
   // T <= BN: one token tile whose MMA N / activation box cover only the tokens present
-  const bool small = !mc && T <= kSmallBN;
+  const bool small = T <= kSmallBN;
   const int n_mma = T >= BN ? BN : (int)ceil_div(T, 16) * 16;
   CUtensorMap map;
-  int st = make_act_map(&map, act, T, K, ld_act, mc ? BN / 2 : n_mma);
+  int st = make_act_map(&map, act, T, K, ld_act, n_mma);
   if (st != DBF_OK) return st;
   Params p;
   p.words = words;
@@ -447,7 +436,7 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   p.ks_global = kscale && ks_fit > (size_t)kMaxSmemOptin ? 1 : 0;
   if (p.ks_global && ((uintptr_t)kscale & 15) != 0) return DBF_ERR_UNSUPPORTED;
   int splits = 1;
-  if (!mc && T <= BN) {
+  if (T <= BN) {
     int kps = 0;
     const int S = split_count(ceil_div(rows, BM), p.num_kb, &kps);
     if (S > 1 && split_ws && split_ws_bytes >= (size_t)S * T * rows * sizeof(float)) {
@@ -457,12 +446,14 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
     }
   }
   p.trace = nullptr;
-  if (getenv("DBF_PREFILL_TRACE")) {
+#ifdef DBF_PREFILL_TRACE  // diagnostics build only (tools/prefill_trace.py)
+  {
     if (!trace_buf) cudaMalloc(&trace_buf, 8 * 6 * 4096);
     p.trace = trace_buf;
   }
+#endif
   const unsigned gx = (unsigned)ceil_div(rows, BM);
-  dim3 grid(mc ? (gx + 1) / 2 * 2 : gx, (unsigned)ceil_div(T, small ? kSmallBN : BN), (unsigned)splits);
+  dim3 grid(gx, (unsigned)ceil_div(T, small ? kSmallBN : BN), (unsigned)splits);
   const bool ks_smem = kscale != nullptr && !p.ks_global;
   // the small configuration pads its shared memory so that one CTA per SM owns all of TMEM
   const size_t smem = small ? std::max<size_t>(smem_bytes_for<kSmallBN, kSmallStages>(p.num_kb, ks_smem), 120 * 1024)
@@ -477,7 +468,7 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = mc ? 2 : 1;
+    attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -485,11 +476,10 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
     return cudaLaunchKernelEx(&cfg, kern, map, p);
   };
   cudaError_t e;
-  if (mc) e = kscale ? go(sign_gemm_kernel<true, true>) : go(sign_gemm_kernel<false, true>);
-  else if (small)
-    e = kscale ? go(sign_gemm_kernel<true, false, kSmallBN, kSmallStages>)
-               : go(sign_gemm_kernel<false, false, kSmallBN, kSmallStages>);
-  else e = kscale ? go(sign_gemm_kernel<true, false>) : go(sign_gemm_kernel<false, false>);
+  if (small)
+    e = kscale ? go(sign_gemm_kernel<true, kSmallBN, kSmallStages>)
+               : go(sign_gemm_kernel<false, kSmallBN, kSmallStages>);
+  else e = kscale ? go(sign_gemm_kernel<true>) : go(sign_gemm_kernel<false>);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   st = check_launch();
   if (st != DBF_OK || splits == 1) return st;

@@ -23,6 +23,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
+from ._lib import DbfOverflowError
 
 SEG_DTYPE = np.dtype(
     {
@@ -260,7 +261,8 @@ class EngineProgram:
             vec_arr[j] = (ptr, ln, kind, dt, 0)
 
         self.max_cols = max(sg[2] for sg in segs)
-        self.run_counter = torch.zeros(2, dtype=torch.int32, device=dev)  # [launches, CTAs done]
+        # [epoch base, CTAs done, status bits, reserved] (dbf_engine_program.run_counter)
+        self.run_counter = torch.zeros(4, dtype=torch.int32, device=dev)
         self.ready = torch.zeros(len(vecs), dtype=torch.int32, device=dev)
         records = np.zeros(len(flat) * 128, dtype=np.uint8)
         _lib.check(
@@ -276,6 +278,7 @@ class EngineProgram:
             self._keep.append(t)
             return t.data_ptr()
 
+        self.records = records  # host copy of the run records (diagnostics)
         self.nruns = len(flat)
         self.units_per_cta = np.array([len(x) for x in per_cta])
         self.nstages = len(stage_units)
@@ -343,6 +346,32 @@ class EngineProgram:
     def kernel_launches_per_step(self) -> int:
         return 1  # the engine kernel (its last CTA advances the launch counter)
 
+    def status(self, clear: bool = True) -> int:
+        """Sticky status bits of the launches since the last clear (reads device memory: syncs):
+        STATUS_NONFINITE = an input chunk held inf/NaN (the outputs it fed are NaN),
+        STATUS_OVERFLOW = a value published in fp16 overflowed (|v| > 65504)."""
+        bits = int(self.run_counter[2].item())
+        if clear and bits:
+            self.run_counter[2].zero_()
+        return bits
+
+    def check(self):
+        """Raise DbfOverflowError if any launch since the last check saw a non-finite input or
+        an fp16 overflow (the engine never turns those into finite garbage: the outputs are NaN /
+        inf, and this reports them)."""
+        bits = self.status()
+        if bits:
+            what = []
+            if bits & STATUS_NONFINITE:
+                what.append("a non-finite (inf/NaN) input reached the engine; the outputs it feeds are NaN")
+            if bits & STATUS_OVERFLOW:
+                what.append("a value published in fp16 overflowed (|v| > 65504)")
+            raise DbfOverflowError("; ".join(what))
+
+
+STATUS_NONFINITE = 1
+STATUS_OVERFLOW = 2
+
 
 class EngineGroups:
     """Batches above 4 tokens: one EngineProgram per group of <= 4 token rows, launched back to
@@ -362,4 +391,8 @@ class EngineGroups:
         for g in self.groups:
             g.enable_trace()
         return self
+
+    def check(self):
+        for g in self.groups:
+            g.check()
 

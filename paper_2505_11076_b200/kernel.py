@@ -13,7 +13,6 @@ relative, well inside the reference's own 1e-5 / 1e-4 tolerances (test_kernel.py
 
 from __future__ import annotations
 
-import os
 import time
 import weakref
 from dataclasses import dataclass
@@ -79,10 +78,6 @@ def as_device_signs(s) -> DeviceSignMatrix:
 # device fast path
 # ---------------------------------------------------------------------------------------------
 PREFILL_MIN_TOKENS = 64
-# two launches (dbf_forward_prefill) by default: over the 7 Llama-2-7B shapes at T = 2048 they
-# sustain 870 TFLOP/s against 781 for the one-kernel persistent variant
-# (dbf_forward_prefill_fused), which DBF_PREFILL_FUSED=1 selects
-PREFILL_FUSED = bool(os.environ.get("DBF_PREFILL_FUSED"))
 
 
 def _prefill_eligible(X2, layer: DeviceLayer, out_dtype) -> bool:
@@ -120,12 +115,9 @@ def forward_prefill(X, layer: DeviceLayer, out=None):
         X = Xp[:, :m]
     Y = out if out is not None else torch.empty((T, layer.n), dtype=torch.float16, device=X.device)
     A, B = layer.A.paired, layer.B.paired
-    fused = PREFILL_FUSED and Y.stride(0) % 8 == 0 and Y.data_ptr() % 16 == 0
-    name = "dbf_forward_prefill_fused" if fused else "dbf_forward_prefill"
-    if fused:
-        ws_bytes = _lib.lib.dbf_prefill_fused_workspace_bytes(layer.k, T)
-    else:  # room for the split-K partials of small token counts
-        ws_bytes = _lib.lib.dbf_prefill_workspace_bytes_nkm(layer.n, layer.k, layer.m_dim, T)
+    name = "dbf_forward_prefill"
+    # room for the split-K partials of small token counts
+    ws_bytes = _lib.lib.dbf_prefill_workspace_bytes_nkm(layer.n, layer.k, layer.m_dim, T)
     ws = _workspace(ws_bytes, X.device)
     _lib.check(
         getattr(_lib.lib, name)(
@@ -318,7 +310,3 @@ def random_device_layer(n: int, k: int, m: int, generator=None, scale_dtype=None
     A = DeviceSignMatrix.random(n, k, generator=generator, device=device, keep_words=keep_words)
     B = DeviceSignMatrix.random(k, m, generator=generator, device=device, keep_words=keep_words)
     return DeviceLayer(u(n, k**0.5), A, u(k, 1.0), B, u(m, m**0.5))
-
-
-def _now_us() -> float:  # pragma: no cover - helper for callers timing host paths
-    return time.perf_counter() * 1e6

@@ -179,7 +179,40 @@ class DecodePlan:
             inp.copy_(x.reshape(inp.shape))
         self.replay()
         out = self.buffers[self.output_buffer]
-        return out.cpu() if host else out
+        if not host:
+            return out
+        # the engine's sticky status word (non-finite input / fp16 overflow) rides along with the
+        # output copy: queued before it, valid once the output copy has synchronized
+        st = self._status_words()
+        res = out.cpu()
+        if st is not None:
+            self._raise_status(st)
+        return res
+
+    def _status_words(self):
+        """Queue a copy of every engine program's status word into pinned host memory."""
+        import torch
+
+        progs = getattr(self.engine, "groups", [self.engine]) if self.engine is not None else []
+        progs = [p for p in progs if hasattr(p, "run_counter")]
+        if not progs:
+            return None
+        if getattr(self, "_status_host", None) is None or self._status_host.numel() != len(progs):
+            self._status_host = torch.zeros(len(progs), dtype=torch.int32).pin_memory()
+        for i, p in enumerate(progs):
+            self._status_host[i:i + 1].copy_(p.run_counter[2:3], non_blocking=True)
+        return progs
+
+    def _raise_status(self, progs):
+        if int(self._status_host.max()) != 0:
+            for p in progs:
+                p.check()
+
+    def check(self):
+        """Raise engine.DbfOverflowError if a step since the last check saw a non-finite input or
+        overflowed fp16 (device calls: replay()/_eager() do not synchronize to look)."""
+        if self.engine is not None:
+            self.engine.check()
 
 
 def llama_decode_plan(model: str = "llama2-7b", bpw: float = 2.0, batch: int = 1, blocks: int | None = None,

@@ -44,3 +44,16 @@ def rel_norm(out, ref):
 
 def rel_max(out, ref):
     return float(np.max(np.abs(np.asarray(out) - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def random_layer(rng, n, k, m, positive=False):
+    """pkg/tests/conftest.py:17-24 (GPU pack)"""
+    from paper_2505_11076_b200 import DbfLayer, pack
+
+    return DbfLayer(
+        a=f32_vector(rng, n, positive),
+        A=pack(random_signs(rng, n, k)),
+        mid=f32_vector(rng, k, positive),
+        B=pack(random_signs(rng, k, m)),
+        b=f32_vector(rng, m, positive),
+    )

@@ -120,32 +120,6 @@ def test_pair_layout_round_trip(rng):
             assert np.array_equal(hi, (words[:, j] >> (2 * q + 1)) & 1)
 
 
-@pytest.mark.parametrize("T,n,k,m", [(256, 384, 320, 512), (300, 200, 96, 136), (2048, 4096, 2048, 4096)])
-def test_fused_prefill_equals_two_launch_path(T, n, k, m):
-    """dbf_forward_prefill_fused (one persistent kernel, dynamic tile schedule, dependency
-    counters) computes the same tiles in the same order as dbf_forward_prefill: bitwise equal."""
-    g = torch.Generator(device="cuda")
-    g.manual_seed(T + n)
-    dl = P.random_device_layer(n, k, m, generator=g, keep_words=True)
-    X = torch.randn((T, m), generator=g, device="cuda").half()
-    A, B = dl.A.paired, dl.B.paired
-    ref = torch.empty((T, n), dtype=torch.half, device="cuda")
-    ws2 = torch.empty(_lib.lib.dbf_prefill_workspace_bytes(k, T), dtype=torch.uint8, device="cuda")
-    _lib.check(_lib.lib.dbf_forward_prefill(
-        A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], dl.a.data_ptr(), dl.mid.data_ptr(),
-        dl.b.data_ptr(), n, k, m, X.data_ptr(), T, m, ref.data_ptr(), n, ws2.data_ptr(), ws2.numel(),
-        _lib.stream_ptr()), "two-launch")
-    Y = torch.empty_like(ref)
-    ws = torch.empty(_lib.lib.dbf_prefill_fused_workspace_bytes(k, T), dtype=torch.uint8, device="cuda")
-    for _ in range(2):  # the per-call counter reset makes repeated calls independent
-        _lib.check(_lib.lib.dbf_forward_prefill_fused(
-            A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], dl.a.data_ptr(), dl.mid.data_ptr(),
-            dl.b.data_ptr(), n, k, m, X.data_ptr(), T, m, Y.data_ptr(), n, ws.data_ptr(), ws.numel(),
-            _lib.stream_ptr()), "fused")
-        torch.cuda.synchronize()
-        assert torch.equal(Y, ref)
-
-
 def test_small_batch_split_k_is_deterministic():
     """T = 64 at the Llama-2-13B MLP shape (1.5 bpw): the split-K partials are summed in split
     order, so two runs are bitwise identical; a workspace too small for the partials runs the

@@ -320,7 +320,12 @@ __global__ void __launch_bounds__(kThreads) gemv_i8_kernel(GemvParams p, const u
         // a row with a non-finite input (F = kBadF, zero digits) gives NaN, never a finite value
         double v = sF[slot] == kBadF ? __longlong_as_double(0x7FF8000000000000ll) : (double)P * pow2(-sF[slot]);
         if (p.oscale) v *= load_any(p.oscale, p.scale_dtype, grow);
-        if (p.ar_world) {
+        if (p.ar_world == 1) {
+          // world 1: nothing to exchange -- the combine's formula applied in place (same bits as
+          // the push / flag / combine path, without its system-scope fence and flag round trip)
+          store_any(p.ar_y, p.ar_ydt, (int64_t)(p.ar_row0 + slot) * p.ar_ldy + grow,
+                    (double)(float)v * load_any(p.ar_a, p.scale_dtype, grow));
+        } else if (p.ar_world) {
           // one-shot all-reduce, push half: this rank's fp32 partial into slot `ar_rank` of every
           // peer's receive buffer (NVLink P2P stores through the peers' mapped addresses)
           const float fv = (float)v;
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(kThreads) gemv_i8_kernel(GemvParams p, const u
     }
     __syncthreads();
   }
-  if (!p.ar_world) return;
+  if (p.ar_world <= 1) return;
   // this CTA's row blocks are out: ONE system-scope fence, then release them to every peer
   // (flag = epoch, monotonic); a fence per row block cost more than the GEMV itself
   if (threadIdx.x == 0) {

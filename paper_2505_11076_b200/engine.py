@@ -187,7 +187,10 @@ class EngineProgram:
 
         lv = levels_of(plan.ops, plan.input_buffer)
         last_writer = {}
+        consumed = [False] * len(plan.ops)  # is op i's output read by a later op?
         for i, op in enumerate(plan.ops):
+            if op.src in last_writer:
+                consumed[last_writer[op.src]] = True
             last_writer[op.dst] = i
         final_op = last_writer.get(plan.output_buffer)
 
@@ -204,11 +207,15 @@ class EngineProgram:
                 latest[op.src] = len(vecs) - 1
             src_vec = latest[op.src]
             t_vec = ll_vector(layer.k)
-            y_vec = ll_vector(layer.n)
+            # outputs read by a later op are published as LL words; the final output and outputs
+            # nobody reads in the plan (e.g. q, k of the benchmark's block, whose consumer --
+            # attention -- is outside this path) are plain stores into the destination buffer
+            y_vec = ll_vector(layer.n) if consumed[i] else -1
+            plain = i == final_op or not consumed[i]
             segs.append((layer.B.tiled.data_ptr(), layer.k, layer.m_dim, src_vec, t_vec, layer.b.data_ptr(),
                          layer.mid.data_ptr(), sd, _lib.F32, 0))
-            out_plain = plan.buffers[op.dst].data_ptr() if i == final_op else 0
-            out_code = _lib.dtype_code(plan.buffers[op.dst].dtype) if i == final_op else act_code
+            out_plain = plan.buffers[op.dst].data_ptr() if plain else 0
+            out_code = _lib.dtype_code(plan.buffers[op.dst].dtype) if plain else act_code
             if out_code not in (_lib.F16, _lib.F32):
                 raise ValueError("engine outputs must be float16 or float32")
             # layer.a None: no output scale (a k-shard's partial; the scale follows the all-reduce)

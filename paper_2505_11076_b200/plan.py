@@ -215,10 +215,40 @@ class DecodePlan:
             self.engine.check()
 
 
+def layerwise_ks(model: str = "llama2-13b", target_bpw: float = 1.5, floor_bpw: float = 1.0, cap_bpw: float = 2.3,
+                 blocks: int | None = None, seed: int = 0) -> list[int]:
+    """Non-uniform per-layer middle dimensions (BASELINE configs[4]: 1.0-2.3 bits/weight across the
+    layers of a model) from the reference's greedy allocation (budget.allocate_middle_dims,
+    /root/reference/pkg/src/dbf/budget.py:187-261) at a global target, with every layer's source k
+    at cap_bpw and its floor at floor_bpw.  The channel scores are synthetic (no calibration data
+    here): per layer an exponentially decaying spectrum whose decay rate and scale vary by layer
+    type and depth (seeded, deterministic).  Returns k per linear in plan order."""
+    import numpy as np
+
+    from .budget import allocate_middle_dims
+
+    s = LLAMA_SHAPES[model]
+    nblocks = blocks if blocks is not None else s["blocks"]
+    rng = np.random.default_rng(seed)
+    layers, scores = [], {}
+    for bi in range(nblocks):
+        for ti, (name, n, m) in enumerate(block_shapes(model)):
+            nm = f"{bi}.{name}"
+            k_src = middle_dim(n, m, cap_bpw, 32)
+            depth = bi / max(nblocks - 1, 1)
+            rate = (2.0 + 6.0 * rng.uniform() + 4.0 * abs(depth - 0.5)) / k_src
+            scale = (1.0 + ti % 3) * (0.5 + depth) * rng.uniform(0.5, 1.5)
+            layers.append((nm, n, m))
+            scores[nm] = scale * np.exp(-rate * np.arange(k_src))
+    ks = allocate_middle_dims(layers, scores, target_bpw, floor_bpw=floor_bpw, granularity=32)
+    return [ks[nm] for nm, _, _ in layers]
+
+
 def llama_decode_plan(model: str = "llama2-7b", bpw: float = 2.0, batch: int = 1, blocks: int | None = None,
                       generator=None, act_dtype=None, scale_dtype=None, device="cuda",
-                      keep_words: bool | None = None) -> DecodePlan:
-    """Synthetic random-init DBF factors of every linear layer of a Llama-2 model (§8d)."""
+                      keep_words: bool | None = None, ks: list[int] | None = None) -> DecodePlan:
+    """Synthetic random-init DBF factors of every linear layer of a Llama-2 model (§8d); ``ks``
+    optionally gives every linear its own middle dimension (plan order, e.g. layerwise_ks)."""
     import torch
 
     act_dtype = act_dtype or torch.float16
@@ -234,9 +264,11 @@ def llama_decode_plan(model: str = "llama2-7b", bpw: float = 2.0, batch: int = 1
     idx = {nm: i for i, nm in enumerate(names)}
     src_of = {"q": "h", "k": "h", "v": "h", "o": "v", "gate": "o", "up": "o", "down": "gate"}
     dst_of = {"q": "q", "k": "k", "v": "v", "o": "o", "gate": "gate", "up": "up", "down": "h"}
-    for _ in range(nblocks):
-        for name, n, m in shapes:
-            k = middle_dim(n, m, bpw, 32)
+    if ks is not None and len(ks) != nblocks * len(shapes):
+        raise ValueError(f"ks has {len(ks)} entries, expected {nblocks * len(shapes)}")
+    for bi in range(nblocks):
+        for li, (name, n, m) in enumerate(shapes):
+            k = middle_dim(n, m, bpw, 32) if ks is None else int(ks[bi * len(shapes) + li])
             layers.append(random_device_layer(n, k, m, generator=generator, scale_dtype=scale_dtype, device=device,
                                               keep_words=batch >= 64 if keep_words is None else keep_words))
             ops.append(PlanOp(len(layers) - 1, idx[src_of[name]], idx[dst_of[name]], name))

@@ -98,8 +98,8 @@ def _ptrs(ts):
 
 @pytest.mark.parametrize("batch", [1, 3, 16])
 def test_fused_allreduce_single_rank_equals_partial_path(batch):
-    """world = 1: the fused kernel's push/flag/combine path gives the same bits as
-    dbf_forward_partial + dbf_finalize_partial, over several epochs (both buffer parities)."""
+    """world = 1: the fused kernel's in-place combine (no push, fence or flags: nothing to exchange)
+    gives the same bits as dbf_forward_partial + dbf_finalize_partial, over several epochs."""
     import torch
 
     from paper_2505_11076_b200 import _lib
@@ -117,7 +117,8 @@ def test_fused_allreduce_single_rank_equals_partial_path(batch):
         torch.cuda.synchronize()
         assert torch.equal(y, ref), epoch
         assert int(counter.item()) == epoch
-        assert int(flags.view(16, 1, -1)[0].min()) == epoch
+        # world 1 takes the in-place combine: no flags are raised (nothing waits on them)
+        assert int(flags.abs().max()) == 0
     out = oracle.c_forward(X.double().cpu().numpy(), layer.a, layer.A.bits, layer.mid, layer.B.bits, layer.b)
     assert rel_max(y.float().cpu().numpy(), out) <= 1e-2
 
@@ -214,9 +215,9 @@ def test_fused_allreduce_symmetric_memory_single_rank():
 
 @pytest.mark.parametrize("batch", [1, 3, 4])
 def test_engine_fused_allreduce_single_rank_equals_engine_partial(batch):
-    """world = 1 through the decode engine: the fused push / flag / combine in the last stage gives
-    the same bits as partial_engine + dbf_finalize_partial, over several calls (both buffer
-    parities); the call counter and this rank's flags advance once per call."""
+    """world = 1 through the decode engine: the fused last stage (in-place combine at world 1) gives
+    the same bits as partial_engine + dbf_finalize_partial, over several calls; the call counter
+    advances once per call."""
     import torch
 
     from paper_2505_11076_b200 import _lib
@@ -235,7 +236,8 @@ def test_engine_fused_allreduce_single_rank_equals_engine_partial(batch):
         torch.cuda.synchronize()
         assert torch.equal(y, ref), epoch
         assert int(counter.item()) == epoch
-        assert int(flags.view(16, 1, -1)[0].min()) == epoch
+        # world 1 takes the in-place combine: no flags are raised (nothing waits on them)
+        assert int(flags.abs().max()) == 0
     # the per-layer fused path shares the counter / flags / buffers: calls of both paths interleave
     y2 = ds.forward_allreduce(X, _ptrs([recv]), _ptrs([flags]), counter)
     y3 = ds.forward_allreduce_engine(X, _ptrs([recv]), _ptrs([flags]), counter)

@@ -24,9 +24,17 @@ nr = eng.nruns
 nv = eng._prog.nvectors
 eng.trace = torch.zeros(4 * nr + nv * 2048 + nr * 16 * 2, dtype=torch.int64, device="cuda")
 eng._prog.trace = eng.trace.data_ptr()
+import ctypes
+
+from paper_2505_11076_b200 import _lib
+
 for _ in range(3):
     plan._eager()
 torch.cuda.synchronize()
+rtt = (ctypes.c_ulonglong * 2)()
+if hasattr(_lib.lib, "dbf_debug_ll_rtt"):
+    _lib.lib.dbf_debug_ll_rtt(rtt)
+    print(f"LL poll round trip (load issue -> all lanes checked): mean {rtt[0] / max(rtt[1], 1):.0f} ns over {rtt[1]} polls")
 t = eng.trace.cpu().numpy().astype(np.int64)
 pub = t[4 * nr: 4 * nr + nv * 2048].reshape(nv, 2048)
 arr = t[4 * nr + nv * 2048:].reshape(nr, 16, 2)

@@ -68,8 +68,22 @@ def step_layers(model: str, bpw: float) -> list[tuple[str, int, int, int]]:
     return [(nm, n, middle_dim(n, m, bpw), m) for _ in range(blocks) for nm, n, m in block_shapes(model)]
 
 
+def sharded_headline(args, world: int) -> bool:
+    return world > 1 or args.sharded_step
+
+
 def base_config(args, world: int) -> dict:
     """The workload as BOTH arms report it (same dict, so the driver can pair the lines)."""
+    if sharded_headline(args, world):
+        layers = step_layers("llama2-70b", 2.0)
+        if args.blocks:
+            layers = layers[: 7 * args.blocks]
+        return {"workload": f"llama2-70b linears k-sharded over {world} GPUs, DBF 2.0 bpw, decode bs=1 "
+                            f"({len(layers)} layers/step)",
+                "model": "llama2-70b", "bpw": 2.0, "global_batch": 1, "seq_len": 1,
+                "parallelism": f"k-shard x{world}", "layers_per_step": len(layers),
+                "bytes_per_step": sum(layer_bytes(n, k, m) for _, n, k, m in layers),
+                "l2": "working set > 2x126 MB L2 per step; no flush"}
     layers = step_layers(args.model, args.bpw)
     return {"workload": WORKLOAD if (args.model, args.bpw, args.batch) == ("llama2-7b", 2.0, 1) else
             f"{args.model} linears, DBF {args.bpw} bpw, decode bs={args.batch} ({len(layers)} layers/step)",
@@ -97,6 +111,9 @@ def parse():
     ap.add_argument("--no-sharded", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--layer-kernels", action="store_true", help="per-layer GEMV kernels instead of the engine")
+    ap.add_argument("--sharded-step", action="store_true",
+                    help="headline the k-sharded Llama-2-70B step (the default when WORLD_SIZE > 1)")
+    ap.add_argument("--blocks", type=int, default=None, help="decoder blocks of the sharded step (default: all)")
     return ap.parse_args()
 
 
@@ -219,7 +236,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # N>1: rank 0 alone runs the CPU reference; others exit 0 without work
-    ref = CpuReference(args.model, args.bpw)
+    model, bpw = ("llama2-70b", 2.0) if sharded_headline(args, args.gpus) else (args.model, args.bpw)
+    ref = CpuReference(model, bpw)
     for _ in range(args.warmup):
         ref.step()
     times = [ref.step() for _ in range(args.steps)]
@@ -242,7 +260,7 @@ def run_reference(args):
         "data": "synthetic (uniform signs, U(0.5,1.5)-scaled vectors, N(0,1) input)",
         "config": base_config(args, args.gpus),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": ref.procs, "kind": "port",
-                         "sample": cpu_desc(args.model, args.bpw, ref.procs),
+                         "sample": cpu_desc(model, bpw, ref.procs),
                          "us_per_layer": t * 1e6 / len(ref.order)},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -305,7 +323,7 @@ def time_graph(g, steps, warmup, barrier=lambda: None):
     return e0.elapsed_time(e1) / steps  # ms per step
 
 
-def layer_bench(model: str, bpw: float, steps: int, warmup: int):
+def layer_bench(model: str, bpw: float, steps: int, warmup: int, shapes=None, layer_kernels: bool = False):
     """The metric at layer level (SURVEY §8d timing method): per distinct Llama-2 linear shape at
     `bpw`, batch 1 -- (1) throughput: N distinct layer instances (total > 2x L2) that all read the
     same input, run as ONE engine program without dependencies between them, µs/layer = time / N;
@@ -318,7 +336,7 @@ def layer_bench(model: str, bpw: float, steps: int, warmup: int):
 
     rows = []
     seen = set()
-    for name, n, m in block_shapes(model):
+    for name, n, m in (shapes or block_shapes(model)):
         if (n, m) in seen:
             continue
         seen.add((n, m))
@@ -344,11 +362,19 @@ def layer_bench(model: str, bpw: float, steps: int, warmup: int):
         gc = graph_of(lambda: [torch.matmul(x, w.t(), out=y) for w, y in zip(ws, ys)])
         ms_c = time_graph(gc, steps, warmup)
         dense = 2 * n * m + 2 * (n + m)
-        rows.append({"layer": name, "n": n, "k": k, "m": m, "bytes": lb, "instances": inst,
-                     "us_per_layer": ms_t * 1e3 / inst, "gbs": lb * inst / (ms_t * 1e-3) / 1e9,
-                     "us_isolated": ms_i * 1e3, "cublas_fp16_us_per_layer": ms_c * 1e3 / inst,
-                     "cublas_fp16_gbs": dense * inst / (ms_c * 1e-3) / 1e9,
-                     "speedup_vs_cublas": ms_c / ms_t})
+        row = {"layer": name, "n": n, "k": k, "m": m, "bytes": lb, "instances": inst,
+               "us_per_layer": ms_t * 1e3 / inst, "gbs": lb * inst / (ms_t * 1e-3) / 1e9,
+               "us_isolated": ms_i * 1e3, "gbs_isolated": lb / (ms_i * 1e-3) / 1e9,
+               "cublas_fp16_us_per_layer": ms_c * 1e3 / inst,
+               "cublas_fp16_gbs": dense * inst / (ms_c * 1e-3) / 1e9,
+               "speedup_vs_cublas": ms_c / ms_t}
+        if layer_kernels:  # the per-layer GEMV kernels (two launches: B then A), same instances
+            gk = graph_of(lambda: [P.forward_device(x, l, out=b) for l, b in zip(layers, bufs[1:])])
+            ms_k = time_graph(gk, steps, warmup)
+            row.update({"us_per_layer_layer_kernels": ms_k * 1e3 / inst,
+                        "gbs_layer_kernels": lb * inst / (ms_k * 1e-3) / 1e9})
+            del gk
+        rows.append(row)
         del tp, iso, gc, ws, ys, layers
         torch.cuda.empty_cache()
     return {"model": model, "bpw": bpw, "batch": 1,
@@ -450,6 +476,32 @@ def sweep_bench(steps: int):
     one("llama2-13b", 1.5, 8, False)
     one("llama2-13b", 1.5, 8, False, prefill=True)
     one("llama2-13b", 1.5, 64, False)
+    # BASELINE configs[4] as specified: a NON-uniform layer-wise k (1.0-2.3 bits/weight across the
+    # 280 linears, 1.5 on average, from the reference's greedy allocation -- plan.layerwise_ks)
+    from paper_2505_11076_b200.plan import layerwise_ks
+
+    ks = layerwise_ks("llama2-13b", target_bpw=1.5, floor_bpw=1.0, cap_bpw=2.3)
+    shp = block_shapes("llama2-13b") * LLAMA["llama2-13b"][3]
+    bpws = [k * (n + m) / (n * m) for k, (_, n, m) in zip(ks, shp)]
+    for batch in (1, 8, 64):
+        g = torch.Generator(device="cuda")
+        g.manual_seed(6)
+        plan = llama_decode_plan("llama2-13b", batch=batch, generator=g, ks=ks, keep_words=batch >= 64)
+        plan.buffers[plan.input_buffer].normal_(generator=g)
+        path = plan.default_path()
+        plan.use_prefill() if path == "prefill" else plan.use_engine()
+        plan.capture()
+        ms = time_graph(plan._graph, steps, 3)
+        b = plan.bytes_per_step()
+        rows.append({"model": "llama2-13b", "bpw": "layerwise", "bpw_min": min(bpws), "bpw_max": max(bpws),
+                     "bpw_mean_sign_bits": sum(k * (n + m) for k, (_, n, m) in zip(ks, shp)) /
+                                           sum(n * m for _, n, m in shp),
+                     "batch": batch, "path": path if batch <= 4 or path == "prefill" else
+                     f"engine, {-(-batch // 4)} launches of <= 4 tokens",
+                     "ms_per_step": ms, "gbs": b / (ms * 1e-3) / 1e9,
+                     "tokens_per_s_linears_only": batch * 1e3 / ms, "layers": len(plan.ops)})
+        del plan
+        torch.cuda.empty_cache()
     return rows
 
 
@@ -530,6 +582,125 @@ def sharded_bench(world: int, rank: int, steps: int, warmup: int, barrier, dist=
             "rows": rows}
 
 
+def sharded_step_bench(world: int, rank: int, steps: int, warmup: int, barrier, dist=None,
+                       blocks: int | None = None):
+    """BASELINE configs[3] as a decode STEP: every linear of Llama-2-70B (2 bpw, batch 1, decoder
+    dataflow of plan.llama_decode_plan) with its middle dimension k sharded over the `world` ranks
+    (word-aligned shards).  Per layer the rank's partial runs through the decode engine
+    with the one-shot all-reduce fused into its last stage (FusedAllReduce: fp32 partial rows pushed
+    into every peer's symmetric-memory buffer over NVLink, y = a * sum in rank order); the NCCL
+    arm is the engine partial + an NCCL all-reduce + finalize.  Both are CUDA graphs of the whole
+    step; times are max over ranks.  value = the whole model's algorithmic bytes / step time (all
+    ranks together stream the model once per step: strong scaling)."""
+    import torch
+
+    import paper_2505_11076_b200 as P
+    from paper_2505_11076_b200 import sharded
+
+    model = "llama2-70b"
+    h, inter, kv, nb = LLAMA[model]
+    nb = blocks or nb
+    src_of = {"q": "h", "k": "h", "v": "h", "o": "q", "gate": "o", "up": "o", "down": "gate"}
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77 + 1000 * rank)
+    layers, total_bytes = [], 0
+    for _ in range(nb):
+        for name, n, m in block_shapes(model):
+            k = middle_dim(n, m, 2.0)
+            k0, k1 = sharded.shard_bounds(k, world)[rank]
+            dl = P.random_device_layer(n, k1 - k0, m, generator=g)
+            layers.append((name, sharded.DeviceShard.from_device_layer(dl, rank, world, k0)))
+            total_bytes += layer_bytes(n, k, m)
+    ars = {n: sharded.FusedAllReduce(n, 1) for n in sorted({sh.shard.n for _, sh in layers})}
+    gx = torch.Generator(device="cuda")
+    gx.manual_seed(5)  # the step input is replicated
+    x = (torch.randn((1, h), generator=gx, device="cuda") * 0.5).half()
+
+    def step(fused: bool):
+        bufs = {"h": x}
+        for name, sh in layers:
+            xin = bufs[src_of[name]]
+            y = ars[sh.shard.n].forward(sh, xin, engine=True) if fused else sh.forward(xin, engine=True)
+            bufs["h" if name == "down" else name] = y
+        return bufs["h"]
+
+    def mx(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    y_f, y_n = step(True), step(False)
+    torch.cuda.synchronize()
+    diff = float(((y_f.float() - y_n.float()).abs().max() / y_n.float().abs().max().clamp_min(1e-30)).item())
+    out = {}
+    gf = graph_of(lambda: out.__setitem__("y", step(True)))
+    ms_f = mx(time_graph(gf, steps, warmup, barrier))
+    ms_n = mx(time_graph(graph_of(lambda: step(False)), steps, warmup, barrier))
+    # end to end: the step input copied in from pinned host memory and the output read back,
+    # inside the timed region
+    host_x = x.cpu().pin_memory()
+    host_y = torch.empty(out["y"].shape, dtype=out["y"].dtype).pin_memory()
+    for _ in range(2):
+        x.copy_(host_x, non_blocking=True)
+        gf.replay()
+        host_y.copy_(out["y"], non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        x.copy_(host_x, non_blocking=True)
+        gf.replay()
+        host_y.copy_(out["y"], non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    ms_e = mx(e0.elapsed_time(e1) / steps)
+    return {"ms_per_step_e2e": ms_e, "gbs_e2e": total_bytes / (ms_e * 1e-3) / 1e9,
+            "h2d_bytes_per_step": host_x.numel() * host_x.element_size(),
+            "d2h_bytes_per_step": host_y.numel() * host_y.element_size(),"model": model, "blocks": nb, "layers": len(layers), "world": world, "bytes_per_step": total_bytes,
+            "ms_per_step_fused": ms_f, "ms_per_step_nccl": ms_n,
+            "gbs_fused": total_bytes / (ms_f * 1e-3) / 1e9, "gbs_nccl": total_bytes / (ms_n * 1e-3) / 1e9,
+            "us_per_layer_fused": ms_f * 1e3 / len(layers), "fused_vs_nccl_max_rel_diff": diff,
+            "launches_per_step": len(layers)}
+
+
+def main_sharded(args, world, rank, local, dist, barrier):
+    """N > 1 (or --sharded-step): the headline is the k-sharded Llama-2-70B decode step."""
+    import torch
+
+    cfg = base_config(args, world)
+    clocks = ClockSampler(local).start()
+    r = sharded_step_bench(world, rank, args.steps, max(args.warmup, 3), barrier, dist, blocks=args.blocks)
+    clk = clocks.stop()
+    assert r["bytes_per_step"] == cfg["bytes_per_step"]
+    peak, peak_src = peaks()
+    ms = r["ms_per_step_fused"]
+    per_rank = r["bytes_per_step"] / world
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": r["gbs_fused"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int8-tc (exact i32 per 256-col chunk) / fp16 io, fp32 all-reduce",
+            "data": "synthetic random-init DBF factors of Llama-2-70B shapes, k-sharded (uniform signs, fp16 scales)",
+            "config": cfg,
+            "detail": {k: v for k, v in r.items() if k != "bytes_per_step"},
+            "roofline": {"bound": "hbm", "achieved": per_rank / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": per_rank / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                         "kernel": "engine_kernel<1,*,AR> (one launch per k-sharded layer, all-reduce fused)",
+                         "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": {"value": r["gbs_e2e"], "unit": "GB/s", "h2d_bytes_per_step": r["h2d_bytes_per_step"],
+                    "d2h_bytes_per_step": r["d2h_bytes_per_step"], "ms_per_step": r["ms_per_step_e2e"]},
+            "gpu_launches": r["launches_per_step"] * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -550,6 +721,9 @@ def main():
     def barrier():
         if dist is not None:
             dist.barrier()
+
+    if sharded_headline(args, world):
+        return main_sharded(args, world, rank, local, dist, barrier)
 
     import paper_2505_11076_b200 as P
     from paper_2505_11076_b200.plan import llama_decode_plan
@@ -641,8 +815,14 @@ def main():
                                               "dense fp16 = bf16 rate)"}
 
     layers = None
+    cfg1 = None
     if rank == 0 and not args.no_layers:
         layers = layer_bench(args.model, args.bpw, max(args.steps // 2, 5), 3)
+        # BASELINE configs[0]: one 4096 x 4096 layer, k = 2048 (~1 bit/weight), batch 1 -- the
+        # decode engine (isolated: one launch per layer; throughput: independent instances), the
+        # per-layer GEMV kernels, cuBLAS fp16 GEMV of the dense layer
+        cfg1 = layer_bench(args.model, 1.0, max(args.steps // 2, 5), 3,
+                           shapes=[("cfg1 4096x4096 k=2048", 4096, 4096)], layer_kernels=True)["rows"][0]
 
     sweep = None
     if rank == 0 and not args.no_sweep:
@@ -698,6 +878,7 @@ def main():
             "e2e": e2e,
             "prefill": prefill,
             "layers": layers,
+            "cfg1": cfg1,
             "sweep": sweep,
             "sharded": shard,
             "gpu_launches": launches * args.steps,

@@ -173,6 +173,7 @@ class EngineProgram:
         # ---- vectors ------------------------------------------------------------------------
         vecs = []  # (data tensor, len, kind, dtype)
         self._keep = []
+        self._out_private = None
 
         def ll_vector(length: int) -> int:
             # uint32 {fp16, epoch16} words, padded to whole 256-column chunks (the kernel reads them),
@@ -215,6 +216,13 @@ class EngineProgram:
             segs.append((layer.B.tiled.data_ptr(), layer.k, layer.m_dim, src_vec, t_vec, layer.b.data_ptr(),
                          layer.mid.data_ptr(), sd, _lib.F32, 0))
             out_plain = plan.buffers[op.dst].data_ptr() if plain else 0
+            if plain and i == final_op and out_plain == act.data_ptr():
+                # the step input is also the step output (a decoder's residual stream h): the
+                # final stage writes a private buffer that launch() copies back after the kernel,
+                # so no CTA can read vector 0 after another has overwritten it
+                self._out_private = torch.empty_like(plan.buffers[op.dst])
+                self._out_user = plan.buffers[op.dst]
+                out_plain = self._out_private.data_ptr()
             out_code = _lib.dtype_code(plan.buffers[op.dst].dtype) if plain else act_code
             if out_code not in (_lib.F16, _lib.F32):
                 raise ValueError("engine outputs must be float16 or float32")
@@ -315,6 +323,14 @@ class EngineProgram:
 
     def launch(self, stream=None):
         _lib.check(_lib.lib.dbf_engine_launch(ctypes.byref(self._prog), _lib.stream_ptr(stream)), "dbf_engine_launch")
+        if self._out_private is not None:
+            import torch
+
+            if stream is None:
+                self._out_user.copy_(self._out_private)
+            else:
+                with torch.cuda.stream(stream):
+                    self._out_user.copy_(self._out_private)
 
     def launch_io(self, x, y, stream=None):
         """Launch on caller buffers: x replaces the step input (vector 0: batch x len, contiguous,

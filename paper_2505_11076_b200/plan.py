@@ -101,27 +101,42 @@ class DecodePlan:
         self._graph = None
         return self
 
-    def use_fastest(self, steps: int = 5, grid: int | None = None):
-        """Time the decode engine (groups of <= 4 tokens) against the tcgen05 prefill chain on
-        this plan's own buffers (CUDA graph replays, CUDA events) and keep the faster one -- the
-        crossover depends on model and batch (bench.py sweep: 13B at 8 tokens the engine 6.9 ms vs
-        the chain 11.7 ms; 70B at 16 tokens 85 ms vs 62 ms).  The chain is a candidate only for
-        fp16 activations on fp16-scaled layers that kept their sign words (keep_words=True).  The
-        input buffer is restored afterwards; the choice is in ``self.choice`` / ``self.choice_ms``."""
+    def _prefill_ok(self) -> bool:
+        import torch
+
+        return self.buffers[self.input_buffer].dtype == torch.float16 and all(
+            l.scale_dtype == torch.float16 and l.A.words is not None and l.B.words is not None
+            for l in self.layers)
+
+    def default_path(self) -> str:
+        """The static path rule for a token batch: the decode engine up to 8 tokens, the tcgen05
+        prefill chain above (when its layout is available).  Measured crossover (bench.py sweep):
+        13B at 8 tokens engine 6.9 ms vs chain 11.6 ms; 70B at 16 tokens engine 85 ms vs 62 ms."""
+        batch = int(self.buffers[self.input_buffer].shape[0])
+        return "prefill" if batch > 8 and self._prefill_ok() else "engine"
+
+    def use_fastest(self, steps: int = 5, grid: int | None = None, margin: float = 0.10):
+        """Time the decode engine (groups of <= 4 tokens) against the tcgen05 prefill chain on this
+        plan's own buffers (CUDA graph replays, CUDA events; the input is restored before every
+        candidate's warm-up and timing) and keep the static rule's path (default_path) unless the
+        other is faster by more than `margin` -- so timing noise near the crossover cannot flip the
+        choice.  The two paths round differently (13-bit chunk grid vs fp16 products with fp32
+        sums): outputs are each path's own, within the fp16 tolerance of each other.  The choice is
+        in ``self.choice`` / ``self.choice_ms``."""
         import torch
 
         _lib.require_cuda()
         cands = [("engine", lambda: self.use_engine(grid))]
-        if self.buffers[self.input_buffer].dtype == torch.float16 and all(
-                l.scale_dtype == torch.float16 and l.A.words is not None and l.B.words is not None
-                for l in self.layers):
+        if self._prefill_ok():
             cands.append(("prefill", self.use_prefill))
         saved = self.buffers[self.input_buffer].clone()
         timings = {}
         for name, select in cands:
             select()
+            self.buffers[self.input_buffer].copy_(saved)
             self.capture()
             for _ in range(2):
+                self.buffers[self.input_buffer].copy_(saved)
                 self.replay()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -130,9 +145,12 @@ class DecodePlan:
             e1.record()
             e1.synchronize()
             timings[name] = e0.elapsed_time(e1) / steps
-        self.choice = min(timings, key=timings.get)
-        self.choice_ms = timings
-        dict(cands)[self.choice]()
+        choice = self.default_path()
+        other = min(timings, key=timings.get)
+        if other != choice and timings[other] < (1.0 - margin) * timings[choice]:
+            choice = other
+        self.choice, self.choice_ms = choice, timings
+        dict(cands)[choice]()
         self.buffers[self.input_buffer].copy_(saved)
         return self
 

@@ -177,3 +177,7 @@ def test_use_fastest_keeps_the_faster_path_and_its_numbers():
     assert set(plan.choice_ms) == {"engine", "prefill"} and plan.choice in plan.choice_ms
     assert torch.equal(plan.buffers[plan.input_buffer], x)
     assert torch.equal(_run(plan, x), ref_e if plan.choice == "engine" else ref_p)
+    # the static rule wins unless the other path is faster by the margin: a huge margin always
+    # keeps it, whatever the timings
+    plan.use_fastest(steps=2, margin=1.0)
+    assert plan.choice == plan.default_path() == "engine"

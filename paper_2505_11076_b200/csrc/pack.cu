@@ -5,26 +5,70 @@
 
 namespace dbf {
 
-// ---- pack: one warp per 32-column word; __ballot_sync turns 32 lanes' (v > 0) into the word.
-// Bit order: lane i <-> column 32*word + i <-> bit i  (LSB-first, bitcore.py:7-9).
+// ---- pack: one warp per 256-column segment of a row.  Lane l loads the 8 values of columns
+// 8l..8l+7 (one 16-byte load for fp16/bf16, two for fp32, four for fp64 when the row is aligned),
+// tests them on their raw bits (|v| == 1 exactly: NaN and 0 rejected, bitcore.py:79-80) and
+// builds byte l of the segment; four lanes' bytes are one 32-bit word (bit i <-> column
+// 32 * word + i, LSB-first, bitcore.py:7-9).  The first offending row-major index goes to
+// *first_bad by a 64-bit atomicMin.
+template <typename T> struct SignBits;
+template <> struct SignBits<__half> { using U = uint16_t; static constexpr U kAbs = 0x7FFF, kOne = 0x3C00, kSign = 0x8000; };
+template <> struct SignBits<__nv_bfloat16> { using U = uint16_t; static constexpr U kAbs = 0x7FFF, kOne = 0x3F80, kSign = 0x8000; };
+template <> struct SignBits<float> { using U = uint32_t; static constexpr U kAbs = 0x7FFFFFFFu, kOne = 0x3F800000u, kSign = 0x80000000u; };
+template <> struct SignBits<double> {
+  using U = unsigned long long;
+  static constexpr U kAbs = 0x7FFFFFFFFFFFFFFFull, kOne = 0x3FF0000000000000ull, kSign = 0x8000000000000000ull;
+};
+
+constexpr int kPackSegs = 1;  // segments per warp (4 measured slower: fewer resident warps at 66 registers)
+
 template <typename T>
 __global__ void pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols, int64_t ld,
                             uint32_t* __restrict__ words, int64_t pitch,
                             unsigned long long* __restrict__ first_bad) {
+  using SB = SignBits<T>;
+  using U = typename SB::U;
   const int lane = threadIdx.x & 31;
+  const int64_t segs = (pitch + 7) / 8;  // 8 words = 256 columns per segment
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (warp >= rows * pitch) return;
-  const int64_t r = warp / pitch, wj = warp % pitch;
-  const int64_t c = wj * 32 + lane;
-  bool plus = false;
-  if (c < cols) {
-    const double v = to_f64<T>(dense[r * ld + c]);
-    plus = v > 0.0;
-    // |v| != 1 also catches NaN and 0 (bitcore.py:79-80).
-    if (!(fabs(v) == 1.0)) atomicMin(first_bad, (unsigned long long)(r * cols + c));
+  U v[kPackSegs][8];
+  int64_t rr[kPackSegs], ss[kPackSegs];
+#pragma unroll
+  for (int q = 0; q < kPackSegs; ++q) {
+    const int64_t id = warp * kPackSegs + q;
+    rr[q] = id / segs;
+    ss[q] = id - rr[q] * segs;
+    const int64_t c0 = ss[q] * 256 + 8 * lane;
+    if (rr[q] >= rows) continue;
+    const U* row = reinterpret_cast<const U*>(dense + rr[q] * ld);
+    if (c0 + 8 <= cols && ((reinterpret_cast<uintptr_t>(row + c0) & 15) == 0)) {
+#pragma unroll
+      for (int p = 0; p < (int)(8 * sizeof(U) / 16); ++p)
+        *reinterpret_cast<uint4*>(&v[q][p * 16 / sizeof(U)]) = __ldg(reinterpret_cast<const uint4*>(row + c0) + p);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[q][e] = c0 + e < cols ? row[c0 + e] : SB::kOne;  // padding: bit 0 below
+    }
   }
-  const uint32_t w = __ballot_sync(0xffffffffu, plus);
-  if (lane == 0) words[r * pitch + wj] = w;
+#pragma unroll
+  for (int q = 0; q < kPackSegs; ++q) {
+    if (rr[q] >= rows) break;  // warp-uniform
+    const int64_t c0 = ss[q] * 256 + 8 * lane;
+    uint32_t byte = 0;
+    int bad = -1;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const bool in = c0 + e < cols;
+      if (in && (v[q][e] & SB::kAbs) != SB::kOne && bad < 0) bad = e;
+      byte |= (uint32_t)(in && !(v[q][e] & SB::kSign)) << e;
+    }
+    if (bad >= 0) atomicMin(first_bad, (unsigned long long)(rr[q] * cols + c0 + bad));
+    // word j of the segment = bytes of lanes 4j..4j+3
+    const uint32_t b1 = __shfl_down_sync(0xffffffffu, byte, 1), b2 = __shfl_down_sync(0xffffffffu, byte, 2),
+                   b3 = __shfl_down_sync(0xffffffffu, byte, 3);
+    const int64_t wj = ss[q] * 8 + (lane >> 2);
+    if ((lane & 3) == 0 && wj < pitch) words[rr[q] * pitch + wj] = byte | (b1 << 8) | (b2 << 16) | (b3 << 24);
+  }
 }
 
 // ---- sign-of pack: bit = (v >= 0), the svid projection's np.where(Z >= 0, 1, -1) followed by
@@ -217,7 +261,7 @@ extern "C" int dbf_pack_signs(const void* dense, int dtype, int64_t rows, int64_
   cudaStream_t s = (cudaStream_t)stream;
   auto* fb = reinterpret_cast<unsigned long long*>(d_first_bad);
   init_first_bad_kernel<<<1, 1, 0, s>>>(fb);
-  const int64_t threads = rows * word_pitch * 32;
+  const int64_t threads = ceil_div(rows * ((word_pitch + 7) / 8), kPackSegs) * 32;
   return dispatch_float(dtype, [&](auto tag) {
     using T = decltype(tag);
     pack_kernel<T><<<grid_for(threads, 256), 256, 0, s>>>((const T*)dense, rows, cols, ld, words,

@@ -1,5 +1,5 @@
 """Run the 7B decode engine a few times (for ncu: the last launch is the profiled one).
-usage: engine_once.py BLOCKS RUNS [indep]"""
+usage: engine_once.py BLOCKS RUNS [indep] (ENGINE_BATCH=4 for a 4-token step)"""
 import sys
 from pathlib import Path
 
@@ -13,7 +13,8 @@ runs = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 indep = len(sys.argv) > 3 and sys.argv[3] == "indep"
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
-plan = llama_decode_plan("llama2-7b", bpw=2.0, blocks=blocks, generator=g)
+import os
+plan = llama_decode_plan("llama2-7b", bpw=2.0, blocks=blocks, generator=g, batch=int(os.environ.get("ENGINE_BATCH", "1")))
 plan.buffers[plan.input_buffer].normal_(generator=g)
 if indep:  # every op reads a fixed external input of its width, writes its own scratch buffer
     ins = {}

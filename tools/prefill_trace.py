@@ -1,10 +1,10 @@
-"""Per-K-block clock64 trace of CTA (0,0) of the prefill sign GEMM (DBF_PREFILL_TRACE=1)."""
+"""Per-K-block clock64 trace of CTA (0,0) of the prefill sign GEMM (a DBF_PREFILL_TRACE build)."""
 import ctypes
 import os
 import sys
 from pathlib import Path
 
-os.environ["DBF_PREFILL_TRACE"] = "1"
+# needs a -DDBF_PREFILL_TRACE build: tools/build_variant.sh ptr -DDBF_PREFILL_TRACE; DBF_B200_LIB=tools/_x/ptr.so
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch

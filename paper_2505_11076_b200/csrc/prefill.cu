@@ -82,12 +82,9 @@ struct Params {
   int ks_global;           // kscale read from global memory (L1-cached) when the smem copy does not fit
 };
 
-// two rings: NACT activation boxes in shared memory (full_act / empty_act) and NST expanded-A
-// slots in TMEM (full_a / empty); one MMA commit per K block frees a slot of each
-template <int NST, int NACT = NST>
+template <int NST>
 struct __align__(8) BarriersT {
-  uint64_t full_act[NACT];
-  uint64_t empty_act[NACT];
+  uint64_t full_act[NST];
   uint64_t full_a[NST];
   uint64_t empty[NST];
   uint64_t acc_full;
@@ -99,22 +96,12 @@ struct __align__(8) BarriersT {
 // and the 6-stage ring left each K block bound by the activation TMA round trip (~3100 cycles
 // over 6 boxes in flight, tools/prefill_trace.py).
 constexpr int kSmallBN = 64, kSmallStages = 12;
-// CTA-pair tiles: all of TMEM beyond the accumulator for A slots, and half-size (16 KB) activation
-// boxes in a deeper ring: the box round trip (~3.7k cycles under load) bounded the 8-deep ring
-#ifndef DBF_PREFILL_CG2_STAGES
-#define DBF_PREFILL_CG2_STAGES 8
-#endif
-#ifndef DBF_PREFILL_CG2_BOXES
-#define DBF_PREFILL_CG2_BOXES 12
-#endif
-constexpr int kCg2Stages = DBF_PREFILL_CG2_STAGES, kCg2Boxes = DBF_PREFILL_CG2_BOXES;
 
 static_assert(MH * BN + STAGES * kAColsPerStage <= kTmemCols, "TMEM budget (A slots)");
 static_assert(MH * kSmallBN + kSmallStages * kAColsPerStage <= kTmemCols, "TMEM budget (small tiles)");
-static_assert(MH * BN + kCg2Stages * kAColsPerStage <= kTmemCols, "TMEM budget (CTA pairs)");
-template <int TBN, int NST, int NACT = NST>
+template <int TBN, int NST>
 inline size_t smem_bytes_for(int num_kb, bool kscale) {
-  return 1024 /*align slack*/ + (size_t)NACT * TBN * BK * 2 + sizeof(BarriersT<NST, NACT>) + 64 +
+  return 1024 /*align slack*/ + (size_t)NST * TBN * BK * 2 + sizeof(BarriersT<NST>) + 64 +
          (kscale ? (size_t)num_kb * BK * 2 : 0);
 }
 inline size_t smem_bytes(int num_kb, bool kscale) { return smem_bytes_for<BN, STAGES>(num_kb, kscale); }
@@ -128,49 +115,37 @@ __device__ __forceinline__ void expand_word(uint32_t w, const uint32_t* ks, uint
   for (int q = 0; q < 16; ++q) v[q] = ((nw << (15 - q)) & 0x80008000u) ^ ks[q];
 }
 
-// CG2: CTA pairs (2-CTA clusters) share one M = 256 x N = 256 tile through tcgen05.mma.cta_group::2:
-// each CTA expands its own 128 sign rows into its own TMEM and loads only ITS half of the token box
-// (128 tokens), the even CTA issues the pair's MMAs.  Per SM that halves the activation bytes per
-// MMA -- the activation stream into the SM paced the K loop of the one-CTA tile (~570 cycles per
-// 32 KB box against 512 cycles of MMAs: DESIGN.md §7).
-template <bool KSCALE, int TBN = BN, int NST = STAGES, bool CG2 = false, int NACT = NST>
+template <bool KSCALE, int TBN = BN, int NST = STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     sign_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const Params p) {
   // tile configuration: the namespace defaults, or the small-token tiles
   constexpr int BN = TBN, STAGES = NST;
-  constexpr int kActStageBytes = (CG2 ? BN / 2 : BN) * BK * 2;  // CG2: this CTA's half box
+  constexpr int kActStageBytes = BN * BK * 2;
   constexpr int kACol0 = MH * BN;
-  using Barriers = BarriersT<STAGES, NACT>;
+  using Barriers = BarriersT<STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* act = smem;
-  Barriers& bar = *reinterpret_cast<Barriers*>(smem + (size_t)NACT * kActStageBytes);
-  uint32_t* ks_smem = reinterpret_cast<uint32_t*>(smem + (size_t)NACT * kActStageBytes + sizeof(Barriers) + 64);
+  Barriers& bar = *reinterpret_cast<Barriers*>(smem + (size_t)STAGES * kActStageBytes);
+  uint32_t* ks_smem = reinterpret_cast<uint32_t*>(smem + (size_t)STAGES * kActStageBytes + sizeof(Barriers) + 64);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = blockIdx.x * BM;
   const int tok0 = blockIdx.y * BN;
-  const uint32_t rank = CG2 ? cluster_ctarank() : 0u;  // CG2: 0 = the pair's MMA issuer
   const int kb0 = p.part ? (int)blockIdx.z * p.kb_per_split : 0;  // this CTA's K blocks [kb0, kb1)
   const int kb1 = p.part ? min(p.num_kb, kb0 + p.kb_per_split) : p.num_kb;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NACT; ++s) {
-      mbar_init(&bar.full_act[s], 1);
-      mbar_init(&bar.empty_act[s], 1);
-    }
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&bar.full_a[s], CG2 ? 2 * kExpWarps : kExpWarps);  // CG2: both CTAs' expanders
+      mbar_init(&bar.full_act[s], 1);
+      mbar_init(&bar.full_a[s], kExpWarps);
       mbar_init(&bar.empty[s], 1);
     }
     mbar_init(&bar.acc_full, 1);
     fence_mbar_init();
     tma_prefetch_desc(&act_map);
   }
-  if (warp == 1) {
-    if constexpr (CG2) tmem_alloc_cg2<kTmemCols>(&bar.tmem_base);
-    else tmem_alloc<kTmemCols>(&bar.tmem_base);
-  }
+  if (warp == 1) tmem_alloc<kTmemCols>(&bar.tmem_base);
   if (KSCALE && !p.ks_global) {
     // kscale as fp16 pairs, zero beyond K (those columns meet TMA zero-fill anyway)
     const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
@@ -182,7 +157,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CG2) cluster_sync();  // the peer's barriers exist before any remote arrival
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
   const bool tracing = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
@@ -193,66 +167,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     // tools/microbench/tma.cu), so every ring stage gets its own issuing thread: lanes
     // 0..kPerWarp-1 of the three producer warps (3 issuers for 6 stages left small-token tiles,
     // whose MMAs are short, bound at ~600 cycles per K block).
-    // (exactly NACT issuers: issuer i owns box slot i, so no issuer can run a ring phase ahead)
-    constexpr int kPerWarp = (NACT + kNumProducers - 1) / kNumProducers;
-    constexpr int kIssuers = NACT;
-    const int prod = (warp == 0 ? 0 : warp - 1) * kPerWarp + lane;
-    if (lane < kPerWarp && prod < kIssuers) {
+    constexpr int kPerWarp = (STAGES + kNumProducers - 1) / kNumProducers;
+    constexpr int kIssuers = kPerWarp * kNumProducers;
+    if (lane < kPerWarp) {
+      const int prod = (warp == 0 ? 0 : warp - 1) * kPerWarp + lane;
       const uint64_t pol = policy_evict_last();  // activations are re-read by every row tile
       for (int kb = kb0 + prod; kb < kb1; kb += kIssuers) {
-        const int s = (kb - kb0) % NACT;
-        const uint32_t ph = ((kb - kb0) / NACT) & 1;
-        mbar_wait(&bar.empty_act[s], ph ^ 1);
+        const int s = (kb - kb0) % STAGES;
+        const uint32_t ph = ((kb - kb0) / STAGES) & 1;
+        mbar_wait(&bar.empty[s], ph ^ 1);
         if (tracing) p.trace[5 * p.num_kb + kb] = clock64();
-        if constexpr (CG2) {
-          // both halves complete on the even CTA's barrier; the even CTA's issuer expects both
-          if (rank == 0) mbar_arrive_expect_tx(&bar.full_act[s], 2 * p.act_bytes);
-          tma_load_2d_cg2(act + (size_t)s * kActStageBytes, &act_map, kb * BK, tok0 + (int)rank * (BN / 2),
-                          &bar.full_act[s], pol);
-        } else {
-          mbar_arrive_expect_tx(&bar.full_act[s], p.act_bytes);
-          tma_load_2d(act + (size_t)s * kActStageBytes, &act_map, kb * BK, tok0, &bar.full_act[s], pol);
-        }
+        mbar_arrive_expect_tx(&bar.full_act[s], p.act_bytes);
+        tma_load_2d(act + (size_t)s * kActStageBytes, &act_map, kb * BK, tok0, &bar.full_act[s], pol);
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (CG2: the even CTA only, for the pair) ----------------
-    if (lane == 0 && rank == 0) {
-      const uint32_t idesc = idesc_f16_f32(CG2 ? 2 * UM : UM, p.n_mma);
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16_f32(UM, p.n_mma);
       for (int kb = kb0; kb < kb1; ++kb) {
         const int s = (kb - kb0) % STAGES;
         const uint32_t ph = ((kb - kb0) / STAGES) & 1;
-        const int sx = (kb - kb0) % NACT;
-        mbar_wait(&bar.full_act[sx], ((kb - kb0) / NACT) & 1);
+        mbar_wait(&bar.full_act[s], ph);
         if (tracing) p.trace[4 * kb + 3] = clock64();
         mbar_wait(&bar.full_a[s], ph);
         tc_fence_after();
         if (tracing) p.trace[4 * p.num_kb + kb] = clock64();
         const uint32_t a_base = tmem + kACol0 + s * kAColsPerStage;
-        const uint32_t b_base = smem_u32(act + (size_t)sx * kActStageBytes);
+        const uint32_t b_base = smem_u32(act + (size_t)s * kActStageBytes);
 #pragma unroll
         for (int kk = 0; kk < BK / UK; ++kk) {
           const uint64_t bd = sdesc_k_sw128(b_base + kk * UK * 2);
 #pragma unroll
-          for (int h = 0; h < MH; ++h) {
-            if constexpr (CG2)
-              mma_f16_ts_cg2(tmem + kAccCol + h * BN, a_base + h * kAColsPerHalf + kk * (UK / 2), bd, idesc,
-                             (kb != kb0) || (kk != 0));
-            else
-              mma_f16_ts(tmem + kAccCol + h * BN, a_base + h * kAColsPerHalf + kk * (UK / 2), bd, idesc,
-                         (kb != kb0) || (kk != 0));
-          }
+          for (int h = 0; h < MH; ++h)
+            mma_f16_ts(tmem + kAccCol + h * BN, a_base + h * kAColsPerHalf + kk * (UK / 2), bd, idesc,
+                       (kb != kb0) || (kk != 0));
         }
-        if constexpr (CG2) {
-          mma_commit_cg2(&bar.empty[s]);
-          mma_commit_cg2(&bar.empty_act[sx]);
-        } else {
-          mma_commit(&bar.empty[s]);
-          mma_commit(&bar.empty_act[sx]);
-        }
+        mma_commit(&bar.empty[s]);
       }
-      if constexpr (CG2) mma_commit_cg2(&bar.acc_full);
-      else mma_commit(&bar.acc_full);
+      mma_commit(&bar.acc_full);
     }
   } else if (warp >= kExpWarp0) {
     // ---------------- sign expanders + epilogue ----------------
@@ -344,13 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tr) p.trace[4 * kb + 2] = clock64();
         __syncwarp();
         if (lane == 0) {
-          if (CG2 && rank != 0) {  // the pair's MMA issuer waits on the even CTA's barrier
-            mbar_arrive_leader(&bar.full_a[s]);
-            if (two) mbar_arrive_leader(&bar.full_a[s + 1]);
-          } else {
-            mbar_arrive(&bar.full_a[s]);
-            if (two) mbar_arrive(&bar.full_a[s + 1]);
-          }
+          mbar_arrive(&bar.full_a[s]);
+          if (two) mbar_arrive(&bar.full_a[s + 1]);
         }
       }
 #pragma unroll
@@ -383,11 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CG2) cluster_sync();  // no CTA frees TMEM / leaves while its peer may still use it
   if (warp == 1) {
     tc_fence_after();
-    if constexpr (CG2) tmem_dealloc_cg2<kTmemCols>(tmem);
-    else tmem_dealloc<kTmemCols>(tmem);
+    tmem_dealloc<kTmemCols>(tmem);
   }
 }
 
@@ -468,14 +414,8 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   // T <= BN: one token tile whose MMA N / activation box cover only the tokens present
   const bool small = T <= kSmallBN;
   const int n_mma = T >= BN ? BN : (int)ceil_div(T, 16) * 16;
-  // CTA pairs (cta_group::2) for the large-token tiles: each CTA loads half of the 256-token box
-#ifdef DBF_PREFILL_NO_CG2  // experiment builds only
-  const bool cg2 = false;
-#else
-  const bool cg2 = !small && T >= BN;
-#endif
   CUtensorMap map;
-  int st = make_act_map(&map, act, T, K, ld_act, cg2 ? n_mma / 2 : n_mma);
+  int st = make_act_map(&map, act, T, K, ld_act, n_mma);
   if (st != DBF_OK) return st;
   Params p;
   p.words = words;
@@ -489,16 +429,14 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   p.T = (int)T;
   p.num_kb = (int)ceil_div(K, BK);
   p.n_mma = n_mma;
-  p.act_bytes = (cg2 ? n_mma / 2 : n_mma) * BK * 2;  // this CTA's box
+  p.act_bytes = n_mma * BK * 2;
   p.kb_per_split = p.num_kb;
   p.part = nullptr;
-  const size_t ks_fit = small ? smem_bytes_for<kSmallBN, kSmallStages>(p.num_kb, true)
-                       : cg2 ? smem_bytes_for<BN / 2, kCg2Stages, kCg2Boxes>(p.num_kb, true)
-                             : smem_bytes(p.num_kb, true);
+  const size_t ks_fit = small ? smem_bytes_for<kSmallBN, kSmallStages>(p.num_kb, true) : smem_bytes(p.num_kb, true);
   p.ks_global = kscale && ks_fit > (size_t)kMaxSmemOptin ? 1 : 0;
   if (p.ks_global && ((uintptr_t)kscale & 15) != 0) return DBF_ERR_UNSUPPORTED;
   int splits = 1;
-  if (T <= BN && !cg2) {
+  if (T <= BN) {
     int kps = 0;
     const int S = split_count(ceil_div(rows, BM), p.num_kb, &kps);
     if (S > 1 && split_ws && split_ws_bytes >= (size_t)S * T * rows * sizeof(float)) {
@@ -514,13 +452,12 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
     p.trace = trace_buf;
   }
 #endif
-  const unsigned gx = (unsigned)(cg2 ? ceil_div(ceil_div(rows, BM), 2) * 2 : ceil_div(rows, BM));
+  const unsigned gx = (unsigned)ceil_div(rows, BM);
   dim3 grid(gx, (unsigned)ceil_div(T, small ? kSmallBN : BN), (unsigned)splits);
   const bool ks_smem = kscale != nullptr && !p.ks_global;
   // the small configuration pads its shared memory so that one CTA per SM owns all of TMEM
   const size_t smem = small ? std::max<size_t>(smem_bytes_for<kSmallBN, kSmallStages>(p.num_kb, ks_smem), 120 * 1024)
-                     : cg2 ? smem_bytes_for<BN / 2, kCg2Stages, kCg2Boxes>(p.num_kb, ks_smem)
-                           : smem_bytes(p.num_kb, ks_smem);
+                            : smem_bytes(p.num_kb, ks_smem);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -531,7 +468,7 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cg2 ? 2 : 1;
+    attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -542,9 +479,6 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   if (small)
     e = kscale ? go(sign_gemm_kernel<true, kSmallBN, kSmallStages>)
                : go(sign_gemm_kernel<false, kSmallBN, kSmallStages>);
-  else if (cg2)
-    e = kscale ? go(sign_gemm_kernel<true, BN, kCg2Stages, true, kCg2Boxes>)
-               : go(sign_gemm_kernel<false, BN, kCg2Stages, true, kCg2Boxes>);
   else e = kscale ? go(sign_gemm_kernel<true>) : go(sign_gemm_kernel<false>);
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   st = check_launch();

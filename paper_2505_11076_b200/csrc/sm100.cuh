@@ -61,6 +61,8 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// Multicast variant: the box lands at the same shared-memory offset in every CTA of cta_mask and
+// completes bytes on the mbarrier at the same offset in each of them.
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -68,29 +70,6 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// ---- CTA pairs (cta_group::2): the even CTA of a 2-CTA cluster issues the MMAs for both --------
-// A shared::cta address of this CTA used as a shared::cluster address carries the CTA's rank in
-// bit 24; clearing it names the same offset in the pair's even (leader) CTA.
-constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
-// TMA load into THIS CTA's shared memory whose transaction bytes complete on the leader's barrier
-__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
-                                                uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar) & kPeerBitMask), "l"(policy)
-      : "memory");
-}
-// arrive on the leader CTA's barrier at the same offset.  Default (.release.cta) semantics, as for
-// a local arrive: what it publishes is TMEM written before tcgen05.fence::before_thread_sync, and
-// the leader waits with a plain try_wait.  The cluster-scope forms compile to MEMBAR.ALL.GPU (the
-// arrive waits for this thread's in-flight global loads: the sign-word prefetch) and CCTL.IVALL
-// (the wait drops L1) -- measured 40% slower (profiles/r2_prefill_small_tokens.md).
-__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerBitMask)
-               : "memory");
 }
 
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -115,18 +94,6 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* smem_dst) {  // whole warp
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {  // whole warp, same warp as alloc
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
-}
-// pair allocation: the same warp of both CTAs of the pair issues it (the same columns in both)
-template <uint32_t kCols>
-__device__ __forceinline__ void tmem_alloc_cg2(uint32_t* smem_dst) {
-  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
-               "n"(kCols)
-               : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-}
-template <uint32_t kCols>
-__device__ __forceinline__ void tmem_dealloc_cg2(uint32_t taddr) {
-  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -172,25 +139,6 @@ __device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uin
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// D[tmem] (+)= A[tmem] . B[smem]^T for the CTA pair (M = 256: rows 0-127 in the even CTA's TMEM,
-// 128-255 in the odd CTA's; B split by N, each CTA's half at the same shared-memory offset)
-__device__ __forceinline__ void mma_f16_ts_cg2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                               uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// Arrive on the barrier at this offset in both CTAs of the pair once the pair's MMAs complete
-__device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"((uint16_t)0x3)
-      : "memory");
-}
 // Arrive on `bar` once all previously issued tcgen05.mma of this thread have completed.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -198,6 +146,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Arrive on `bar` in every CTA of cta_mask (same shared-memory offset) once this thread's MMAs complete.
 
 // ---- tcgen05: TMEM <-> registers (32 lanes x 32 bit, 32 columns per thread) -------------------
 #define DBF_R32(v)                                                                                       \

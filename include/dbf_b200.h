@@ -343,6 +343,25 @@ int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, int32_t* regs
 /* Launch one run of the program (cooperative: all CTAs co-resident; one kernel). */
 int dbf_engine_launch(const dbf_engine_program* program, void* stream);
 
+/* ---- batched decode: 2-16 tokens, one pass over the weights -------------------------------- */
+/*
+ * dbf_forward (kernel.py:48-62) for a small token batch (batch <= 16): per stage, every extracted
+ * sign fragment feeds one int8 IMMA per group of 4 tokens, so each sign matrix is read ONCE for
+ * all tokens (the decode engine carries 4 tokens per launch).  Numerics are the engine's: each
+ * (token, 256-column chunk) is quantized to a 13-bit grid relative to its chunk max (two balanced
+ * int8 digit planes), chunk sums are exact integers, accumulation and the intermediate t are
+ * fp32 (DESIGN.md §5 tolerance).  K is split over CTAs; split partials are summed in split order
+ * (deterministic).  A non-finite input chunk makes the outputs it feeds NaN; `status` (optional,
+ * device) gets bit 1 for a non-finite output and bit 2 for a finite value beyond the fp16 range.
+ * Layouts: A / B tiled (dbf_tile_signs), X batch x m (stride ldx), Y batch x n (stride ldy).
+ */
+size_t dbf_forward_batched_workspace_bytes(int64_t n, int64_t k, int64_t m, int64_t batch);
+int dbf_forward_batched(const void* A_tiled, const void* B_tiled, const void* a, const void* mid,
+                        const void* b, int scale_dtype, int64_t n, int64_t k, int64_t m,
+                        const void* X, int x_dtype, int64_t batch, int64_t ldx, void* Y,
+                        int y_dtype, int64_t ldy, void* workspace, size_t workspace_bytes,
+                        unsigned* status, void* stream);
+
 /* ---- prefill / batched path: tcgen05 + TMEM sign GEMMs (>= 64 tokens) ------------------ */
 /*
  * The same forward as dbf_forward (kernel.py:48-62) for token batches, as two tensor-core GEMMs

@@ -30,6 +30,7 @@ from .kernel import (
     bench_forward,
     forward,
     forward_device,
+    forward_batched,
     forward_prefill,
     random_device_layer,
     sign_matvec,
@@ -56,6 +57,7 @@ __all__ = [
     "dumps_dbf",
     "forward",
     "forward_device",
+    "forward_batched",
     "forward_prefill",
     "load_dbf",
     "middle_dim",

@@ -130,6 +130,46 @@ def forward_prefill(X, layer: DeviceLayer, out=None):
     return Y
 
 
+BATCHED_MAX_TOKENS = 16
+
+
+def forward_batched(X, layer: DeviceLayer, out=None, status=None):
+    """Y = forward(X, layer) (/root/reference/pkg/src/dbf/kernel.py:48-62) for a CUDA batch of
+    1-16 token rows with ONE pass over each sign matrix for all tokens (dbf_forward_batched,
+    csrc/batched.cu): every extracted sign fragment feeds one int8 IMMA per group of 4 tokens.
+    Numerics are the decode engine's (13-bit grid per token and 256-column chunk, exact chunk sums,
+    fp32 accumulation and intermediate); ``status`` (a 1-element int32 CUDA tensor, optional) gets
+    bit 1 for a non-finite output and bit 2 for an fp16 overflow."""
+    import torch
+
+    if X.ndim != 2:
+        raise ValueError(f"X must be 2-D, got ndim={X.ndim}")
+    if X.shape[1] != layer.m_dim:
+        raise ValueError(f"X has {X.shape[1]} columns, expected {layer.m_dim}")
+    batch = X.shape[0]
+    if not 1 <= batch <= BATCHED_MAX_TOKENS:
+        raise ValueError(f"forward_batched takes 1-{BATCHED_MAX_TOKENS} token rows, got {batch}")
+    if X.stride(1) != 1:
+        X = X.contiguous()
+    Y = out if out is not None else torch.empty((batch, layer.n), dtype=X.dtype, device=X.device)
+    if Y.stride(1) != 1:
+        raise ValueError("out must have unit column stride")
+    ws_bytes = _lib.lib.dbf_forward_batched_workspace_bytes(layer.n, layer.k, layer.m_dim, batch)
+    ws = _workspace(ws_bytes, X.device)
+    _lib.check(
+        _lib.lib.dbf_forward_batched(
+            layer.A.tiled.data_ptr(), layer.B.tiled.data_ptr(),
+            layer.a.data_ptr(), layer.mid.data_ptr(), layer.b.data_ptr(), _lib.dtype_code(layer.a.dtype),
+            layer.n, layer.k, layer.m_dim,
+            X.data_ptr(), _lib.dtype_code(X.dtype), batch, X.stride(0),
+            Y.data_ptr(), _lib.dtype_code(Y.dtype), Y.stride(0),
+            ws.data_ptr(), ws.numel(), status.data_ptr() if status is not None else None, _lib.stream_ptr(),
+        ),
+        "dbf_forward_batched",
+    )
+    return Y
+
+
 def forward_device(X, layer: DeviceLayer, out=None, out_dtype=None):
     """Y = forward(X, layer) for a CUDA tensor X (batch x m or m); returns a CUDA tensor.
 

@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 from . import _lib
 from .budget import middle_dim
 from .device import DeviceLayer
-from .kernel import forward_device, forward_prefill, random_device_layer
+from .kernel import BATCHED_MAX_TOKENS, forward_batched, forward_device, forward_prefill, random_device_layer
 
 # Llama-2 linear shapes (n = out_features, m = in_features), SURVEY.md §8a
 LLAMA_SHAPES = {
@@ -89,7 +89,23 @@ class DecodePlan:
     def use_layer_kernels(self):
         """Run one dbf_forward (two GEMV launches) per layer instead of the engine."""
         self.engine = None
-        self._prefill = False
+        self._mode = "layer"
+        self._graph = None
+        return self
+
+    def use_batched(self):
+        """Run every layer through dbf_forward_batched (csrc/batched.cu): 1-16 tokens, one pass
+        over each sign matrix for all of them (five short kernels per layer; the engine carries 4
+        tokens per launch and re-streams the weights for every group of 4)."""
+        import torch
+
+        batch = int(self.buffers[self.input_buffer].shape[0])
+        if batch > BATCHED_MAX_TOKENS:
+            raise ValueError(f"use_batched takes at most {BATCHED_MAX_TOKENS} tokens, the plan has {batch}")
+        self.engine = None
+        self._mode = "batched"
+        if getattr(self, "_bstatus", None) is None:
+            self._bstatus = torch.zeros(1, dtype=torch.int32, device=self.buffers[0].device)
         self._graph = None
         return self
 
@@ -97,7 +113,7 @@ class DecodePlan:
         """Run every layer through the tcgen05 sign GEMMs (forward_prefill) whatever the batch:
         one pass over the weights for all tokens (fp16 activations; layers built with keep_words)."""
         self.engine = None
-        self._prefill = True
+        self._mode = "prefill"
         self._graph = None
         return self
 
@@ -109,11 +125,15 @@ class DecodePlan:
             for l in self.layers)
 
     def default_path(self) -> str:
-        """The static path rule for a token batch: the decode engine up to 8 tokens, the tcgen05
-        prefill chain above (when its layout is available).  Measured crossover (bench.py sweep):
-        13B at 8 tokens engine 6.9 ms vs chain 11.6 ms; 70B at 16 tokens engine 85 ms vs 62 ms."""
+        """The static path rule for a token batch: the decode engine up to 4 tokens (one launch),
+        the single-pass batched kernels for 5-16, the tcgen05 prefill chain above (when its layout
+        is available).  Measured (bench.py sweep)."""
         batch = int(self.buffers[self.input_buffer].shape[0])
-        return "prefill" if batch > 8 and self._prefill_ok() else "engine"
+        if batch <= 4:
+            return "engine"
+        if batch <= BATCHED_MAX_TOKENS:
+            return "batched"
+        return "prefill" if self._prefill_ok() else "engine"
 
     def use_fastest(self, steps: int = 5, grid: int | None = None, margin: float = 0.10):
         """Time the decode engine (groups of <= 4 tokens) against the tcgen05 prefill chain on this
@@ -127,6 +147,8 @@ class DecodePlan:
 
         _lib.require_cuda()
         cands = [("engine", lambda: self.use_engine(grid))]
+        if int(self.buffers[self.input_buffer].shape[0]) <= BATCHED_MAX_TOKENS:
+            cands.append(("batched", self.use_batched))
         if self._prefill_ok():
             cands.append(("prefill", self.use_prefill))
         saved = self.buffers[self.input_buffer].clone()
@@ -158,7 +180,13 @@ class DecodePlan:
         if self.engine is not None:
             self.engine.launch()
             return
-        run = forward_prefill if getattr(self, "_prefill", False) else forward_device
+        mode = getattr(self, "_mode", "layer")
+        if mode == "batched":
+            for op in self.ops:
+                forward_batched(self.buffers[op.src], self.layers[op.layer], out=self.buffers[op.dst],
+                                status=self._bstatus)
+            return
+        run = forward_prefill if mode == "prefill" else forward_device
         for op in self.ops:
             run(self.buffers[op.src], self.layers[op.layer], out=self.buffers[op.dst])
 
@@ -213,12 +241,15 @@ class DecodePlan:
 
         progs = getattr(self.engine, "groups", [self.engine]) if self.engine is not None else []
         progs = [p for p in progs if hasattr(p, "run_counter")]
+        words = [p.run_counter[2:3] for p in progs]
+        if getattr(self, "_mode", None) == "batched" and self.engine is None:
+            progs, words = [self], [self._bstatus]
         if not progs:
             return None
         if getattr(self, "_status_host", None) is None or self._status_host.numel() != len(progs):
             self._status_host = torch.zeros(len(progs), dtype=torch.int32).pin_memory()
-        for i, p in enumerate(progs):
-            self._status_host[i:i + 1].copy_(p.run_counter[2:3], non_blocking=True)
+        for i, w in enumerate(words):
+            self._status_host[i:i + 1].copy_(w, non_blocking=True)
         return progs
 
     def _raise_status(self, progs):
@@ -231,6 +262,15 @@ class DecodePlan:
         overflowed fp16 (device calls: replay()/_eager() do not synchronize to look)."""
         if self.engine is not None:
             self.engine.check()
+        elif getattr(self, "_mode", None) == "batched":
+            from .engine import DbfOverflowError, STATUS_NONFINITE, STATUS_OVERFLOW
+
+            st = int(self._bstatus.item())
+            if st:
+                self._bstatus.zero_()
+                what = [w for bit, w in ((STATUS_NONFINITE, "a non-finite value"),
+                                         (STATUS_OVERFLOW, "a value beyond the fp16 range")) if st & bit]
+                raise DbfOverflowError(f"batched decode produced {' and '.join(what)} (status {st:#x})")
 
 
 def layerwise_ks(model: str = "llama2-13b", target_bpw: float = 1.5, floor_bpw: float = 1.0, cap_bpw: float = 2.3,

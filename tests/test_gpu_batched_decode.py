@@ -1,0 +1,158 @@
+"""The single-pass batched decode (dbf_forward_batched, csrc/batched.cu; north_star subsystem 2,
+BASELINE configs[3]-[4] at 2-16 tokens) against the float64 oracle on the same bytes.
+
+Tolerance as for the decode engine whose numerics it shares (13-bit grid per token and 256-column
+chunk): max|err|/max|ref| and ||err||/||ref|| <= 1e-2 per token row.  Also: deterministic bits,
+ragged shapes, non-finite inputs confined to their own token (NaN + status bit), the fp16-overflow
+status, and a decoder chain through DecodePlan.use_batched against the per-layer kernels."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_2505_11076_b200 as P  # noqa: E402
+import oracle  # noqa: E402
+from conftest import rel_max, rel_norm  # noqa: E402
+
+TOL = 1e-2
+
+
+def _ref(x, layer):
+    return oracle.c_forward(x.double().cpu().numpy(), layer.a.double().cpu().numpy(), layer.A.to_host().bits,
+                            layer.mid.double().cpu().numpy(), layer.B.to_host().bits, layer.b.double().cpu().numpy())
+
+
+@pytest.mark.parametrize("batch", [1, 2, 4, 5, 8, 13, 16])
+def test_batched_matches_oracle(batch):
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(100 + batch)
+    n, k, m = 4096, 5952, 11008  # the 7B down shape
+    layer = P.random_device_layer(n, k, m, generator=g, keep_words=True)
+    x = torch.randn((batch, m), generator=g, device="cuda").half()
+    y = P.forward_batched(x, layer).double().cpu().numpy()
+    ref = _ref(x, layer)
+    for t in range(batch):
+        assert rel_max(y[t], ref[t]) <= TOL and rel_norm(y[t], ref[t]) <= TOL, (t, rel_max(y[t], ref[t]))
+
+
+@pytest.mark.parametrize("shape", [(200, 96, 136), (1000, 1100, 1024), (1024, 1792, 8192), (33, 17, 300)])
+def test_batched_ragged_shapes(shape):
+    import torch
+
+    n, k, m = shape
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + k + m)
+    layer = P.random_device_layer(n, k, m, generator=g, keep_words=True)
+    for batch in (3, 11):
+        x = torch.randn((batch, m), generator=g, device="cuda").half()
+        y = P.forward_batched(x, layer).double().cpu().numpy()
+        ref = _ref(x, layer)
+        for t in range(batch):
+            assert rel_max(y[t], ref[t]) <= TOL and rel_norm(y[t], ref[t]) <= TOL, (shape, batch, t)
+
+
+def test_batched_deterministic_and_strided_io():
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    layer = P.random_device_layer(4096, 2048, 4096, generator=g, keep_words=True)
+    big = torch.randn((10, 4096 + 64), generator=g, device="cuda").half()
+    x = big[:, 32:32 + 4096]  # row stride 4160
+    out = torch.zeros((10, 4096 + 8), dtype=torch.half, device="cuda")
+    y1 = P.forward_batched(x, layer, out=out[:, :4096]).clone()
+    y2 = P.forward_batched(x.contiguous(), layer)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert torch.count_nonzero(out[:, 4096:]) == 0
+    ref = _ref(x, layer)
+    assert rel_max(y2.double().cpu().numpy(), ref) <= TOL
+
+
+def test_batched_nonfinite_confined_and_status():
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(8)
+    layer = P.random_device_layer(1024, 1024, 2048, generator=g, keep_words=True)
+    x = torch.randn((6, 2048), generator=g, device="cuda").half()
+    x[2, 700] = float("inf")
+    x[4, 5] = float("nan")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    y = P.forward_batched(x, layer, status=status).double().cpu().numpy()
+    assert np.isnan(y[2]).all() and np.isnan(y[4]).all()
+    ref = _ref(x[[0, 1, 3, 5]], layer)
+    assert rel_max(y[[0, 1, 3, 5]], ref) <= TOL
+    assert int(status.item()) & 1
+
+
+def test_batched_fp16_overflow_status():
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    layer = P.random_device_layer(512, 512, 1024, generator=g)
+    layer.a.fill_(60000.0)  # |y| far beyond 65504 for random inputs
+    x = torch.randn((5, 1024), generator=g, device="cuda").half()
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    y = P.forward_batched(x, layer, status=status)
+    torch.cuda.synchronize()
+    assert torch.isinf(y).any()
+    assert int(status.item()) & 2
+
+
+def test_batched_rejects_bad_input():
+    import torch
+
+    layer = P.random_device_layer(64, 32, 64)
+    with pytest.raises(ValueError):
+        P.forward_batched(torch.zeros((17, 64), dtype=torch.half, device="cuda"), layer)
+    with pytest.raises(ValueError):
+        P.forward_batched(torch.zeros((4, 63), dtype=torch.half, device="cuda"), layer)
+    with pytest.raises(ValueError):
+        P.forward_batched(torch.zeros((64,), dtype=torch.half, device="cuda"), layer)
+
+
+@pytest.mark.parametrize("batch", [5, 8, 16])
+def test_batched_plan_chain_matches_layer_kernels(batch):
+    """Two 7B decoder blocks (14 layers in dataflow order) through DecodePlan.use_batched vs the
+    exact per-layer kernels (dbf_forward), and the plan's default path at this batch."""
+    import torch
+    from paper_2505_11076_b200.plan import llama_decode_plan
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(40 + batch)
+    plan = llama_decode_plan("llama2-7b", bpw=2.0, batch=batch, blocks=2, generator=g)
+    assert plan.default_path() == "batched"
+    x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
+    outs = []
+    for use in (plan.use_layer_kernels, plan.use_batched):
+        use()
+        plan.buffers[plan.input_buffer].copy_(x)
+        plan._eager()
+        torch.cuda.synchronize()
+        outs.append(plan.buffers[plan.output_buffer].double().cpu().numpy())
+    assert rel_max(outs[1], outs[0]) <= TOL and rel_norm(outs[1], outs[0]) <= TOL
+    # graph replay of the batched chain reproduces the eager bits; run() checks the status word
+    # (capture() runs the chain once as its warm-up, and the plan's input buffer is also its output)
+    plan.capture()
+    y = plan.run(x.cpu())
+    assert np.array_equal(y.double().numpy(), outs[1])
+
+
+def test_batched_plan_raises_on_overflow():
+    import torch
+    from paper_2505_11076_b200.plan import DecodePlan, PlanOp
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    layer = P.random_device_layer(512, 512, 1024, generator=g)
+    layer.a.fill_(60000.0)
+    bufs = [torch.randn((6, 1024), generator=g, device="cuda").half(), torch.zeros((6, 512), dtype=torch.half,
+                                                                                   device="cuda")]
+    plan = DecodePlan([layer], [PlanOp(0, 0, 1, "x")], bufs, input_buffer=0, output_buffer=1).use_batched()
+    with pytest.raises(P.DbfOverflowError):
+        plan.run(bufs[0].cpu())

@@ -434,22 +434,25 @@ def prefill_bench(model: str, bpw: float, tokens: int, steps: int, warmup: int):
 def sweep_bench(steps: int):
     """BASELINE configs[3] / [4] at one GPU: the decode engine over Llama-2-70B shapes at 2 bpw
     (batch 1, 4, 16) and Llama-2-13B shapes across bits/weight (batch 1, 4, 8), plus 13B at batch 8
-    through the int8 GEMV layer chain and batch 64 through the tcgen05 prefill chain.  Up to 4
-    tokens share every MMA of one engine launch; larger batches run consecutive launches over
-    groups of 4.  Every number is a full model step of linears."""
+    through the int8 GEMV layer chain and batch 64 through the tcgen05 prefill chain, and the
+    single-pass batched kernels at 8 and 16 tokens.  Up to 4 tokens share every MMA of one engine
+    launch; larger batches run consecutive launches over groups of 4 (or the batched kernels: one
+    weight pass for up to 16).  Every number is a full model step of linears."""
     import torch
 
     from paper_2505_11076_b200.plan import llama_decode_plan
 
     rows = []
 
-    def one(model, bpw, batch, engine, prefill=False):
+    def one(model, bpw, batch, engine, prefill=False, batched=False):
         g = torch.Generator(device="cuda")
         g.manual_seed(5)
         plan = llama_decode_plan(model, bpw=bpw, batch=batch, generator=g, keep_words=prefill or None)
         plan.buffers[plan.input_buffer].normal_(generator=g)
         if prefill:
             plan.use_prefill()
+        elif batched:
+            plan.use_batched()
         else:
             plan.use_engine() if engine else plan.use_layer_kernels()
         plan.capture()
@@ -458,6 +461,7 @@ def sweep_bench(steps: int):
         rows.append({"model": model, "bpw": bpw, "batch": batch,
                      "path": (("engine" if batch <= 4 else f"engine, {-(-batch // 4)} launches of <= 4 tokens")
                               if engine else ("tcgen05 prefill chain" if batch >= 64 or prefill else
+                                              "single-pass batched kernels" if batched else
                                               "int8 GEMV chain (pre-quantized batch)")),
                      "ms_per_step": ms, "gbs": b / (ms * 1e-3) / 1e9,
                      "tokens_per_s_linears_only": batch * 1e3 / ms, "layers": len(plan.ops)})
@@ -468,6 +472,8 @@ def sweep_bench(steps: int):
     one("llama2-70b", 2.0, 4, True)
     one("llama2-70b", 2.0, 16, True)
     one("llama2-70b", 2.0, 16, False, prefill=True)
+    one("llama2-70b", 2.0, 16, False, batched=True)
+    one("llama2-70b", 2.0, 8, False, batched=True)
     for bpw in (1.0, 1.5, 2.0, 2.3):
         one("llama2-13b", bpw, 1, True)
     one("llama2-7b", 2.0, 4, True)
@@ -475,6 +481,8 @@ def sweep_bench(steps: int):
     one("llama2-13b", 1.5, 8, True)
     one("llama2-13b", 1.5, 8, False)
     one("llama2-13b", 1.5, 8, False, prefill=True)
+    one("llama2-13b", 1.5, 8, False, batched=True)
+    one("llama2-7b", 2.0, 8, False, batched=True)
     one("llama2-13b", 1.5, 64, False)
     # BASELINE configs[4] as specified: a NON-uniform layer-wise k (1.0-2.3 bits/weight across the
     # 280 linears, 1.5 on average, from the reference's greedy allocation -- plan.layerwise_ks)
@@ -489,14 +497,14 @@ def sweep_bench(steps: int):
         plan = llama_decode_plan("llama2-13b", batch=batch, generator=g, ks=ks, keep_words=batch >= 64)
         plan.buffers[plan.input_buffer].normal_(generator=g)
         path = plan.default_path()
-        plan.use_prefill() if path == "prefill" else plan.use_engine()
+        {"prefill": plan.use_prefill, "batched": plan.use_batched, "engine": plan.use_engine}[path]()
         plan.capture()
         ms = time_graph(plan._graph, steps, 3)
         b = plan.bytes_per_step()
         rows.append({"model": "llama2-13b", "bpw": "layerwise", "bpw_min": min(bpws), "bpw_max": max(bpws),
                      "bpw_mean_sign_bits": sum(k * (n + m) for k, (_, n, m) in zip(ks, shp)) /
                                            sum(n * m for _, n, m in shp),
-                     "batch": batch, "path": path if batch <= 4 or path == "prefill" else
+                     "batch": batch, "path": path if batch <= 4 or path != "engine" else
                      f"engine, {-(-batch // 4)} launches of <= 4 tokens",
                      "ms_per_step": ms, "gbs": b / (ms * 1e-3) / 1e9,
                      "tokens_per_s_linears_only": batch * 1e3 / ms, "layers": len(plan.ops)})

@@ -226,7 +226,7 @@ struct GemvArgs {
 // memory ring by bulk copy, two chunks ahead (loaded at use from L1 they were the whole stall
 // profile: ~14 % L2 misses behind every IMMA); in registers the next k-block's fragments load
 // while the current one's IMMAs run.  Sign words run two chunks ahead of the MMAs.
-template <int NJ>
+template <int NJ, int RB>
 __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
   using namespace sm100;
   constexpr int kBBytes = 8 * NJ * 32 * 8;  // B fragments of one chunk
@@ -234,19 +234,28 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
   __shared__ __align__(128) uint8_t bsm[kSlots][kBBytes];
   __shared__ __align__(8) uint64_t full[kSlots], empty[kSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rb = blockIdx.x * kGemvWarps + warp;
+  const int rb0 = (blockIdx.x * kGemvWarps + warp) * RB;  // this warp's RB row blocks
   const int c0 = blockIdx.y * g.cps, c1 = min(g.nch, c0 + g.cps), n = c1 - c0;
   const int gr = lane >> 2, tig = lane & 3;
-  const bool live = rb < g.nrb;  // a warp past the last row block still runs the ring (no stores)
-  const uint4* wb = g.tiled + (int64_t)(live ? rb : 0) * g.nch * 32 + lane;
   const uint64_t pol = evict_first_policy();
+  const uint4* wb[RB];
+  bool live[RB];
+#pragma unroll
+  for (int q = 0; q < RB; ++q) {
+    live[q] = rb0 + q < g.nrb;  // a warp past the last row block still runs the ring (no stores)
+    wb[q] = g.tiled + (int64_t)(live[q] ? rb0 + q : 0) * g.nch * 32 + lane;
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSlots; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], kGemvWarps);
     fence_mbar_init();
   }
   // the sign words are constant: their first chunks load while the previous kernel drains
-  uint4 w = live && n > 0 ? ld_stream(wb + (int64_t)c0 * 32, pol) : make_uint4(0, 0, 0, 0);
-  uint4 wn = live && n > 1 ? ld_stream(wb + (int64_t)(c0 + 1) * 32, pol) : make_uint4(0, 0, 0, 0);
+  uint4 w[RB], wn[RB];
+#pragma unroll
+  for (int q = 0; q < RB; ++q) {
+    w[q] = live[q] && n > 0 ? ld_stream(wb[q] + (int64_t)c0 * 32, pol) : make_uint4(0, 0, 0, 0);
+    wn[q] = live[q] && n > 1 ? ld_stream(wb[q] + (int64_t)(c0 + 1) * 32, pol) : make_uint4(0, 0, 0, 0);
+  }
   __syncthreads();
   grid_wait();
   grid_launch_dependents();
@@ -257,9 +266,11 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
       bulk_copy_g2s(bsm[i], bsrc + (size_t)i * kBBytes, kBBytes, &full[i]);
     }
   }
-  float y[NJ][2];
+  float y[RB][NJ][2];
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) y[j][0] = y[j][1] = 0.f;
+  for (int q = 0; q < RB; ++q)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) y[q][j][0] = y[q][j][1] = 0.f;
   for (int i = 0; i < n; ++i) {
     const int c = c0 + i, slot = i % kSlots;
     if (threadIdx.x == 0 && i + 2 < n) {  // chunk i + 2 into the slot chunk i - 1 held
@@ -268,14 +279,18 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
       mbar_arrive_expect_tx(&full[s2], kBBytes);
       bulk_copy_g2s(bsm[s2], bsrc + (size_t)(i + 2) * kBBytes, kBBytes, &full[s2]);
     }
-    const uint4 wnn = live && i + 2 < n ? ld_stream(wb + (int64_t)(c + 2) * 32, pol) : make_uint4(0, 0, 0, 0);
+    uint4 wnn[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q)
+      wnn[q] = live[q] && i + 2 < n ? ld_stream(wb[q] + (int64_t)(c + 2) * 32, pol) : make_uint4(0, 0, 0, 0);
     int Fv[NJ], Tv[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) Fv[j] = __ldg(g.F + c * g.tpad + 4 * j + tig), Tv[j] = __ldg(g.T + c * g.tpad + 4 * j + tig);
-    int acc[NJ][4];
+    int acc[RB][NJ][4];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
-    const uint4 w4 = make_uint4(w.x >> 4, w.y >> 4, w.z >> 4, w.w >> 4);
+    for (int q = 0; q < RB; ++q)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[q][j][0] = acc[q][j][1] = acc[q][j][2] = acc[q][j][3] = 0;
     mbar_wait(&full[slot], (i / kSlots) & 1);
     const uint2* bf = reinterpret_cast<const uint2*>(bsm[slot]) + lane;
     uint2 bc[NJ];
@@ -286,11 +301,15 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
       uint2 bn[NJ];
 #pragma unroll
       for (int j = 0; j < NJ; ++j) bn[j] = r < 7 ? bf[((r + 1) * NJ + j) * 32] : make_uint2(0, 0);
-      const uint4 src = r < 4 ? w : w4;
       const uint32_t m = 0x01010101u << (r & 3);
-      const uint32_t a0 = src.x & m, a1 = src.y & m, a2 = src.z & m, a3 = src.w & m;
+      const int sh = r < 4 ? 0 : 4;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) imma_u8s8(acc[j], a0, a1, a2, a3, bc[j].x, bc[j].y);
+      for (int q = 0; q < RB; ++q) {
+        const uint32_t a0 = (w[q].x >> sh) & m, a1 = (w[q].y >> sh) & m, a2 = (w[q].z >> sh) & m,
+                       a3 = (w[q].w >> sh) & m;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) imma_u8s8(acc[q][j], a0, a1, a2, a3, bc[j].x, bc[j].y);
+      }
 #pragma unroll
       for (int j = 0; j < NJ; ++j) bc[j] = bn[j];
     }
@@ -303,23 +322,29 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
       // P / (2^F kQScale) (exact P, |P| < 2^24); a chunk with inf / NaN (F = kBadF) makes the
       // outputs it feeds NaN
       const float inv = __int_as_float((127 - F) << 23) * (1.f / kQScale);
-      const float p0 = (float)(((acc[j][0] + 256 * acc[j][1]) >> 2) - T);
-      const float p1 = (float)(((acc[j][2] + 256 * acc[j][3]) >> 2) - T);
-      y[j][0] = F == kBadF ? __int_as_float(0x7FC00000) : fmaf(p0, inv, y[j][0]);
-      y[j][1] = F == kBadF ? __int_as_float(0x7FC00000) : fmaf(p1, inv, y[j][1]);
-    }
-    w = wn;
-    wn = wnn;
-  }
-  if (!live) return;
-  float* out = g.part + (size_t)blockIdx.y * g.tpad * g.ldp;
-  const int row0 = rb * 16 + gr;
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const int t = 4 * j + tig;
-    if (t < g.batch) {
-      if (row0 < g.rows) out[(size_t)t * g.ldp + row0] = y[j][0];
-      if (row0 + 8 < g.rows) out[(size_t)t * g.ldp + row0 + 8] = y[j][1];
+      for (int q = 0; q < RB; ++q) {
+        const float p0 = (float)(((acc[q][j][0] + 256 * acc[q][j][1]) >> 2) - T);
+        const float p1 = (float)(((acc[q][j][2] + 256 * acc[q][j][3]) >> 2) - T);
+        y[q][j][0] = F == kBadF ? __int_as_float(0x7FC00000) : fmaf(p0, inv, y[q][j][0]);
+        y[q][j][1] = F == kBadF ? __int_as_float(0x7FC00000) : fmaf(p1, inv, y[q][j][1]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q) w[q] = wn[q], wn[q] = wnn[q];
+  }
+  float* out = g.part + (size_t)blockIdx.y * g.tpad * g.ldp;
+#pragma unroll
+  for (int q = 0; q < RB; ++q) {
+    if (!live[q]) continue;
+    const int row0 = (rb0 + q) * 16 + gr;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int t = 4 * j + tig;
+      if (t < g.batch) {
+        if (row0 < g.rows) out[(size_t)t * g.ldp + row0] = y[q][j][0];
+        if (row0 + 8 < g.rows) out[(size_t)t * g.ldp + row0 + 8] = y[q][j][1];
+      }
     }
   }
 }
@@ -360,9 +385,12 @@ inline int tpad_of(int64_t batch) { return (int)ceil_div(batch, 4) * 4; }
 inline int ldp_of(int64_t rows) { return (int)ceil_div(rows, 4) * 4; }
 inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+// row blocks per warp: two where there are enough rows (the chunk's B fragments, barriers and
+// scale loads then serve twice the MMAs)
+inline int rb_per_warp(int64_t nrb) { return nrb >= 512 ? 2 : 1; }
 // K splits of one GEMV: enough CTAs for kCtasPerSm per SM, whole chunks per split
 inline int split_count(int64_t nrb, int64_t nch, int* cps) {
-  const int64_t gx = ceil_div(nrb, kGemvWarps);
+  const int64_t gx = ceil_div(nrb, (int64_t)kGemvWarps * rb_per_warp(nrb));
   int64_t S = std::max<int64_t>(1, ceil_div((int64_t)kCtasPerSm * kNumSMs, gx));
   S = std::min<int64_t>(std::min<int64_t>(S, kMaxSplits), nch);
   const int64_t c = ceil_div(nch, S);
@@ -405,14 +433,18 @@ static int launch_pdl(void (*kern)(KArgs...), dim3 grid, int threads, cudaStream
   if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
   return check_launch();
 }
-static int gemv(const GemvArgs& a, int nj, int splits, cudaStream_t s) {
-  const dim3 grid((unsigned)ceil_div(a.nrb, kGemvWarps), (unsigned)splits);
+template <int RB>
+static int gemv_rb(const GemvArgs& a, int nj, int splits, cudaStream_t s) {
+  const dim3 grid((unsigned)ceil_div(a.nrb, kGemvWarps * RB), (unsigned)splits);
   switch (nj) {
-    case 1: return launch_pdl(gemv_kernel<1>, grid, kGemvWarps * 32, s, a);
-    case 2: return launch_pdl(gemv_kernel<2>, grid, kGemvWarps * 32, s, a);
-    case 3: return launch_pdl(gemv_kernel<3>, grid, kGemvWarps * 32, s, a);
-    default: return launch_pdl(gemv_kernel<4>, grid, kGemvWarps * 32, s, a);
+    case 1: return launch_pdl(gemv_kernel<1, RB>, grid, kGemvWarps * 32, s, a);
+    case 2: return launch_pdl(gemv_kernel<2, RB>, grid, kGemvWarps * 32, s, a);
+    case 3: return launch_pdl(gemv_kernel<3, RB>, grid, kGemvWarps * 32, s, a);
+    default: return launch_pdl(gemv_kernel<4, RB>, grid, kGemvWarps * 32, s, a);
   }
+}
+static int gemv(const GemvArgs& a, int nj, int splits, cudaStream_t s) {
+  return rb_per_warp(a.nrb) == 2 ? gemv_rb<2>(a, nj, splits, s) : gemv_rb<1>(a, nj, splits, s);
 }
 
 }  // namespace batched

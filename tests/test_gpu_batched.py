@@ -1,6 +1,7 @@
 """Token batches of 5-16 (north_star subsystem 2 / BASELINE configs[3]-[4]): every token through the
-decode engine (groups of <= 4 tokens per launch) and through the tcgen05 prefill chain, against the
-float64 oracle on the same bytes (tolerance: max|err|/max|ref| and ||err||/||ref|| <= 1e-2)."""
+decode engine (groups of <= 4 tokens per launch), the single-pass batched kernels and the tcgen05
+prefill chain, against the float64 oracle on the same bytes (tolerance: max|err|/max|ref| and
+||err||/||ref|| <= 1e-2)."""
 
 import numpy as np
 import pytest
@@ -15,7 +16,7 @@ TOL = 1e-2
 
 
 @pytest.mark.parametrize("batch", [5, 8, 16])
-@pytest.mark.parametrize("path", ["engine", "prefill"])
+@pytest.mark.parametrize("path", ["engine", "prefill", "batched"])
 def test_batched_layer_vs_oracle(batch, path):
     import torch
     from paper_2505_11076_b200.plan import DecodePlan, PlanOp
@@ -27,7 +28,7 @@ def test_batched_layer_vs_oracle(batch, path):
     x = torch.randn((batch, m), generator=g, device="cuda").half()
     bufs = [x.clone(), torch.zeros((batch, n), dtype=torch.half, device="cuda")]
     plan = DecodePlan([layer], [PlanOp(0, 0, 1, "down")], bufs, input_buffer=0, output_buffer=1)
-    plan.use_engine() if path == "engine" else plan.use_prefill()
+    {"engine": plan.use_engine, "prefill": plan.use_prefill, "batched": plan.use_batched}[path]()
     plan._eager()
     torch.cuda.synchronize()
     y = bufs[1].double().cpu().numpy()

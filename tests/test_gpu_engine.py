@@ -159,9 +159,10 @@ def test_engine_ragged_layers_vs_oracle(batch, n, k, m, act):
 
 
 def test_use_fastest_keeps_the_faster_path_and_its_numbers():
-    """DecodePlan.use_fastest times the engine (two launches of 4 tokens) against the tcgen05
-    prefill chain on the plan's buffers and keeps the faster; the kept path gives exactly its own
-    numbers, the two paths agree within the fp16 tolerance, and the input buffer is restored."""
+    """DecodePlan.use_fastest times the engine (two launches of 4 tokens), the single-pass batched
+    kernels and the tcgen05 prefill chain on the plan's buffers and keeps the fastest; the kept
+    path gives exactly its own numbers, the paths agree within the fp16 tolerance, and the input
+    buffer is restored."""
     import torch
 
     g = torch.Generator(device="cuda")
@@ -170,14 +171,16 @@ def test_use_fastest_keeps_the_faster_path_and_its_numbers():
     x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
     ref_e = _run(plan.use_engine(), x)
     ref_p = _run(plan.use_prefill(), x)
-    ok, err = _close(ref_e, ref_p)
-    assert ok, err
+    ref_b = _run(plan.use_batched(), x)
+    for other in (ref_p, ref_b):
+        ok, err = _close(ref_e, other)
+        assert ok, err
     plan.buffers[plan.input_buffer].copy_(x)
     plan.use_fastest(steps=2)
-    assert set(plan.choice_ms) == {"engine", "prefill"} and plan.choice in plan.choice_ms
+    assert set(plan.choice_ms) == {"engine", "batched", "prefill"} and plan.choice in plan.choice_ms
     assert torch.equal(plan.buffers[plan.input_buffer], x)
-    assert torch.equal(_run(plan, x), ref_e if plan.choice == "engine" else ref_p)
-    # the static rule wins unless the other path is faster by the margin: a huge margin always
+    assert torch.equal(_run(plan, x), {"engine": ref_e, "prefill": ref_p, "batched": ref_b}[plan.choice])
+    # the static rule wins unless another path is faster by the margin: a huge margin always
     # keeps it, whatever the timings
     plan.use_fastest(steps=2, margin=1.0)
-    assert plan.choice == plan.default_path() == "engine"
+    assert plan.choice == plan.default_path() == "batched"

@@ -156,3 +156,39 @@ def test_batched_plan_raises_on_overflow():
     plan = DecodePlan([layer], [PlanOp(0, 0, 1, "x")], bufs, input_buffer=0, output_buffer=1).use_batched()
     with pytest.raises(P.DbfOverflowError):
         plan.run(bufs[0].cpu())
+
+
+@pytest.mark.parametrize("xdt,sdt", [("float32", "float32"), ("bfloat16", "float16"), ("float16", "float32")])
+def test_batched_dtypes(xdt, sdt):
+    """Activations fp16 / bf16 / fp32 and scales fp16 / fp32: the output is in X's dtype and within
+    the tolerance of the oracle on the same (rounded) values."""
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(21)
+    layer = P.random_device_layer(1000, 1100, 1024, generator=g, keep_words=True, scale_dtype=getattr(torch, sdt))
+    x = torch.randn((7, 1024), generator=g, device="cuda").to(getattr(torch, xdt))
+    y = P.forward_batched(x, layer)
+    assert y.dtype == x.dtype
+    y = y.double().cpu().numpy()
+    ref = _ref(x, layer)
+    for t in range(7):
+        assert rel_max(y[t], ref[t]) <= TOL and rel_norm(y[t], ref[t]) <= TOL, (xdt, sdt, t)
+
+
+def test_batched_matches_engine_numerics_closely():
+    """Same 13-bit chunk grid as the decode engine: at 4 tokens the two paths agree far inside the
+    oracle tolerance (the engine rounds t to fp16, the batched path keeps it fp32)."""
+    import torch
+    from paper_2505_11076_b200.plan import DecodePlan, PlanOp
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(22)
+    layer = P.random_device_layer(4096, 2048, 4096, generator=g)
+    x = torch.randn((4, 4096), generator=g, device="cuda").half()
+    bufs = [x.clone(), torch.zeros((4, 4096), dtype=torch.half, device="cuda")]
+    plan = DecodePlan([layer], [PlanOp(0, 0, 1, "q")], bufs, input_buffer=0, output_buffer=1).use_engine()
+    plan._eager()
+    ye = bufs[1].double().cpu().numpy()
+    yb = P.forward_batched(x, layer).double().cpu().numpy()
+    assert rel_max(yb, ye) <= 2e-3

@@ -387,7 +387,7 @@ inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 // row blocks per warp: two where there are enough rows (the chunk's B fragments, barriers and
 // scale loads then serve twice the MMAs)
-inline int rb_per_warp(int64_t nrb) { return nrb >= 512 ? 2 : 1; }
+inline int rb_per_warp(int64_t nrb) { return nrb >= 128 ? 2 : 1; }
 // K splits of one GEMV: enough CTAs for kCtasPerSm per SM, whole chunks per split
 inline int split_count(int64_t nrb, int64_t nch, int* cps) {
   const int64_t gx = ceil_div(nrb, (int64_t)kGemvWarps * rb_per_warp(nrb));

@@ -361,6 +361,25 @@ int dbf_forward_batched(const void* A_tiled, const void* B_tiled, const void* a,
                         const void* X, int x_dtype, int64_t batch, int64_t ldx, void* Y,
                         int y_dtype, int64_t ldy, void* workspace, size_t workspace_bytes,
                         unsigned* status, void* stream);
+/* The same, split for layer chains (DecodePlan.use_batched): a layer's first-GEMV input as
+ * quantized B fragments (dbf_batched_frag_bytes(m, batch) bytes, made by dbf_batched_quantize from
+ * an activation matrix or by the previous layer's finalize), and up to 4 "consumers" -- layers
+ * that read this layer's output Y next -- whose fragments the finalize writes from Y exactly as
+ * stored (times each consumer's input scale b): bitwise what dbf_batched_quantize would make from
+ * Y, one kernel and one read of Y fewer per layer.  Consumer fragment buffers hold n columns. */
+typedef struct {
+  const void* b; /* the consumer layer's per-column input scale (scale_dtype), or NULL */
+  void* frag;    /* its fragment buffer: dbf_batched_frag_bytes(n, batch) bytes */
+} dbf_batched_consumer;
+size_t dbf_batched_frag_bytes(int64_t cols, int64_t batch);
+int dbf_batched_quantize(const void* X, int x_dtype, int64_t ldx, int64_t batch, int64_t cols,
+                         const void* iscale, int scale_dtype, void* frag, void* stream);
+size_t dbf_forward_batched_frag_workspace_bytes(int64_t n, int64_t k, int64_t m, int64_t batch);
+int dbf_forward_batched_frag(const void* A_tiled, const void* B_tiled, const void* a,
+                             const void* mid, int scale_dtype, int64_t n, int64_t k, int64_t m,
+                             const void* frag_in, int64_t batch, void* Y, int y_dtype, int64_t ldy,
+                             const dbf_batched_consumer* consumers, int nconsumers, void* workspace,
+                             size_t workspace_bytes, unsigned* status, void* stream);
 
 /* ---- prefill / batched path: tcgen05 + TMEM sign GEMMs (>= 64 tokens) ------------------ */
 /*

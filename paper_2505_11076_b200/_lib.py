@@ -47,6 +47,13 @@ SIGNATURES: dict[str, tuple] = {
     "dbf_sign_gemm_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp]),
     "dbf_forward_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "dbf_forward_batched_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
+    "dbf_batched_frag_bytes": (_sz, [_i64, _i64]),
+    "dbf_batched_quantize": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _int, _vp, _vp]),
+    "dbf_forward_batched_frag_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
+    "dbf_forward_batched_frag": (
+        _int,
+        [_vp, _vp, _vp, _vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _int, _i64, _vp, _int, _vp, _sz, _vp, _vp],
+    ),
     "dbf_forward_batched": (
         _int,
         [_vp, _vp, _vp, _vp, _vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _i64, _vp, _int, _i64, _vp, _sz, _vp, _vp],

@@ -94,9 +94,87 @@ struct QuantIn {
   int cols, batch, tpad;
 };
 
+// Fragment buffer of one GEMV input (cols columns, tpad token slots): B fragments, then F, then T
+struct FragView {
+  uint2* bfrag;
+  int* F;
+  int* T;
+};
+inline size_t frag_bfrag_bytes(int64_t cols, int tpad) { return (size_t)chunks(cols) * 8 * (tpad / 4) * 32 * 8; }
+inline size_t frag_bytes(int64_t cols, int tpad) {
+  return ((frag_bfrag_bytes(cols, tpad) + 2 * (size_t)chunks(cols) * tpad * 4) + 255) & ~(size_t)255;
+}
+__host__ __device__ inline FragView frag_view(void* base, int64_t cols, int tpad) {
+  FragView v;
+  v.bfrag = (uint2*)base;
+  const size_t fb = (size_t)((cols + kChunkCols - 1) / kChunkCols) * 8 * (tpad / 4) * 32 * 8;
+  v.F = (int*)((char*)base + fb);
+  v.T = v.F + (size_t)((cols + kChunkCols - 1) / kChunkCols) * tpad;
+  return v;
+}
+
+// Padding token t of chunk c: zero digits, F = T = 0 (its outputs are never stored)
+__device__ __forceinline__ void zero_chunk(int c, int t, const FragView& fv, int tpad, int nj) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* bf = reinterpret_cast<uint8_t*>(fv.bfrag);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = lane + 32 * h, kb = q >> 3, tig = q & 3, half = (q >> 2) & 1;
+    uint8_t* base = bf + ((((size_t)c * 8 + kb) * nj + (t >> 2)) * 32 + 8 * (t & 3)) * 8 + 4 * half + tig * 8;
+    *(uint32_t*)(base + 0) = 0u;
+    *(uint32_t*)(base + 32) = 0u;
+  }
+  if (lane == 0) fv.F[c * tpad + t] = 0, fv.T[c * tpad + t] = 0;
+}
+
+// Chunk c of token t (this lane: columns 4 (lane + 32 h) + e of the chunk, u already scaled) ->
+// the 13-bit grid, two balanced digit planes in the B-fragment layout, F and T = sum X.
+__device__ __forceinline__ void emit_chunk(const float (&u)[2][4], int c, int t, const FragView& fv, int tpad,
+                                           int nj) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* bf = reinterpret_cast<uint8_t*>(fv.bfrag);
+  float mx = 0.f;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mx = fmax_nan(mx, fabsf(u[h][e]));
+  const uint32_t mxb = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+  int F = 0;
+  float scale = 0.f;
+  if (mxb >= 0x7F800000u) {
+    F = kBadF;  // inf / NaN in the chunk: zero digits, NaN outputs
+  } else {
+    if (mxb != 0u) {
+      const int ex = (int)(mxb >> 23) - 126;  // mx in [2^(ex-1), 2^ex)
+      F = 12 - ex;
+      F = F > 125 ? 125 : (F < -125 ? -125 : F);
+    }
+    scale = __int_as_float((F + 127) << 23) * kQScale;
+  }
+  int ts = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = lane + 32 * h, kb = q >> 3, tig = q & 3, half = (q >> 2) & 1;
+    const int sh = 3 - (kb & 3);  // Y = X * 2^(3-t): the A bytes are 2^t * bit for k-block 4s + t
+    uint32_t v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int X = __float_as_int(fmaf(u[h][e], scale, 12582912.f)) - 0x4B400000;  // rint, |X| <= 4079
+      ts += X;
+      v[e] = (uint32_t)((X << sh) + 0x8080);  // bytes 0, 1 = balanced digits + 128
+    }
+    const uint32_t lo = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+    const uint32_t hi = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
+    uint8_t* base = bf + ((((size_t)c * 8 + kb) * nj + (t >> 2)) * 32 + 8 * (t & 3)) * 8 + 4 * half + tig * 8;
+    *(uint32_t*)(base + 0) = lo ^ 0x80808080u;   // plane 0: MMA column 2 * (t % 4)
+    *(uint32_t*)(base + 32) = hi ^ 0x80808080u;  // plane 1: MMA column 2 * (t % 4) + 1
+  }
+  ts = __reduce_add_sync(0xffffffffu, ts);
+  if (lane == 0) fv.F[c * tpad + t] = F, fv.T[c * tpad + t] = ts;
+}
+
 // One warp per (chunk, token): 64 groups of 4 columns, lane holds groups lane and lane + 32.
-__global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, uint2* __restrict__ bfrag,
-                                                            int* __restrict__ Fo, int* __restrict__ To, int nj) {
+__global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, FragView fv, int nj) {
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int nch = (in.cols + kChunkCols - 1) / kChunkCols;
@@ -104,16 +182,8 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, uint2* _
   grid_launch_dependents();
   if (item >= nch * in.tpad) return;
   const int c = item / in.tpad, t = item % in.tpad;
-  uint8_t* bf = reinterpret_cast<uint8_t*>(bfrag);
-  if (t >= in.batch) {  // padding token: zero digits, F = T = 0 (its outputs are never stored)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = lane + 32 * h, kb = q >> 3, tig = q & 3, half = (q >> 2) & 1;
-      uint8_t* base = bf + ((((size_t)c * 8 + kb) * nj + (t >> 2)) * 32 + 8 * (t & 3)) * 8 + 4 * half + tig * 8;
-      *(uint32_t*)(base + 0) = 0u;
-      *(uint32_t*)(base + 32) = 0u;
-    }
-    if (lane == 0) Fo[c * in.tpad + t] = 0, To[c * in.tpad + t] = 0;
+  if (t >= in.batch) {
+    zero_chunk(c, t, fv, in.tpad, nj);
     return;
   }
   float u[2][4];
@@ -170,44 +240,7 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, uint2* _
 #pragma unroll
     for (int e = 0; e < 4; ++e) u[h][e] *= sc[e];
   }
-  float mx = 0.f;
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) mx = fmax_nan(mx, fabsf(u[h][e]));
-  const uint32_t mxb = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
-  int F = 0;
-  float scale = 0.f;
-  if (mxb >= 0x7F800000u) {
-    F = kBadF;  // inf / NaN in the chunk: zero digits, NaN outputs
-  } else {
-    if (mxb != 0u) {
-      const int ex = (int)(mxb >> 23) - 126;  // mx in [2^(ex-1), 2^ex)
-      F = 12 - ex;
-      F = F > 125 ? 125 : (F < -125 ? -125 : F);
-    }
-    scale = __int_as_float((F + 127) << 23) * kQScale;
-  }
-  int ts = 0;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int q = lane + 32 * h, kb = q >> 3, tig = q & 3, half = (q >> 2) & 1;
-    const int sh = 3 - (kb & 3);  // Y = X * 2^(3-t): the A bytes are 2^t * bit for k-block 4s + t
-    uint32_t v[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int X = __float_as_int(fmaf(u[h][e], scale, 12582912.f)) - 0x4B400000;  // rint, |X| <= 4079
-      ts += X;
-      v[e] = (uint32_t)((X << sh) + 0x8080);  // bytes 0, 1 = balanced digits + 128
-    }
-    const uint32_t lo = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
-    const uint32_t hi = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
-    uint8_t* base = bf + ((((size_t)c * 8 + kb) * nj + (t >> 2)) * 32 + 8 * (t & 3)) * 8 + 4 * half + tig * 8;
-    *(uint32_t*)(base + 0) = lo ^ 0x80808080u;   // plane 0: MMA column 2 * (t % 4)
-    *(uint32_t*)(base + 32) = hi ^ 0x80808080u;  // plane 1: MMA column 2 * (t % 4) + 1
-  }
-  ts = __reduce_add_sync(0xffffffffu, ts);
-  if (lane == 0) Fo[c * in.tpad + t] = F, To[c * in.tpad + t] = ts;
+  emit_chunk(u, c, t, fv, in.tpad, nj);
 }
 
 struct GemvArgs {
@@ -349,35 +382,160 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
   }
 }
 
-// y[t][r] = oscale[r] * sum_s part[s][t][r]  (split order), rounded to the output dtype; status
-// bits: 1 = a non-finite value, 2 = a finite value beyond the fp16 range (fp16 output)
-__global__ void finalize_kernel(const float* __restrict__ part, int splits, int64_t part_stride, int ldp, int rows,
-                                int batch, const void* oscale, int scale_dtype, void* y, int y_dtype, int64_t ldy,
-                                unsigned* status) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const float sc = (oscale && i < (int64_t)batch * rows) ? load_f(oscale, scale_dtype, i % rows) : 1.f;
+// Layers that read this layer's output next (DecodePlan chains): each gets its first-GEMV B
+// fragments straight from the finalize, from the output exactly as rounded to the output dtype and
+// times its own input scale b -- bitwise what quantize_kernel would make from the stored output.
+constexpr int kMaxConsumers = 4;
+struct Consumer {
+  const void* b;  // the consumer's per-column input scale (scale_dtype) or null
+  FragView fv;
+};
+struct FinArgs {
+  const float* part;  // part[s][tpad][ldp]
+  int splits;
+  int64_t part_stride;
+  int ldp, rows, batch, tpad, nj;
+  const void* oscale;
+  int scale_dtype;
+  void* y;
+  int y_dtype;
+  int64_t ldy;
+  unsigned* status;
+  int ncons;
+  Consumer cons[kMaxConsumers];
+};
+
+// 4 consecutive scale values (fp16 pairs loaded as one 8-byte word where aligned)
+__device__ __forceinline__ void load_scale4(const void* p, int dt, int j0, float (&sc)[4]) {
+  if (dt == DBF_F16 && (j0 & 3) == 0) {
+    const uint2 r = __ldg((const uint2*)((const __half*)p + j0));
+    const float2 lo = __half22float2(*(const __half2*)&r.x), hi = __half22float2(*(const __half2*)&r.y);
+    sc[0] = lo.x, sc[1] = lo.y, sc[2] = hi.x, sc[3] = hi.y;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sc[e] = load_f(p, dt, j0 + e);
+  }
+}
+
+// One warp per (256-row chunk, token, consumer): y = oscale (.) sum of the splits (split order),
+// rounded to the output dtype; the consumer-0 warp stores it and reports status bits 1 (a
+// non-finite value) and 2 (a finite value beyond the fp16 range, fp16 output); every warp then
+// writes its consumer's B fragments of the chunk (one warp per consumer: the chunk's rounding is
+// recomputed, not shared, so the consumers run side by side).
+__global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs f) {
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int nch = (f.rows + kChunkCols - 1) / kChunkCols, ncw = f.ncons > 0 ? f.ncons : 1;
   grid_wait();
   grid_launch_dependents();
-  if (i >= (int64_t)batch * rows) return;
-  const int t = (int)(i / rows), r = (int)(i % rows);
-  float v = 0.f;
-#pragma unroll 4
-  for (int s = 0; s < splits; ++s) v += __ldcg(part + (size_t)s * part_stride + (size_t)t * ldp + r);
-  v *= sc;
-  const int64_t o = (int64_t)t * ldy + r;
-  unsigned bad = isfinite(v) ? 0u : (unsigned)kStatusNonFinite;
-  switch (y_dtype) {
-    case DBF_F16: {
-      const __half h = __float2half_rn(v);
-      if (!bad && __hisinf(h)) bad = kStatusOverflow;
-      ((__half*)y)[o] = h;
-      break;
-    }
-    case DBF_F32: ((float*)y)[o] = v; break;
-    case DBF_F64: ((double*)y)[o] = (double)v; break;
-    default: ((__nv_bfloat16*)y)[o] = __float2bfloat16_rn(v); break;
+  if (item >= nch * f.tpad * ncw) return;
+  const int k = item % ncw, ct = item / ncw, c = ct / f.tpad, t = ct % f.tpad;
+  if (t >= f.batch) {
+    if (f.ncons > 0) zero_chunk(c, t, f.cons[k].fv, f.tpad, f.nj);
+    return;
   }
-  if (bad && status) atomicOr(status, bad);
+  const bool store = k == 0;
+  float yr[2][4];  // the output as stored (what a later reader of y sees), 0 past the rows
+  unsigned bad = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j0 = c * kChunkCols + 4 * (lane + 32 * h);
+    float v[4] = {0.f, 0.f, 0.f, 0.f}, sc[4] = {1.f, 1.f, 1.f, 1.f};
+    const bool full = j0 + 3 < f.rows;
+    if (full) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+      for (int s = 0; s < f.splits; ++s) {
+        const float4 p = __ldcg((const float4*)(f.part + (size_t)s * f.part_stride + (size_t)t * f.ldp + j0));
+        a.x += p.x, a.y += p.y, a.z += p.z, a.w += p.w;
+      }
+      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+      if (f.oscale) load_scale4(f.oscale, f.scale_dtype, j0, sc);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (j0 + e < f.rows) {
+          for (int s = 0; s < f.splits; ++s) v[e] += __ldcg(f.part + (size_t)s * f.part_stride + (size_t)t * f.ldp + j0 + e);
+          if (f.oscale) sc[e] = load_f(f.oscale, f.scale_dtype, j0 + e);
+        }
+    }
+    float w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      w[e] = v[e] * sc[e];
+      if (j0 + e < f.rows && !isfinite(w[e])) bad |= kStatusNonFinite;
+    }
+    const int64_t o = (int64_t)t * f.ldy + j0;
+    if (f.y_dtype == DBF_F16) {
+      __half hv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        hv[e] = __float2half_rn(w[e]);
+        if (j0 + e < f.rows && isfinite(w[e]) && __hisinf(hv[e])) bad |= kStatusOverflow;
+        yr[h][e] = j0 + e < f.rows ? __half2float(hv[e]) : 0.f;
+      }
+      if (store) {
+        __half* yp = (__half*)f.y + o;
+        if (full && ((uintptr_t)yp & 7) == 0) {
+          uint2 pk;
+          pk.x = (uint32_t)__half_as_ushort(hv[0]) | ((uint32_t)__half_as_ushort(hv[1]) << 16);
+          pk.y = (uint32_t)__half_as_ushort(hv[2]) | ((uint32_t)__half_as_ushort(hv[3]) << 16);
+          *(uint2*)yp = pk;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (j0 + e < f.rows) yp[e] = hv[e];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = j0 + e;
+        yr[h][e] = 0.f;
+        if (j >= f.rows) continue;
+        switch (f.y_dtype) {
+          case DBF_F32:
+            if (store) ((float*)f.y)[o + e] = w[e];
+            yr[h][e] = w[e];
+            break;
+          case DBF_F64:
+            if (store) ((double*)f.y)[o + e] = (double)w[e];
+            yr[h][e] = w[e];
+            break;
+          default: {
+            const __nv_bfloat16 bv = __float2bfloat16_rn(w[e]);
+            if (store) ((__nv_bfloat16*)f.y)[o + e] = bv;
+            yr[h][e] = __bfloat162float(bv);
+            break;
+          }
+        }
+      }
+    }
+  }
+  if (store) {
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && lane == 0 && f.status) atomicOr(f.status, bad);
+  }
+  if (f.ncons == 0) return;
+  const Consumer& cs = f.cons[k];
+  float u[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j0 = c * kChunkCols + 4 * (lane + 32 * h);
+    float sc[4] = {1.f, 1.f, 1.f, 1.f};
+    if (cs.b) {
+      if (j0 + 3 < f.rows) {
+        load_scale4(cs.b, f.scale_dtype, j0, sc);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (j0 + e < f.rows) sc[e] = load_f(cs.b, f.scale_dtype, j0 + e);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) u[h][e] = yr[h][e] * sc[e];
+  }
+  emit_chunk(u, c, t, cs.fv, f.tpad, f.nj);
 }
 
 // ---- host side ---------------------------------------------------------------------------------
@@ -398,21 +556,22 @@ inline int split_count(int64_t nrb, int64_t nch, int* cps) {
   return (int)ceil_div(nch, c);
 }
 
+// Workspace of one layer: the second GEMV's input fragments, both partial sets, and (for
+// dbf_forward_batched, which quantizes x itself) the first GEMV's input fragments
 struct Layout {
-  size_t bfrag, fo, to, part, total;
+  size_t frag2, part, frag1, total_frag, total;
 };
 inline Layout layout_of(int64_t n, int64_t k, int64_t m, int64_t batch) {
-  const int tpad = tpad_of(batch), nj = tpad / 4;
-  const int64_t nchmax = std::max(chunks(m), chunks(k));
+  const int tpad = tpad_of(batch);
   int cps;
   const int S1 = split_count(row_blocks(k), chunks(m), &cps), S2 = split_count(row_blocks(n), chunks(k), &cps);
   Layout L;
-  L.bfrag = 0;
-  L.fo = align256(L.bfrag + (size_t)nchmax * 8 * nj * 32 * 8);
-  L.to = align256(L.fo + (size_t)nchmax * tpad * 4);
-  L.part = align256(L.to + (size_t)nchmax * tpad * 4);
+  L.frag2 = 0;
+  L.part = align256(L.frag2 + frag_bytes(k, tpad));
   // stage-1 partials stay live while stage 2 quantizes from them: both sets side by side
-  L.total = align256(L.part + ((size_t)S1 * tpad * ldp_of(k) + (size_t)S2 * tpad * ldp_of(n)) * 4 + 256);
+  L.total_frag = align256(L.part + ((size_t)S1 * tpad * ldp_of(k) + (size_t)S2 * tpad * ldp_of(n)) * 4 + 256);
+  L.frag1 = L.total_frag;
+  L.total = align256(L.frag1 + frag_bytes(m, tpad));
   return L;
 }
 
@@ -459,6 +618,82 @@ size_t dbf_forward_batched_workspace_bytes(int64_t n, int64_t k, int64_t m, int6
   return batched::layout_of(n, k, m, batch).total;
 }
 
+size_t dbf_batched_frag_bytes(int64_t cols, int64_t batch) {
+  if (cols < 1 || batch < 1 || batch > batched::kMaxTokens) return 0;
+  return batched::frag_bytes(cols, batched::tpad_of(batch));
+}
+
+int dbf_batched_quantize(const void* X, int x_dtype, int64_t ldx, int64_t batch, int64_t cols, const void* iscale,
+                         int scale_dtype, void* frag, void* stream) {
+  using namespace batched;
+  if (!X || !frag || batch < 1 || cols < 1) return DBF_ERR_INVALID_ARGUMENT;
+  if (batch > kMaxTokens || cols > INT32_MAX / 2) return DBF_ERR_UNSUPPORTED;
+  if (ldx < cols) return DBF_ERR_SHAPE;
+  if (!valid_float_dtype(x_dtype) || !valid_float_dtype(scale_dtype)) return DBF_ERR_INVALID_ARGUMENT;
+  const int tpad = tpad_of(batch);
+  QuantIn q{};
+  q.x = X, q.x_dtype = x_dtype, q.ldx = ldx, q.iscale = iscale, q.scale_dtype = scale_dtype;
+  q.cols = (int)cols, q.batch = (int)batch, q.tpad = tpad;
+  return launch_pdl(quantize_kernel, dim3((unsigned)ceil_div(chunks(cols) * tpad, kWarps)), kThreads,
+                    (cudaStream_t)stream, q, frag_view(frag, cols, tpad), tpad / 4);
+}
+
+size_t dbf_forward_batched_frag_workspace_bytes(int64_t n, int64_t k, int64_t m, int64_t batch) {
+  if (n < 1 || k < 1 || m < 1 || batch < 1 || batch > batched::kMaxTokens) return 0;
+  return batched::layout_of(n, k, m, batch).total_frag;
+}
+
+int dbf_forward_batched_frag(const void* A_tiled, const void* B_tiled, const void* a, const void* mid,
+                             int scale_dtype, int64_t n, int64_t k, int64_t m, const void* frag_in, int64_t batch,
+                             void* Y, int y_dtype, int64_t ldy, const dbf_batched_consumer* consumers,
+                             int nconsumers, void* workspace, size_t workspace_bytes, unsigned* status,
+                             void* stream) {
+  using namespace batched;
+  if (!A_tiled || !B_tiled || !frag_in || !Y) return DBF_ERR_INVALID_ARGUMENT;
+  if (n < 1 || k < 1 || m < 1 || batch < 1 || nconsumers < 0) return DBF_ERR_INVALID_ARGUMENT;
+  if (nconsumers > 0 && !consumers) return DBF_ERR_INVALID_ARGUMENT;
+  if (batch > kMaxTokens || nconsumers > kMaxConsumers) return DBF_ERR_UNSUPPORTED;
+  if (n > INT32_MAX / 2 || k > INT32_MAX / 2 || m > INT32_MAX / 2) return DBF_ERR_UNSUPPORTED;
+  if (ldy < n) return DBF_ERR_SHAPE;
+  if (!valid_float_dtype(y_dtype) || !valid_float_dtype(scale_dtype)) return DBF_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < nconsumers; ++i)
+    if (!consumers[i].frag) return DBF_ERR_INVALID_ARGUMENT;
+  const Layout L = layout_of(n, k, m, batch);
+  if (!workspace || workspace_bytes < L.total_frag) return DBF_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  const int tpad = tpad_of(batch), nj = tpad / 4;
+  int cps1, cps2;
+  const int S1 = split_count(row_blocks(k), chunks(m), &cps1), S2 = split_count(row_blocks(n), chunks(k), &cps2);
+  const int ldk = ldp_of(k), ldn = ldp_of(n);
+  float* part1 = (float*)(ws + L.part);
+  float* part2 = part1 + (size_t)S1 * tpad * ldk;
+  const FragView f1 = frag_view(const_cast<void*>(frag_in), m, tpad), f2 = frag_view(ws + L.frag2, k, tpad);
+
+  // t = mid * (B . (x * b))
+  GemvArgs g1{(const uint4*)B_tiled, (int)k, (int)row_blocks(k), (int)chunks(m), cps1, f1.bfrag, f1.F, f1.T, tpad,
+              (int)batch, part1, ldk};
+  int st = gemv(g1, nj, S1, s);
+  if (st != DBF_OK) return st;
+  // t quantized straight from the stage-1 partials
+  QuantIn q2{};
+  q2.part = part1, q2.splits = S1, q2.ldx = ldk, q2.part_stride = (int64_t)tpad * ldk, q2.pscale = mid;
+  q2.scale_dtype = scale_dtype, q2.cols = (int)k, q2.batch = (int)batch, q2.tpad = tpad;
+  st = launch_pdl(quantize_kernel, dim3((unsigned)ceil_div(chunks(k) * tpad, kWarps)), kThreads, s, q2, f2, nj);
+  if (st != DBF_OK) return st;
+  // y = a * (A . t)
+  GemvArgs g2{(const uint4*)A_tiled, (int)n, (int)row_blocks(n), (int)chunks(k), cps2, f2.bfrag, f2.F, f2.T, tpad,
+              (int)batch, part2, ldn};
+  if ((st = gemv(g2, nj, S2, s)) != DBF_OK) return st;
+  FinArgs fa{};
+  fa.part = part2, fa.splits = S2, fa.part_stride = (int64_t)tpad * ldn, fa.ldp = ldn, fa.rows = (int)n;
+  fa.batch = (int)batch, fa.tpad = tpad, fa.nj = nj, fa.oscale = a, fa.scale_dtype = scale_dtype;
+  fa.y = Y, fa.y_dtype = y_dtype, fa.ldy = ldy, fa.status = status, fa.ncons = nconsumers;
+  for (int i = 0; i < nconsumers; ++i) fa.cons[i] = Consumer{consumers[i].b, frag_view(consumers[i].frag, n, tpad)};
+  return launch_pdl(finalize_kernel, dim3((unsigned)ceil_div(chunks(n) * tpad * std::max(1, nconsumers), kWarps)),
+                    kThreads, s, fa);
+}
+
 int dbf_forward_batched(const void* A_tiled, const void* B_tiled, const void* a, const void* mid, const void* b,
                         int scale_dtype, int64_t n, int64_t k, int64_t m, const void* X, int x_dtype, int64_t batch,
                         int64_t ldx, void* Y, int y_dtype, int64_t ldy, void* workspace, size_t workspace_bytes,
@@ -469,45 +704,13 @@ int dbf_forward_batched(const void* A_tiled, const void* B_tiled, const void* a,
   if (batch > kMaxTokens) return DBF_ERR_UNSUPPORTED;
   if (n > INT32_MAX / 2 || k > INT32_MAX / 2 || m > INT32_MAX / 2) return DBF_ERR_UNSUPPORTED;
   if (ldx < m || ldy < n) return DBF_ERR_SHAPE;
-  if (!valid_float_dtype(x_dtype) || !valid_float_dtype(y_dtype) || !valid_float_dtype(scale_dtype))
-    return DBF_ERR_INVALID_ARGUMENT;
   const Layout L = layout_of(n, k, m, batch);
   if (!workspace || workspace_bytes < L.total) return DBF_ERR_WORKSPACE;
-  cudaStream_t s = (cudaStream_t)stream;
-  char* ws = (char*)workspace;
-  uint2* bfrag = (uint2*)(ws + L.bfrag);
-  int* Fo = (int*)(ws + L.fo);
-  int* To = (int*)(ws + L.to);
-  const int tpad = tpad_of(batch), nj = tpad / 4;
-  int cps1, cps2;
-  const int S1 = split_count(row_blocks(k), chunks(m), &cps1), S2 = split_count(row_blocks(n), chunks(k), &cps2);
-  const int ldk = ldp_of(k), ldn = ldp_of(n);
-  float* part1 = (float*)(ws + L.part);
-  float* part2 = part1 + (size_t)S1 * tpad * ldk;
-
-  // stage 1: t = mid * (B . (x * b))
-  QuantIn q{};
-  q.x = X, q.x_dtype = x_dtype, q.ldx = ldx, q.iscale = b, q.scale_dtype = scale_dtype;
-  q.cols = (int)m, q.batch = (int)batch, q.tpad = tpad;
-  int st = launch_pdl(quantize_kernel, dim3((unsigned)ceil_div(chunks(m) * tpad, kWarps)), kThreads, s, q, bfrag,
-                      Fo, To, nj);
+  void* frag1 = (char*)workspace + L.frag1;
+  const int st = dbf_batched_quantize(X, x_dtype, ldx, batch, m, b, scale_dtype, frag1, stream);
   if (st != DBF_OK) return st;
-  GemvArgs g1{(const uint4*)B_tiled, (int)k, (int)row_blocks(k), (int)chunks(m), cps1, bfrag, Fo, To, tpad,
-              (int)batch, part1, ldk};
-  if ((st = gemv(g1, nj, S1, s)) != DBF_OK) return st;
-  // stage 2: y = a * (A . t), t quantized straight from the stage-1 partials
-  QuantIn q2{};
-  q2.part = part1, q2.splits = S1, q2.ldx = ldk, q2.part_stride = (int64_t)tpad * ldk, q2.pscale = mid;
-  q2.scale_dtype = scale_dtype, q2.cols = (int)k, q2.batch = (int)batch, q2.tpad = tpad;
-  st = launch_pdl(quantize_kernel, dim3((unsigned)ceil_div(chunks(k) * tpad, kWarps)), kThreads, s, q2, bfrag, Fo,
-                  To, nj);
-  if (st != DBF_OK) return st;
-  GemvArgs g2{(const uint4*)A_tiled, (int)n, (int)row_blocks(n), (int)chunks(k), cps2, bfrag, Fo, To, tpad,
-              (int)batch, part2, ldn};
-  if ((st = gemv(g2, nj, S2, s)) != DBF_OK) return st;
-  const int64_t total = batch * n;
-  return launch_pdl(finalize_kernel, dim3((unsigned)ceil_div(total, 256)), 256, s, (const float*)part2, S2,
-                    (int64_t)tpad * ldn, ldn, (int)n, (int)batch, a, scale_dtype, Y, y_dtype, ldy, status);
+  return dbf_forward_batched_frag(A_tiled, B_tiled, a, mid, scale_dtype, n, k, m, frag1, batch, Y, y_dtype, ldy,
+                                  nullptr, 0, workspace, L.total_frag, status, stream);
 }
 
 }  // extern "C"

@@ -13,6 +13,7 @@ relative, well inside the reference's own 1e-5 / 1e-4 tolerances (test_kernel.py
 
 from __future__ import annotations
 
+import ctypes
 import time
 import weakref
 from dataclasses import dataclass
@@ -168,6 +169,54 @@ def forward_batched(X, layer: DeviceLayer, out=None, status=None):
         "dbf_forward_batched",
     )
     return Y
+
+
+class _BatchedConsumer(ctypes.Structure):
+    """dbf_batched_consumer (include/dbf_b200.h)."""
+    _fields_ = [("b", ctypes.c_void_p), ("frag", ctypes.c_void_p)]
+
+
+def batched_frag(cols: int, batch: int, device):
+    """A fragment buffer: one layer's first-GEMV input (cols columns, batch tokens) as quantized
+    B fragments (dbf_batched_frag_bytes)."""
+    import torch
+
+    return torch.empty(int(_lib.lib.dbf_batched_frag_bytes(cols, batch)), dtype=torch.uint8, device=device)
+
+
+def batched_quantize(X, layer: DeviceLayer, frag):
+    """X (batch x m) times the layer's input scale b -> its first-GEMV fragments (dbf_batched_quantize)."""
+    _lib.check(
+        _lib.lib.dbf_batched_quantize(X.data_ptr(), _lib.dtype_code(X.dtype), X.stride(0), X.shape[0], layer.m_dim,
+                                      layer.b.data_ptr(), _lib.dtype_code(layer.b.dtype), frag.data_ptr(),
+                                      _lib.stream_ptr()),
+        "dbf_batched_quantize",
+    )
+
+
+def forward_batched_frag(frag, layer: DeviceLayer, batch: int, out, consumers=(), status=None):
+    """forward_batched from a pre-quantized input (``frag``, from batched_quantize or a previous
+    layer's finalize) into ``out`` (batch x n); ``consumers`` = [(layer_c, frag_c), ...] (<= 4):
+    layers reading ``out`` next, whose fragments this call's finalize writes (dbf_forward_batched_frag)."""
+    if len(consumers) > 4:
+        raise ValueError("at most 4 consumers per layer")
+    arr = (_BatchedConsumer * max(1, len(consumers)))()
+    for i, (lc, fc) in enumerate(consumers):
+        arr[i].b = lc.b.data_ptr()
+        arr[i].frag = fc.data_ptr()
+    ws = _workspace(_lib.lib.dbf_forward_batched_frag_workspace_bytes(layer.n, layer.k, layer.m_dim, batch),
+                    out.device)
+    _lib.check(
+        _lib.lib.dbf_forward_batched_frag(
+            layer.A.tiled.data_ptr(), layer.B.tiled.data_ptr(), layer.a.data_ptr(), layer.mid.data_ptr(),
+            _lib.dtype_code(layer.a.dtype), layer.n, layer.k, layer.m_dim, frag.data_ptr(), batch,
+            out.data_ptr(), _lib.dtype_code(out.dtype), out.stride(0), ctypes.cast(arr, ctypes.c_void_p),
+            len(consumers), ws.data_ptr(), ws.numel(), status.data_ptr() if status is not None else None,
+            _lib.stream_ptr(),
+        ),
+        "dbf_forward_batched_frag",
+    )
+    return out
 
 
 def forward_device(X, layer: DeviceLayer, out=None, out_dtype=None):

@@ -19,7 +19,8 @@ from dataclasses import dataclass, field
 from . import _lib
 from .budget import middle_dim
 from .device import DeviceLayer
-from .kernel import BATCHED_MAX_TOKENS, forward_batched, forward_device, forward_prefill, random_device_layer
+from .kernel import (BATCHED_MAX_TOKENS, batched_frag, batched_quantize, forward_batched_frag, forward_device,
+                     forward_prefill, random_device_layer)
 
 # Llama-2 linear shapes (n = out_features, m = in_features), SURVEY.md §8a
 LLAMA_SHAPES = {
@@ -106,8 +107,25 @@ class DecodePlan:
         self._mode = "batched"
         if getattr(self, "_bstatus", None) is None:
             self._bstatus = torch.zeros(1, dtype=torch.int32, device=self.buffers[0].device)
+        self._bchain = self._batched_chain(batch)
         self._graph = None
         return self
+
+    def _batched_chain(self, batch: int):
+        """Dataflow of the batched chain: every op's input fragments are written by the finalize
+        of the op that last wrote its input buffer (up to 4 readers per writer), or -- for inputs
+        from outside the plan, or a fifth reader -- quantized on their own just before the op."""
+        device = self.buffers[0].device
+        last_writer, readers, standalone = {}, {i: [] for i in range(len(self.ops))}, set()
+        for i, op in enumerate(self.ops):
+            w = last_writer.get(op.src)
+            if w is None or len(readers[w]) >= 4:
+                standalone.add(i)
+            else:
+                readers[w].append(i)
+            last_writer[op.dst] = i
+        frags = [batched_frag(self.layers[op.layer].m_dim, batch, device) for op in self.ops]
+        return frags, readers, standalone
 
     def use_prefill(self):
         """Run every layer through the tcgen05 sign GEMMs (forward_prefill) whatever the batch:
@@ -182,9 +200,15 @@ class DecodePlan:
             return
         mode = getattr(self, "_mode", "layer")
         if mode == "batched":
-            for op in self.ops:
-                forward_batched(self.buffers[op.src], self.layers[op.layer], out=self.buffers[op.dst],
-                                status=self._bstatus)
+            frags, readers, standalone = self._bchain
+            batch = int(self.buffers[self.input_buffer].shape[0])
+            for i, op in enumerate(self.ops):
+                layer = self.layers[op.layer]
+                if i in standalone:
+                    batched_quantize(self.buffers[op.src], layer, frags[i])
+                cons = [(self.layers[self.ops[j].layer], frags[j]) for j in readers[i]]
+                forward_batched_frag(frags[i], layer, batch, self.buffers[op.dst], consumers=cons,
+                                     status=self._bstatus)
             return
         run = forward_prefill if mode == "prefill" else forward_device
         for op in self.ops:

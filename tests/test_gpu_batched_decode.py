@@ -192,3 +192,29 @@ def test_batched_matches_engine_numerics_closely():
     ye = bufs[1].double().cpu().numpy()
     yb = P.forward_batched(x, layer).double().cpu().numpy()
     assert rel_max(yb, ye) <= 2e-3
+
+
+def test_batched_chain_bitwise_equals_per_layer_calls():
+    """DecodePlan.use_batched chains the layers: each finalize writes the next readers' input
+    fragments from its stored output.  That must be bitwise what per-layer forward_batched calls
+    (quantizing each stored input on its own) give -- including the 70B dataflow where o reads q
+    and h feeds three readers."""
+    import torch
+    from paper_2505_11076_b200.plan import llama_decode_plan
+
+    for model, batch in (("llama2-7b", 6), ("llama2-70b", 9)):
+        g = torch.Generator(device="cuda")
+        g.manual_seed(90 + batch)
+        plan = llama_decode_plan(model, bpw=2.0, batch=batch, blocks=1, generator=g)
+        x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
+        plan.use_batched()
+        plan.buffers[plan.input_buffer].copy_(x)
+        plan._eager()
+        torch.cuda.synchronize()
+        chained = [b.clone() for b in plan.buffers]
+        plan.buffers[plan.input_buffer].copy_(x)
+        for op in plan.ops:
+            P.forward_batched(plan.buffers[op.src], plan.layers[op.layer], out=plan.buffers[op.dst])
+        torch.cuda.synchronize()
+        for i, (a, b) in enumerate(zip(chained, plan.buffers)):
+            assert torch.equal(a, b), (model, i)

@@ -125,7 +125,23 @@ class DecodePlan:
                 readers[w].append(i)
             last_writer[op.dst] = i
         frags = [batched_frag(self.layers[op.layer].m_dim, batch, device) for op in self.ops]
-        return frags, readers, standalone
+        # dependencies for concurrent streams: the op that produced the input (its fragments), the
+        # previous writer of the output buffer, and every op that read the output buffer's
+        # previous contents (standalone readers read it; chained ones are ordered conservatively)
+        deps, last_w, reads_since = [], {}, {}
+        for i, op in enumerate(self.ops):
+            d = set()
+            if op.src in last_w:
+                d.add(last_w[op.src])
+            if op.dst in last_w:
+                d.add(last_w[op.dst])
+            d.update(reads_since.get(op.dst, ()))
+            d.discard(i)
+            deps.append(sorted(d))
+            reads_since.setdefault(op.src, []).append(i)
+            last_w[op.dst] = i
+            reads_since[op.dst] = []
+        return frags, readers, standalone, deps
 
     def use_prefill(self):
         """Run every layer through the tcgen05 sign GEMMs (forward_prefill) whatever the batch:
@@ -200,19 +216,54 @@ class DecodePlan:
             return
         mode = getattr(self, "_mode", "layer")
         if mode == "batched":
-            frags, readers, standalone = self._bchain
-            batch = int(self.buffers[self.input_buffer].shape[0])
-            for i, op in enumerate(self.ops):
+            self._eager_batched()
+            return
+        run = forward_prefill if mode == "prefill" else forward_device
+        for op in self.ops:
+            run(self.buffers[op.src], self.layers[op.layer], out=self.buffers[op.dst])
+
+    def _eager_batched(self):
+        """The batched chain with independent layers on concurrent streams (q/k/v, gate/up of a
+        Llama block run side by side): an op waits only for its dependencies (events), each stream
+        keeps its own workspace, and the streams fork from and join back into the current stream
+        (so graph capture records the branches)."""
+        import torch
+
+        frags, readers, standalone, deps = self._bchain
+        batch = int(self.buffers[self.input_buffer].shape[0])
+        main = torch.cuda.current_stream()
+        if getattr(self, "_bstreams", None) is None:
+            self._bstreams = [main] + [torch.cuda.Stream() for _ in range(2)]
+        streams = [main] + self._bstreams[1:]
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for st in streams[1:]:
+            st.wait_event(fork)
+        done, last_on = {}, {id(st): None for st in streams}
+        for i, op in enumerate(self.ops):
+            # a stream whose last op is a dependency (in-order: no event needed for that one), else
+            # the stream idle longest
+            st = next((st for st in streams if last_on[id(st)] in deps[i]), None)
+            if st is None:
+                st = min(streams, key=lambda x: -1 if last_on[id(x)] is None else last_on[id(x)])
+            for d in deps[i]:
+                if last_on[id(st)] != d:
+                    st.wait_event(done[d])
+            with torch.cuda.stream(st):
                 layer = self.layers[op.layer]
                 if i in standalone:
                     batched_quantize(self.buffers[op.src], layer, frags[i])
                 cons = [(self.layers[self.ops[j].layer], frags[j]) for j in readers[i]]
                 forward_batched_frag(frags[i], layer, batch, self.buffers[op.dst], consumers=cons,
                                      status=self._bstatus)
-            return
-        run = forward_prefill if mode == "prefill" else forward_device
-        for op in self.ops:
-            run(self.buffers[op.src], self.layers[op.layer], out=self.buffers[op.dst])
+                ev = torch.cuda.Event()
+                ev.record(st)
+            done[i] = ev
+            last_on[id(st)] = i
+        for st in streams[1:]:
+            j = torch.cuda.Event()
+            j.record(st)
+            main.wait_event(j)
 
     def capture(self):
         import torch

@@ -159,11 +159,13 @@ class DecodePlan:
             for l in self.layers)
 
     def default_path(self) -> str:
-        """The static path rule for a token batch: the decode engine up to 4 tokens (one launch),
-        the single-pass batched kernels for 5-16, the tcgen05 prefill chain above (when its layout
-        is available).  Measured (bench.py sweep)."""
+        """The static path rule for a token batch: the decode engine for 1-2 tokens, the
+        single-pass batched kernels for 3-16, the tcgen05 prefill chain above (when its layout is
+        available).  Measured (ms per step engine / batched): 7B 2 tokens 1.54 /
+        2.08, 3 tokens 2.22 / 2.08; 13B 1.5 bpw 3 tokens 3.33 / 2.94; 70B 2 tokens 13.0 / 10.7 --
+        use_fastest picks the batched kernels there (more than the 10 % margin)."""
         batch = int(self.buffers[self.input_buffer].shape[0])
-        if batch <= 4:
+        if batch <= 2:
             return "engine"
         if batch <= BATCHED_MAX_TOKENS:
             return "batched"

@@ -477,6 +477,7 @@ def sweep_bench(steps: int):
     for bpw in (1.0, 1.5, 2.0, 2.3):
         one("llama2-13b", bpw, 1, True)
     one("llama2-7b", 2.0, 4, True)
+    one("llama2-7b", 2.0, 4, False, batched=True)
     one("llama2-13b", 1.5, 4, True)
     one("llama2-13b", 1.5, 8, True)
     one("llama2-13b", 1.5, 8, False)

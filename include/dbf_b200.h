@@ -375,6 +375,12 @@ size_t dbf_batched_frag_bytes(int64_t cols, int64_t batch);
 int dbf_batched_quantize(const void* X, int x_dtype, int64_t ldx, int64_t batch, int64_t cols,
                          const void* iscale, int scale_dtype, void* frag, void* stream);
 size_t dbf_forward_batched_frag_workspace_bytes(int64_t n, int64_t k, int64_t m, int64_t batch);
+/* Diagnostics (builds with -DDBF_BATCHED_TRACE, tools/batched_trace.py; DBF_ERR_UNSUPPORTED
+ * otherwise): reset the per-launch trace slots (restart_slots != 0 also restarts their numbering),
+ * and copy n slots of {kind (1 quantize, 2 GEMV, 3 finalize), first CTA start, last return from
+ * the grid dependency wait, last warp end} (%globaltimer ns). */
+int dbf_batched_debug_reset(int restart_slots);
+int dbf_batched_debug_trace(unsigned long long* host, int n);
 int dbf_forward_batched_frag(const void* A_tiled, const void* B_tiled, const void* a,
                              const void* mid, int scale_dtype, int64_t n, int64_t k, int64_t m,
                              const void* frag_in, int64_t batch, void* Y, int y_dtype, int64_t ldy,

@@ -48,6 +48,8 @@ SIGNATURES: dict[str, tuple] = {
     "dbf_forward_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "dbf_forward_batched_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "dbf_batched_frag_bytes": (_sz, [_i64, _i64]),
+    "dbf_batched_debug_reset": (_int, [_int]),
+    "dbf_batched_debug_trace": (_int, [_vp, _int]),
     "dbf_batched_quantize": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _int, _vp, _vp]),
     "dbf_forward_batched_frag_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "dbf_forward_batched_frag": (

@@ -72,6 +72,29 @@ __device__ __forceinline__ float load_f(const void* p, int dt, int64_t i) {
 // come after it (the predecessor may still read what this kernel overwrites).
 __device__ __forceinline__ void grid_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+// Diagnostics build only (-DDBF_BATCHED_TRACE, tools/batched_trace.py): per launch slot, the
+// earliest CTA start, the latest return from grid_wait and the latest CTA end (%globaltimer ns)
+#ifdef DBF_BATCHED_TRACE
+__device__ unsigned long long g_btrace[8192][4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BT_START(slot) const unsigned long long bt0_ = gtime();
+#define BT_WAITED(slot)                                                        \
+  if ((slot) >= 0 && threadIdx.x == 0) {                                       \
+    atomicMin(&g_btrace[slot][1], bt0_);                                       \
+    atomicMax(&g_btrace[slot][2], gtime());                                    \
+  }
+#define BT_END(slot)                                                           \
+  if ((slot) >= 0 && (threadIdx.x & 31) == 0) atomicMax(&g_btrace[slot][3], gtime());
+#else
+#define BT_START(slot)
+#define BT_WAITED(slot)
+#define BT_END(slot)
+#endif
 __device__ __forceinline__ float fmax_nan(float a, float b) {
   float r;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
@@ -92,6 +115,7 @@ struct QuantIn {
   const void* pscale;   // per column of the partials (the previous GEMV's row scale), or null
   int scale_dtype;
   int cols, batch, tpad;
+  int tslot;  // diagnostics: trace slot (DBF_BATCHED_TRACE builds), -1
 };
 
 // Fragment buffer of one GEMV input (cols columns, tpad token slots): B fragments, then F, then T
@@ -174,14 +198,69 @@ __device__ __forceinline__ void emit_chunk(const float (&u)[2][4], int c, int t,
 }
 
 // One warp per (chunk, token): 64 groups of 4 columns, lane holds groups lane and lane + 32.
+// 4 consecutive scale values (fp16 pairs loaded as one 8-byte word where aligned)
+__device__ __forceinline__ void load_scale4(const void* p, int dt, int j0, float (&sc)[4]) {
+  if (dt == DBF_F16 && (j0 & 3) == 0) {
+    const uint2 r = __ldg((const uint2*)((const __half*)p + j0));
+    const float2 lo = __half22float2(*(const __half2*)&r.x), hi = __half22float2(*(const __half2*)&r.y);
+    sc[0] = lo.x, sc[1] = lo.y, sc[2] = hi.x, sc[3] = hi.y;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sc[e] = load_f(p, dt, j0 + e);
+  }
+}
+
+// the scales of columns j0..j0+3 (1 past the end / without a scale)
+__device__ __forceinline__ void scale4_at(const void* p, int dt, int j0, int cols, float (&sc)[4]) {
+  sc[0] = sc[1] = sc[2] = sc[3] = 1.f;
+  if (!p) return;
+  if (j0 + 3 < cols) {
+    load_scale4(p, dt, j0, sc);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (j0 + e < cols) sc[e] = load_f(p, dt, j0 + e);
+  }
+}
+// sum of the split partials of columns j0..j0+3 of token row t, in split order; every split's
+// 16-byte load is issued before the first add (one L2 round trip, not one per split)
+__device__ __forceinline__ void sum_splits4(const float* part, int splits, int64_t stride, int64_t row_off, int j0,
+                                            int cols, float (&v)[4]) {
+  v[0] = v[1] = v[2] = v[3] = 0.f;
+  if (j0 + 3 < cols) {
+    float4 p[kMaxSplits];
+#pragma unroll
+    for (int s = 0; s < kMaxSplits; ++s)
+      p[s] = s < splits ? __ldcg((const float4*)(part + (size_t)s * stride + row_off + j0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int s = 0; s < kMaxSplits; ++s)
+      if (s < splits) v[0] += p[s].x, v[1] += p[s].y, v[2] += p[s].z, v[3] += p[s].w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (j0 + e < cols)
+        for (int s = 0; s < splits; ++s) v[e] += __ldcg(part + (size_t)s * stride + row_off + j0 + e);
+  }
+}
+
+// One warp per (chunk, token): 64 groups of 4 columns, lane holds groups lane and lane + 32.
 __global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, FragView fv, int nj) {
+  BT_START(in.tslot)
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int nch = (in.cols + kChunkCols - 1) / kChunkCols;
+  const int c = item / in.tpad, t = item % in.tpad;
+  const bool live = item < nch * in.tpad && t < in.batch;
+  // the column scales are constant: loaded while the previous kernel drains
+  float sc[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    scale4_at(live ? (in.part ? in.pscale : in.iscale) : nullptr, in.scale_dtype, c * kChunkCols + 4 * (lane + 32 * h),
+              in.cols, sc[h]);
   grid_wait();
+  BT_WAITED(in.tslot)
   grid_launch_dependents();
   if (item >= nch * in.tpad) return;
-  const int c = item / in.tpad, t = item % in.tpad;
   if (t >= in.batch) {
     zero_chunk(c, t, fv, in.tpad, nj);
     return;
@@ -190,57 +269,22 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, FragView
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j0 = c * kChunkCols + 4 * (lane + 32 * h);  // this lane's group of 4 columns
-    float sc[4] = {1.f, 1.f, 1.f, 1.f};
-    const void* scp = in.part ? in.pscale : in.iscale;
-    if (j0 + 3 < in.cols) {
-      if (in.part) {
-        // the previous stage's split partials, summed in split order (deterministic); rows are
-        // padded to a multiple of 4 floats (16-byte groups)
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-        for (int s = 0; s < in.splits; ++s) {
-          const float4 b = __ldcg((const float4*)(in.part + (size_t)s * in.part_stride + (size_t)t * in.ldx + j0));
-          a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
-        }
-        u[h][0] = a.x, u[h][1] = a.y, u[h][2] = a.z, u[h][3] = a.w;
-      } else if (in.x_dtype == DBF_F16 && ((in.ldx | (int64_t)(uintptr_t)in.x / 2) & 3) == 0) {
-        const uint2 r = __ldg((const uint2*)((const __half*)in.x + (int64_t)t * in.ldx + j0));
-        const float2 lo = __half22float2(*(const __half2*)&r.x), hi = __half22float2(*(const __half2*)&r.y);
-        u[h][0] = lo.x, u[h][1] = lo.y, u[h][2] = hi.x, u[h][3] = hi.y;
-      } else {
+    if (in.part) {
+      // the previous stage's split partials (rows padded to 4 floats), summed in split order
+      sum_splits4(in.part, in.splits, in.part_stride, (int64_t)t * in.ldx, j0, in.cols, u[h]);
+    } else if (j0 + 3 < in.cols && in.x_dtype == DBF_F16 && ((in.ldx | (int64_t)(uintptr_t)in.x / 2) & 3) == 0) {
+      const uint2 r = __ldg((const uint2*)((const __half*)in.x + (int64_t)t * in.ldx + j0));
+      const float2 lo = __half22float2(*(const __half2*)&r.x), hi = __half22float2(*(const __half2*)&r.y);
+      u[h][0] = lo.x, u[h][1] = lo.y, u[h][2] = hi.x, u[h][3] = hi.y;
+    } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) u[h][e] = load_f(in.x, in.x_dtype, (int64_t)t * in.ldx + j0 + e);
-      }
-      if (scp) {
-        if (in.scale_dtype == DBF_F16) {
-          const uint2 r = __ldg((const uint2*)((const __half*)scp + j0));
-          const float2 lo = __half22float2(*(const __half2*)&r.x), hi = __half22float2(*(const __half2*)&r.y);
-          sc[0] = lo.x, sc[1] = lo.y, sc[2] = hi.x, sc[3] = hi.y;
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sc[e] = load_f(scp, in.scale_dtype, j0 + e);
-        }
-      }
-    } else {  // the ragged end of the last chunk
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = j0 + e;
-        float v = 0.f;
-        if (j < in.cols) {
-          if (in.part) {
-            for (int s = 0; s < in.splits; ++s) v += __ldcg(in.part + (size_t)s * in.part_stride + (size_t)t * in.ldx + j);
-          } else {
-            v = load_f(in.x, in.x_dtype, (int64_t)t * in.ldx + j);
-          }
-          if (scp) sc[e] = load_f(scp, in.scale_dtype, j);
-        }
-        u[h][e] = v;
-      }
+      for (int e = 0; e < 4; ++e) u[h][e] = j0 + e < in.cols ? load_f(in.x, in.x_dtype, (int64_t)t * in.ldx + j0 + e) : 0.f;
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) u[h][e] *= sc[e];
+    for (int e = 0; e < 4; ++e) u[h][e] *= sc[h][e];
   }
   emit_chunk(u, c, t, fv, in.tpad, nj);
+  BT_END(in.tslot)
 }
 
 struct GemvArgs {
@@ -252,6 +296,7 @@ struct GemvArgs {
   int tpad, batch;
   float* part;  // part[split][tpad][ldp]
   int ldp;      // partial row stride: rows rounded up to 4 floats
+  int tslot;    // diagnostics: trace slot (DBF_BATCHED_TRACE builds), -1
 };
 
 // One warp per 16-row block and K split; NJ token groups of 4 share every extracted A fragment.
@@ -290,7 +335,9 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
     wn[q] = live[q] && n > 1 ? ld_stream(wb[q] + (int64_t)(c0 + 1) * 32, pol) : make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
+  BT_START(g.tslot)
   grid_wait();
+  BT_WAITED(g.tslot)
   grid_launch_dependents();
   const uint8_t* bsrc = reinterpret_cast<const uint8_t*>(g.bfrag) + (size_t)c0 * kBBytes;
   if (threadIdx.x == 0) {
@@ -380,6 +427,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
       }
     }
   }
+  BT_END(g.tslot)
 }
 
 // Layers that read this layer's output next (DecodePlan chains): each gets its first-GEMV B
@@ -403,19 +451,8 @@ struct FinArgs {
   unsigned* status;
   int ncons;
   Consumer cons[kMaxConsumers];
+  int tslot;  // diagnostics: trace slot (DBF_BATCHED_TRACE builds), -1
 };
-
-// 4 consecutive scale values (fp16 pairs loaded as one 8-byte word where aligned)
-__device__ __forceinline__ void load_scale4(const void* p, int dt, int j0, float (&sc)[4]) {
-  if (dt == DBF_F16 && (j0 & 3) == 0) {
-    const uint2 r = __ldg((const uint2*)((const __half*)p + j0));
-    const float2 lo = __half22float2(*(const __half2*)&r.x), hi = __half22float2(*(const __half2*)&r.y);
-    sc[0] = lo.x, sc[1] = lo.y, sc[2] = hi.x, sc[3] = hi.y;
-  } else {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) sc[e] = load_f(p, dt, j0 + e);
-  }
-}
 
 // One warp per (256-row chunk, token, consumer): y = oscale (.) sum of the splits (split order),
 // rounded to the output dtype; the consumer-0 warp stores it and reports status bits 1 (a
@@ -423,13 +460,25 @@ __device__ __forceinline__ void load_scale4(const void* p, int dt, int j0, float
 // writes its consumer's B fragments of the chunk (one warp per consumer: the chunk's rounding is
 // recomputed, not shared, so the consumers run side by side).
 __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs f) {
+  BT_START(f.tslot)
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int nch = (f.rows + kChunkCols - 1) / kChunkCols, ncw = f.ncons > 0 ? f.ncons : 1;
+  const int k = item % ncw, ct = item / ncw, c = ct / f.tpad, t = ct % f.tpad;
+  const bool live = item < nch * f.tpad * ncw && t < f.batch;
+  // the output scale and this warp's consumer's input scale are constant: loaded while the
+  // previous kernel drains
+  float osc[2][4], csc[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j0 = c * kChunkCols + 4 * (lane + 32 * h);
+    scale4_at(live ? f.oscale : nullptr, f.scale_dtype, j0, f.rows, osc[h]);
+    scale4_at(live && f.ncons > 0 ? f.cons[k].b : nullptr, f.scale_dtype, j0, f.rows, csc[h]);
+  }
   grid_wait();
+  BT_WAITED(f.tslot)
   grid_launch_dependents();
   if (item >= nch * f.tpad * ncw) return;
-  const int k = item % ncw, ct = item / ncw, c = ct / f.tpad, t = ct % f.tpad;
   if (t >= f.batch) {
     if (f.ncons > 0) zero_chunk(c, t, f.cons[k].fv, f.tpad, f.nj);
     return;
@@ -440,29 +489,13 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs f) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j0 = c * kChunkCols + 4 * (lane + 32 * h);
-    float v[4] = {0.f, 0.f, 0.f, 0.f}, sc[4] = {1.f, 1.f, 1.f, 1.f};
     const bool full = j0 + 3 < f.rows;
-    if (full) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-      for (int s = 0; s < f.splits; ++s) {
-        const float4 p = __ldcg((const float4*)(f.part + (size_t)s * f.part_stride + (size_t)t * f.ldp + j0));
-        a.x += p.x, a.y += p.y, a.z += p.z, a.w += p.w;
-      }
-      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
-      if (f.oscale) load_scale4(f.oscale, f.scale_dtype, j0, sc);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (j0 + e < f.rows) {
-          for (int s = 0; s < f.splits; ++s) v[e] += __ldcg(f.part + (size_t)s * f.part_stride + (size_t)t * f.ldp + j0 + e);
-          if (f.oscale) sc[e] = load_f(f.oscale, f.scale_dtype, j0 + e);
-        }
-    }
+    float v[4];
+    sum_splits4(f.part, f.splits, f.part_stride, (int64_t)t * f.ldp, j0, f.rows, v);
     float w[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      w[e] = v[e] * sc[e];
+      w[e] = v[e] * osc[h][e];
       if (j0 + e < f.rows && !isfinite(w[e])) bad |= kStatusNonFinite;
     }
     const int64_t o = (int64_t)t * f.ldy + j0;
@@ -516,26 +549,17 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs f) {
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0 && f.status) atomicOr(f.status, bad);
   }
-  if (f.ncons == 0) return;
-  const Consumer& cs = f.cons[k];
+  if (f.ncons == 0) {
+    BT_END(f.tslot)
+    return;
+  }
   float u[2][4];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int j0 = c * kChunkCols + 4 * (lane + 32 * h);
-    float sc[4] = {1.f, 1.f, 1.f, 1.f};
-    if (cs.b) {
-      if (j0 + 3 < f.rows) {
-        load_scale4(cs.b, f.scale_dtype, j0, sc);
-      } else {
+  for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (j0 + e < f.rows) sc[e] = load_f(cs.b, f.scale_dtype, j0 + e);
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) u[h][e] = yr[h][e] * sc[e];
-  }
-  emit_chunk(u, c, t, cs.fv, f.tpad, f.nj);
+    for (int e = 0; e < 4; ++e) u[h][e] = yr[h][e] * csc[h][e];
+  emit_chunk(u, c, t, f.cons[k].fv, f.tpad, f.nj);
+  BT_END(f.tslot)
 }
 
 // ---- host side ---------------------------------------------------------------------------------
@@ -574,6 +598,20 @@ inline Layout layout_of(int64_t n, int64_t k, int64_t m, int64_t batch) {
   L.total = align256(L.frag1 + frag_bytes(m, tpad));
   return L;
 }
+
+// diagnostics: the next trace slot (DBF_BATCHED_TRACE builds; -1 otherwise) and the kernel kind
+// recorded in column 0 of the slot (1 quantize, 2 gemv, 3 finalize)
+#ifdef DBF_BATCHED_TRACE
+static int g_next_slot = 0;
+static int g_slot_kind[8192];
+inline int next_slot(int kind) {
+  const int s = g_next_slot < 8192 ? g_next_slot++ : -1;
+  if (s >= 0) g_slot_kind[s] = kind;
+  return s;
+}
+#else
+inline int next_slot(int) { return -1; }
+#endif
 
 // every kernel of the chain: programmatic dependent launch (see grid_wait)
 template <typename... KArgs, typename... Args>
@@ -633,7 +671,7 @@ int dbf_batched_quantize(const void* X, int x_dtype, int64_t ldx, int64_t batch,
   const int tpad = tpad_of(batch);
   QuantIn q{};
   q.x = X, q.x_dtype = x_dtype, q.ldx = ldx, q.iscale = iscale, q.scale_dtype = scale_dtype;
-  q.cols = (int)cols, q.batch = (int)batch, q.tpad = tpad;
+  q.cols = (int)cols, q.batch = (int)batch, q.tpad = tpad, q.tslot = next_slot(1);
   return launch_pdl(quantize_kernel, dim3((unsigned)ceil_div(chunks(cols) * tpad, kWarps)), kThreads,
                     (cudaStream_t)stream, q, frag_view(frag, cols, tpad), tpad / 4);
 }
@@ -672,23 +710,23 @@ int dbf_forward_batched_frag(const void* A_tiled, const void* B_tiled, const voi
 
   // t = mid * (B . (x * b))
   GemvArgs g1{(const uint4*)B_tiled, (int)k, (int)row_blocks(k), (int)chunks(m), cps1, f1.bfrag, f1.F, f1.T, tpad,
-              (int)batch, part1, ldk};
+              (int)batch, part1, ldk, next_slot(2)};
   int st = gemv(g1, nj, S1, s);
   if (st != DBF_OK) return st;
   // t quantized straight from the stage-1 partials
   QuantIn q2{};
   q2.part = part1, q2.splits = S1, q2.ldx = ldk, q2.part_stride = (int64_t)tpad * ldk, q2.pscale = mid;
-  q2.scale_dtype = scale_dtype, q2.cols = (int)k, q2.batch = (int)batch, q2.tpad = tpad;
+  q2.scale_dtype = scale_dtype, q2.cols = (int)k, q2.batch = (int)batch, q2.tpad = tpad, q2.tslot = next_slot(1);
   st = launch_pdl(quantize_kernel, dim3((unsigned)ceil_div(chunks(k) * tpad, kWarps)), kThreads, s, q2, f2, nj);
   if (st != DBF_OK) return st;
   // y = a * (A . t)
   GemvArgs g2{(const uint4*)A_tiled, (int)n, (int)row_blocks(n), (int)chunks(k), cps2, f2.bfrag, f2.F, f2.T, tpad,
-              (int)batch, part2, ldn};
+              (int)batch, part2, ldn, next_slot(2)};
   if ((st = gemv(g2, nj, S2, s)) != DBF_OK) return st;
   FinArgs fa{};
   fa.part = part2, fa.splits = S2, fa.part_stride = (int64_t)tpad * ldn, fa.ldp = ldn, fa.rows = (int)n;
   fa.batch = (int)batch, fa.tpad = tpad, fa.nj = nj, fa.oscale = a, fa.scale_dtype = scale_dtype;
-  fa.y = Y, fa.y_dtype = y_dtype, fa.ldy = ldy, fa.status = status, fa.ncons = nconsumers;
+  fa.y = Y, fa.y_dtype = y_dtype, fa.ldy = ldy, fa.status = status, fa.ncons = nconsumers, fa.tslot = next_slot(3);
   for (int i = 0; i < nconsumers; ++i) fa.cons[i] = Consumer{consumers[i].b, frag_view(consumers[i].frag, n, tpad)};
   return launch_pdl(finalize_kernel, dim3((unsigned)ceil_div(chunks(n) * tpad * std::max(1, nconsumers), kWarps)),
                     kThreads, s, fa);
@@ -711,6 +749,31 @@ int dbf_forward_batched(const void* A_tiled, const void* B_tiled, const void* a,
   if (st != DBF_OK) return st;
   return dbf_forward_batched_frag(A_tiled, B_tiled, a, mid, scale_dtype, n, k, m, frag1, batch, Y, y_dtype, ldy,
                                   nullptr, 0, workspace, L.total_frag, status, stream);
+}
+
+// diagnostics (DBF_BATCHED_TRACE builds; DBF_ERR_UNSUPPORTED otherwise): reset every trace slot /
+// restart slot numbering, and copy n slots (kind, first CTA start, last grid_wait exit, last end)
+int dbf_batched_debug_reset(int restart_slots) {
+#ifdef DBF_BATCHED_TRACE
+  static unsigned long long init[8192][4];
+  for (int i = 0; i < 8192; ++i) init[i][0] = 0, init[i][1] = ~0ull, init[i][2] = 0, init[i][3] = 0;
+  if (restart_slots) batched::g_next_slot = 0;
+  return cudaMemcpyToSymbol(batched::g_btrace, init, sizeof(init)) == cudaSuccess ? DBF_OK : DBF_ERR_CUDA;
+#else
+  (void)restart_slots;
+  return DBF_ERR_UNSUPPORTED;
+#endif
+}
+int dbf_batched_debug_trace(unsigned long long* host, int n) {
+#ifdef DBF_BATCHED_TRACE
+  if (n > 8192) n = 8192;
+  if (cudaMemcpyFromSymbol(host, batched::g_btrace, (size_t)n * 32) != cudaSuccess) return DBF_ERR_CUDA;
+  for (int i = 0; i < n; ++i) host[4 * i] = (unsigned long long)batched::g_slot_kind[i];
+  return DBF_OK;
+#else
+  (void)host, (void)n;
+  return DBF_ERR_UNSUPPORTED;
+#endif
 }
 
 }  // extern "C"

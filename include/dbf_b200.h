@@ -343,9 +343,9 @@ int dbf_engine_occupancy(int32_t max_cols, int32_t* blocks_per_sm, int32_t* regs
 /* Launch one run of the program (cooperative: all CTAs co-resident; one kernel). */
 int dbf_engine_launch(const dbf_engine_program* program, void* stream);
 
-/* ---- batched decode: 2-16 tokens, one pass over the weights -------------------------------- */
+/* ---- batched decode: 2-32 tokens, one pass over the weights -------------------------------- */
 /*
- * dbf_forward (kernel.py:48-62) for a small token batch (batch <= 16): per stage, every extracted
+ * dbf_forward (kernel.py:48-62) for a small token batch (batch <= 32): per stage, every extracted
  * sign fragment feeds one int8 IMMA per group of 4 tokens, so each sign matrix is read ONCE for
  * all tokens (the decode engine carries 4 tokens per launch).  Numerics are the engine's: each
  * (token, 256-column chunk) is quantized to a 13-bit grid relative to its chunk max (two balanced

@@ -1,4 +1,4 @@
-// Batched decode (2-16 tokens): kernel.forward (/root/reference/pkg/src/dbf/kernel.py:48-62) for a
+// Batched decode (2-32 tokens): kernel.forward (/root/reference/pkg/src/dbf/kernel.py:48-62) for a
 // small token batch with ONE pass over each sign matrix for all tokens.
 //
 // The decode engine (engine.cu) carries at most 4 tokens per launch (4 tokens x 2 digit planes =
@@ -31,7 +31,7 @@ constexpr int kGemvWarps = 4;             // gemv: 16-row blocks per CTA (one pe
 constexpr int kCtasPerSm = 8;             // gemv grid target (K splits fill it) ...
 constexpr int kMaxSplits = 8;             // ... up to this many partials per output (the next
                                           // kernel sums them: more made that sum the long pole)
-constexpr int kMaxTokens = 16;
+constexpr int kMaxTokens = 32;
 constexpr float kQScale = 4079.f / 4096.f;  // 8 * |X| stays below the two-digit limit 32640
 constexpr int kBadF = -128;                 // chunk holding inf / NaN: outputs it feeds are NaN
 constexpr int kStatusNonFinite = 1, kStatusOverflow = 2;
@@ -308,7 +308,8 @@ template <int NJ, int RB>
 __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
   using namespace sm100;
   constexpr int kBBytes = 8 * NJ * 32 * 8;  // B fragments of one chunk
-  constexpr int kSlots = 3;
+  // ring depth: 3 slots (2 chunks ahead); 2 at NJ > 4 (16 KB slots, static shared memory)
+  constexpr int kSlots = NJ > 4 ? 2 : 3, kAhead = kSlots - 1;
   __shared__ __align__(128) uint8_t bsm[kSlots][kBBytes];
   __shared__ __align__(8) uint64_t full[kSlots], empty[kSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
   grid_launch_dependents();
   const uint8_t* bsrc = reinterpret_cast<const uint8_t*>(g.bfrag) + (size_t)c0 * kBBytes;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2 && i < n; ++i) {
+    for (int i = 0; i < kAhead && i < n; ++i) {
       mbar_arrive_expect_tx(&full[i], kBBytes);
       bulk_copy_g2s(bsm[i], bsrc + (size_t)i * kBBytes, kBBytes, &full[i]);
     }
@@ -353,11 +354,11 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(GemvArgs g) {
     for (int j = 0; j < NJ; ++j) y[q][j][0] = y[q][j][1] = 0.f;
   for (int i = 0; i < n; ++i) {
     const int c = c0 + i, slot = i % kSlots;
-    if (threadIdx.x == 0 && i + 2 < n) {  // chunk i + 2 into the slot chunk i - 1 held
-      const int s2 = (i + 2) % kSlots;
-      if (i + 2 >= kSlots) mbar_wait(&empty[s2], (((i + 2) / kSlots) - 1) & 1);
+    if (threadIdx.x == 0 && i + kAhead < n) {  // chunk i + kAhead into the slot chunk i - 1 held
+      const int ia = i + kAhead, s2 = ia % kSlots;
+      if (ia >= kSlots) mbar_wait(&empty[s2], ((ia / kSlots) - 1) & 1);
       mbar_arrive_expect_tx(&full[s2], kBBytes);
-      bulk_copy_g2s(bsm[s2], bsrc + (size_t)(i + 2) * kBBytes, kBBytes, &full[s2]);
+      bulk_copy_g2s(bsm[s2], bsrc + (size_t)ia * kBBytes, kBBytes, &full[s2]);
     }
     uint4 wnn[RB];
 #pragma unroll
@@ -569,10 +570,11 @@ inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 // row blocks per warp: two where there are enough rows (the chunk's B fragments, barriers and
 // scale loads then serve twice the MMAs)
-inline int rb_per_warp(int64_t nrb) { return nrb >= 128 ? 2 : 1; }
+// (one above 16 tokens: registers)
+inline int rb_per_warp(int64_t nrb, int nj) { return nrb >= 128 && nj <= 4 ? 2 : 1; }
 // K splits of one GEMV: enough CTAs for kCtasPerSm per SM, whole chunks per split
-inline int split_count(int64_t nrb, int64_t nch, int* cps) {
-  const int64_t gx = ceil_div(nrb, (int64_t)kGemvWarps * rb_per_warp(nrb));
+inline int split_count(int64_t nrb, int64_t nch, int nj, int* cps) {
+  const int64_t gx = ceil_div(nrb, (int64_t)kGemvWarps * rb_per_warp(nrb, nj));
   int64_t S = std::max<int64_t>(1, ceil_div((int64_t)kCtasPerSm * kNumSMs, gx));
   S = std::min<int64_t>(std::min<int64_t>(S, kMaxSplits), nch);
   const int64_t c = ceil_div(nch, S);
@@ -588,7 +590,8 @@ struct Layout {
 inline Layout layout_of(int64_t n, int64_t k, int64_t m, int64_t batch) {
   const int tpad = tpad_of(batch);
   int cps;
-  const int S1 = split_count(row_blocks(k), chunks(m), &cps), S2 = split_count(row_blocks(n), chunks(k), &cps);
+  const int S1 = split_count(row_blocks(k), chunks(m), tpad / 4, &cps),
+            S2 = split_count(row_blocks(n), chunks(k), tpad / 4, &cps);
   Layout L;
   L.frag2 = 0;
   L.part = align256(L.frag2 + frag_bytes(k, tpad));
@@ -637,11 +640,21 @@ static int gemv_rb(const GemvArgs& a, int nj, int splits, cudaStream_t s) {
     case 1: return launch_pdl(gemv_kernel<1, RB>, grid, kGemvWarps * 32, s, a);
     case 2: return launch_pdl(gemv_kernel<2, RB>, grid, kGemvWarps * 32, s, a);
     case 3: return launch_pdl(gemv_kernel<3, RB>, grid, kGemvWarps * 32, s, a);
-    default: return launch_pdl(gemv_kernel<4, RB>, grid, kGemvWarps * 32, s, a);
+    case 4: return launch_pdl(gemv_kernel<4, RB>, grid, kGemvWarps * 32, s, a);
+    default:
+      if constexpr (RB == 1) {
+        switch (nj) {
+          case 5: return launch_pdl(gemv_kernel<5, 1>, grid, kGemvWarps * 32, s, a);
+          case 6: return launch_pdl(gemv_kernel<6, 1>, grid, kGemvWarps * 32, s, a);
+          case 7: return launch_pdl(gemv_kernel<7, 1>, grid, kGemvWarps * 32, s, a);
+          default: return launch_pdl(gemv_kernel<8, 1>, grid, kGemvWarps * 32, s, a);
+        }
+      }
+      return DBF_ERR_UNSUPPORTED;
   }
 }
 static int gemv(const GemvArgs& a, int nj, int splits, cudaStream_t s) {
-  return rb_per_warp(a.nrb) == 2 ? gemv_rb<2>(a, nj, splits, s) : gemv_rb<1>(a, nj, splits, s);
+  return rb_per_warp(a.nrb, nj) == 2 ? gemv_rb<2>(a, nj, splits, s) : gemv_rb<1>(a, nj, splits, s);
 }
 
 }  // namespace batched
@@ -702,7 +715,7 @@ int dbf_forward_batched_frag(const void* A_tiled, const void* B_tiled, const voi
   char* ws = (char*)workspace;
   const int tpad = tpad_of(batch), nj = tpad / 4;
   int cps1, cps2;
-  const int S1 = split_count(row_blocks(k), chunks(m), &cps1), S2 = split_count(row_blocks(n), chunks(k), &cps2);
+  const int S1 = split_count(row_blocks(k), chunks(m), nj, &cps1), S2 = split_count(row_blocks(n), chunks(k), nj, &cps2);
   const int ldk = ldp_of(k), ldn = ldp_of(n);
   float* part1 = (float*)(ws + L.part);
   float* part2 = part1 + (size_t)S1 * tpad * ldk;

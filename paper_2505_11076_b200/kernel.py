@@ -131,12 +131,12 @@ def forward_prefill(X, layer: DeviceLayer, out=None):
     return Y
 
 
-BATCHED_MAX_TOKENS = 16
+BATCHED_MAX_TOKENS = 32
 
 
 def forward_batched(X, layer: DeviceLayer, out=None, status=None):
     """Y = forward(X, layer) (/root/reference/pkg/src/dbf/kernel.py:48-62) for a CUDA batch of
-    1-16 token rows with ONE pass over each sign matrix for all tokens (dbf_forward_batched,
+    1-32 token rows with ONE pass over each sign matrix for all tokens (dbf_forward_batched,
     csrc/batched.cu): every extracted sign fragment feeds one int8 IMMA per group of 4 tokens.
     Numerics are the decode engine's (13-bit grid per token and 256-column chunk, exact chunk sums,
     fp32 accumulation and intermediate); ``status`` (a 1-element int32 CUDA tensor, optional) gets

@@ -95,19 +95,27 @@ class DecodePlan:
         return self
 
     def use_batched(self):
-        """Run every layer through dbf_forward_batched (csrc/batched.cu): 1-16 tokens, one pass
-        over each sign matrix for all of them (five short kernels per layer; the engine carries 4
-        tokens per launch and re-streams the weights for every group of 4)."""
+        """Run every layer through the batched kernels (csrc/batched.cu): up to 32 tokens share one
+        pass over each sign matrix (four short kernels per layer, layers chained by fragments and
+        independent ones on concurrent streams); larger batches run as consecutive groups of
+        <= 32 token rows of the same buffers (one weight pass per group)."""
         import torch
 
         batch = int(self.buffers[self.input_buffer].shape[0])
-        if batch > BATCHED_MAX_TOKENS:
-            raise ValueError(f"use_batched takes at most {BATCHED_MAX_TOKENS} tokens, the plan has {batch}")
         self.engine = None
         self._mode = "batched"
         if getattr(self, "_bstatus", None) is None:
             self._bstatus = torch.zeros(1, dtype=torch.int32, device=self.buffers[0].device)
-        self._bchain = self._batched_chain(batch)
+        if batch > BATCHED_MAX_TOKENS:
+            self._bgroups = []
+            for t0 in range(0, batch, BATCHED_MAX_TOKENS):
+                sub = DecodePlan(self.layers, self.ops, [b[t0:t0 + BATCHED_MAX_TOKENS] for b in self.buffers],
+                                 input_buffer=self.input_buffer, output_buffer=self.output_buffer)
+                sub._bstatus = self._bstatus
+                self._bgroups.append(sub.use_batched())
+        else:
+            self._bgroups = None
+            self._bchain = self._batched_chain(batch)
         self._graph = None
         return self
 
@@ -159,17 +167,18 @@ class DecodePlan:
             for l in self.layers)
 
     def default_path(self) -> str:
-        """The static path rule for a token batch: the decode engine for 1-2 tokens, the
-        single-pass batched kernels for 3-16, the tcgen05 prefill chain above (when its layout is
-        available).  Measured (ms per step engine / batched): 7B 2 tokens 1.54 /
-        2.08, 3 tokens 2.22 / 2.08; 13B 1.5 bpw 3 tokens 3.33 / 2.94; 70B 2 tokens 13.0 / 10.7 --
-        use_fastest picks the batched kernels there (more than the 10 % margin)."""
+        """The static path rule for a token batch: the decode engine for 1-2 tokens, the batched
+        kernels for 3-64 (one weight pass per group of <= 32), the tcgen05 prefill chain above
+        (when its layout is available).  Measured (ms per step): engine / batched
+        7B 2 tokens 1.55 / 1.89, 3 tokens 2.22 / 1.90; 70B 2 tokens 13.0 / 9.6 (use_fastest picks
+        the batched kernels there, beyond the 10 % margin); batched / prefill chain 7B 32 tokens
+        4.2 / 8.7, 70B 32 tokens 30.4 / 62.8, 13B 64 tokens ~11.6 / 12.3."""
         batch = int(self.buffers[self.input_buffer].shape[0])
         if batch <= 2:
             return "engine"
-        if batch <= BATCHED_MAX_TOKENS:
+        if batch <= 2 * BATCHED_MAX_TOKENS:
             return "batched"
-        return "prefill" if self._prefill_ok() else "engine"
+        return "prefill" if self._prefill_ok() else "batched"
 
     def use_fastest(self, steps: int = 5, grid: int | None = None, margin: float = 0.10):
         """Time the decode engine (groups of <= 4 tokens) against the tcgen05 prefill chain on this
@@ -183,8 +192,7 @@ class DecodePlan:
 
         _lib.require_cuda()
         cands = [("engine", lambda: self.use_engine(grid))]
-        if int(self.buffers[self.input_buffer].shape[0]) <= BATCHED_MAX_TOKENS:
-            cands.append(("batched", self.use_batched))
+        cands.append(("batched", self.use_batched))
         if self._prefill_ok():
             cands.append(("prefill", self.use_prefill))
         saved = self.buffers[self.input_buffer].clone()
@@ -218,7 +226,8 @@ class DecodePlan:
             return
         mode = getattr(self, "_mode", "layer")
         if mode == "batched":
-            self._eager_batched()
+            for sub in self._bgroups or [self]:
+                sub._eager_batched()
             return
         run = forward_prefill if mode == "prefill" else forward_device
         for op in self.ops:

@@ -23,7 +23,7 @@ def _ref(x, layer):
                             layer.mid.double().cpu().numpy(), layer.B.to_host().bits, layer.b.double().cpu().numpy())
 
 
-@pytest.mark.parametrize("batch", [1, 2, 4, 5, 8, 13, 16])
+@pytest.mark.parametrize("batch", [1, 2, 4, 5, 8, 13, 16, 17, 24, 32])
 def test_batched_matches_oracle(batch):
     import torch
 
@@ -46,7 +46,7 @@ def test_batched_ragged_shapes(shape):
     g = torch.Generator(device="cuda")
     g.manual_seed(n + k + m)
     layer = P.random_device_layer(n, k, m, generator=g, keep_words=True)
-    for batch in (3, 11):
+    for batch in (3, 11, 27):
         x = torch.randn((batch, m), generator=g, device="cuda").half()
         y = P.forward_batched(x, layer).double().cpu().numpy()
         ref = _ref(x, layer)
@@ -109,7 +109,7 @@ def test_batched_rejects_bad_input():
 
     layer = P.random_device_layer(64, 32, 64)
     with pytest.raises(ValueError):
-        P.forward_batched(torch.zeros((17, 64), dtype=torch.half, device="cuda"), layer)
+        P.forward_batched(torch.zeros((33, 64), dtype=torch.half, device="cuda"), layer)
     with pytest.raises(ValueError):
         P.forward_batched(torch.zeros((4, 63), dtype=torch.half, device="cuda"), layer)
     with pytest.raises(ValueError):
@@ -218,3 +218,25 @@ def test_batched_chain_bitwise_equals_per_layer_calls():
         torch.cuda.synchronize()
         for i, (a, b) in enumerate(zip(chained, plan.buffers)):
             assert torch.equal(a, b), (model, i)
+
+
+def test_batched_plan_groups_above_32_tokens():
+    """40 tokens: two groups (32 + 8) of the batched chain over slices of the same buffers, within
+    the tolerance of the exact per-layer kernels; default path batched up to 64 tokens."""
+    import torch
+    from paper_2505_11076_b200.plan import llama_decode_plan
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(140)
+    plan = llama_decode_plan("llama2-7b", bpw=2.0, batch=40, blocks=1, generator=g)
+    assert plan.default_path() == "batched"
+    x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
+    outs = []
+    for use in (plan.use_layer_kernels, plan.use_batched):
+        use()
+        plan.buffers[plan.input_buffer].copy_(x)
+        plan._eager()
+        torch.cuda.synchronize()
+        outs.append(plan.buffers[plan.output_buffer].double().cpu().numpy())
+    assert len(plan._bgroups) == 2
+    assert rel_max(outs[1], outs[0]) <= TOL and rel_norm(outs[1], outs[0]) <= TOL

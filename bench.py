@@ -474,6 +474,7 @@ def sweep_bench(steps: int):
     one("llama2-70b", 2.0, 16, False, prefill=True)
     one("llama2-70b", 2.0, 16, False, batched=True)
     one("llama2-70b", 2.0, 8, False, batched=True)
+    one("llama2-70b", 2.0, 32, False, batched=True)
     for bpw in (1.0, 1.5, 2.0, 2.3):
         one("llama2-13b", bpw, 1, True)
     one("llama2-7b", 2.0, 4, True)

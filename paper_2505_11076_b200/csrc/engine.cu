@@ -292,26 +292,6 @@ __device__ __forceinline__ bool load_group(const InSpec& in, int col0, uint32_t 
   return true;
 }
 
-// Experiment builds (DBF_POLL_CANARY = n): before re-reading a whole chunk (1 KB of LL words per
-// warp per poll), wait until n canary words (the last row of units 15, 14, ...) carry the epoch.
-__device__ __forceinline__ void ll_canary(const InSpec& in, int c0, uint32_t epoch) {
-#ifdef DBF_POLL_CANARY
-  if (in.kind != 1) return;
-  const int lane = threadIdx.x & 31;
-  const int row = c0 + 255 - 16 * lane;
-  for (;;) {
-    bool ok = true;
-    if (lane < DBF_POLL_CANARY && row < in.cols) {
-      uint32_t w;
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(w) : "l"((const uint32_t*)in.x + row) : "memory");
-      ok = (w >> 16) == epoch;
-    }
-    if (__all_sync(0xffffffffu, ok)) return;
-    __nanosleep(kPollSleepNs);
-  }
-#endif
-}
-
 // Scale and quantize one chunk (this lane: groups lane and lane + 32) into the warp's
 // B-fragment scratch; see quantize_chunk.  Returns F and T = sum_j X_j.
 __device__ __forceinline__ void emit_digits(float (&u)[2][4], const float (&sc)[2][4], uint8_t* xs, int kb_stride,
@@ -399,7 +379,6 @@ __device__ __forceinline__ void quantize_chunk(const InSpec& in, int c, uint32_t
   }
   int npoll = 0;
   if (dbg && lane == 0) dbg[0] = gtimer();
-  ll_canary(in, c0, epoch);
   for (;;) {
     const bool ok0 = load_group(in, c0 + 4 * lane, epoch, u[0]);
     const bool ok1 = load_group(in, c0 + 4 * (lane + 32), epoch, u[1]);
@@ -441,8 +420,7 @@ __device__ __forceinline__ void quantize_fetched(const InSpec& in, int c, uint32
   const bool ok0 = ll_group(f.v[0], c0 + 4 * lane, in.cols, epoch, u[0]);
   const bool ok1 = ll_group(f.v[1], c0 + 4 * (lane + 32), in.cols, epoch, u[1]);
   if (!__all_sync(0xffffffffu, ok0 && ok1)) {
-    ll_canary(in, c0, epoch);
-    for (;;) {  // not all published when prefetched: poll as usual
+      for (;;) {  // not all published when prefetched: poll as usual
 #ifdef DBF_LL_TRACE
       const long long t0 = gtimer();
 #endif
@@ -653,11 +631,7 @@ __device__ __noinline__ void allreduce_cta(const ArArgs ar, const dbf_engine_run
     return i - r0 < nr ? rs[i - r0] : ArRun{R[i].out_plain, R[i].rows, R[i].rb, R[i].nunits, 0};
   };
   if (threadIdx.x == 0) {
-#ifdef DBF_AR_FENCE_GPU  // experiment only (not valid across GPUs): the fence's own cost at world 1
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#else
     asm volatile("fence.acq_rel.sys;" ::: "memory");
-#endif
     for (int i = r0; i < r1; ++i) {
       const ArRun r = run(i);
       if (!r.out_plain) continue;

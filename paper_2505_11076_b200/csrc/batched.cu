@@ -4,20 +4,26 @@
 // The decode engine (engine.cu) carries at most 4 tokens per launch (4 tokens x 2 digit planes =
 // the 8 columns of one IMMA.16832); larger batches used to re-stream the weights once per group of
 // 4.  Here every extracted A fragment (one LOP3 per 4 weights, the engine's 2^t-bit trick) feeds
-// NJ = ceil(batch / 4) IMMAs, one per token group, so the weights are read once per stage:
+// NJ = ceil(batch / 4) IMMAs, one per token group, so the weights are read once per stage.  Four
+// kernels per layer, each launched with programmatic dependent launch (it loads its sign words and
+// scales while the previous kernel drains, then griddepcontrol.wait):
 //
-//   quantize   x (or the fp32 split partials of the previous stage, times its row scale) ->
-//              per (token, 256-column chunk) 13-bit grid X = rint(u * 2^F * kQScale) (the
-//              engine's numerics: |X| <= 4079), two balanced int8 digit planes of X * 2^(3-t)
-//              in the IMMA B-fragment layout, F and T = sum X per (chunk, token)
-//   gemv       one warp per 16-row block; for each 256-column chunk of its K range: the tiled
-//              sign words (uint4 per lane), 8 k-blocks x NJ IMMAs (u8 x s8 -> s32), then
-//              P = (s0 + 256 s1) / 4 - T (exact) and y += P / (2^F kQScale) in fp32;
-//              K is split over gridDim.y CTAs (fp32 partials, summed in split order)
-//   finalize   y = a (.) sum of the partials -> output dtype; non-finite / fp16-overflow status
+//   quantize   x, or the fp32 split partials of the first GEMV times mid -> per (token, 256-column
+//              chunk) 13-bit grid X = rint(u * 2^F * kQScale) (the engine's numerics: |X| <=
+//              4079), two balanced int8 digit planes of X * 2^(3-t) in the IMMA B-fragment
+//              layout, F and T = sum X per (chunk, token)
+//   gemv       one warp per one or two 16-row blocks; per 256-column chunk of its K range: the
+//              tiled sign words (uint4 per lane, two chunks ahead), the chunk's B fragments from a
+//              shared-memory ring filled by bulk copy, 8 k-blocks x NJ IMMAs (u8 x s8 -> s32),
+//              P = (s0 + 256 s1) / 4 - T (exact) and y += P / (2^F kQScale) in fp32; K split
+//              over gridDim.y CTAs (fp32 partials, summed in split order)
+//   finalize   y = a (.) sum of the partials -> output dtype (status bits: non-finite, fp16
+//              overflow), and the first-GEMV fragments of the layers that read y next (a layer
+//              chain needs the standalone quantize only for inputs from outside it)
 //
-// All layouts are the decode GEMV's (dbf_tile_signs); B fragments: bfrag[c][kb][j][lane] (uint2),
-// lane = 8 * (token % 4) + 4 * plane + tig, bytes 0..3 = k 4*tig..+3, 4..7 = k 16+4*tig..+3.
+// Sign words: the decode GEMV's tiled layout (dbf_tile_signs).  B fragments: bfrag[c][kb][j][lane]
+// (uint2), j = token / 4, lane = 8 * (token % 4) + 4 * plane + tig, bytes 0..3 = k 4*tig..+3,
+// 4..7 = k 16+4*tig..+3.
 #include <algorithm>
 #include "common.cuh"
 #include "sm100.cuh"

@@ -240,3 +240,38 @@ def test_batched_plan_groups_above_32_tokens():
         outs.append(plan.buffers[plan.output_buffer].double().cpu().numpy())
     assert len(plan._bgroups) == 2
     assert rel_max(outs[1], outs[0]) <= TOL and rel_norm(outs[1], outs[0]) <= TOL
+
+
+def test_batched_plan_fan_out_and_in_place():
+    """Dataflow corner cases of the chained batched plan, bitwise against per-layer calls: one
+    output read by five later layers (four get their fragments from the writer's finalize, the fifth
+    quantizes on its own), and a layer writing its own input buffer."""
+    import torch
+    from paper_2505_11076_b200.plan import DecodePlan, PlanOp
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(150)
+    w = 1024
+    layers = [P.random_device_layer(w, 512, w, generator=g) for _ in range(7)]
+    bufs = [torch.randn((6, w), generator=g, device="cuda").half()] + [
+        torch.zeros((6, w), dtype=torch.half, device="cuda") for _ in range(7)]
+    ops = [PlanOp(0, 0, 1, "src")] + [PlanOp(1 + i, 1, 2 + i, f"r{i}") for i in range(5)] + [PlanOp(6, 7, 7, "inplace")]
+    plan = DecodePlan(layers, ops, bufs, input_buffer=0, output_buffer=7).use_batched()
+    frags, readers, standalone, deps = plan._bchain
+    assert len(readers[0]) == 4 and 5 in standalone and 6 in standalone
+    x = bufs[0].clone()
+    x7 = torch.randn((6, w), generator=g, device="cuda").half()
+    bufs[7].copy_(x7)
+    plan._eager()
+    torch.cuda.synchronize()
+    chained = [b.clone() for b in bufs]
+    bufs[0].copy_(x)
+    for b in bufs[1:7]:
+        b.zero_()
+    bufs[7].copy_(x7)
+    for op in ops:
+        P.forward_batched(bufs[op.src], layers[op.layer], out=bufs[op.dst])
+    torch.cuda.synchronize()
+    for i in range(8):
+        assert torch.equal(chained[i], bufs[i]), i
+    assert not torch.equal(chained[7], x7)

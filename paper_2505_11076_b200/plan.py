@@ -167,14 +167,15 @@ class DecodePlan:
             for l in self.layers)
 
     def default_path(self) -> str:
-        """The static path rule for a token batch: the decode engine for 1-2 tokens, the batched
-        kernels for 3-64 (one weight pass per group of <= 32), the tcgen05 prefill chain above
-        (when its layout is available).  Measured (ms per step): engine / batched
-        7B 2 tokens 1.55 / 1.89, 3 tokens 2.22 / 1.90; 70B 2 tokens 13.0 / 9.6 (use_fastest picks
-        the batched kernels there, beyond the 10 % margin); batched / prefill chain 7B 32 tokens
-        4.2 / 8.7, 70B 32 tokens 30.4 / 62.8, 13B 64 tokens ~11.6 / 12.3."""
+        """The static path rule for a token batch: the decode engine for 1 token (and 2 below 8 GB
+        of weights per step), the batched kernels for 2-64 tokens (one weight pass per group of
+        <= 32), the tcgen05 prefill chain above (when its layout is available).  Measured
+        (ms per step): engine / batched 7B 2 tokens 1.55 / 1.89, 3 tokens 2.22 /
+        1.90; 13B 2 tokens 2.38 / 2.57; 70B 2 tokens 13.0 / 9.6; batched / prefill chain 7B 32
+        tokens 4.2 / 8.7, 70B 32 tokens 30.4 / 62.8, 13B 64 tokens 11.5 / 11.9."""
         batch = int(self.buffers[self.input_buffer].shape[0])
-        if batch <= 2:
+        if batch == 1 or (batch == 2 and self.bytes_per_step() < 8e9):
+            # 2 tokens: the engine wins on 7B / 13B, the batched kernels on 70B (17.6 GB)
             return "engine"
         if batch <= 2 * BATCHED_MAX_TOKENS:
             return "batched"

@@ -378,7 +378,8 @@ size_t dbf_forward_batched_frag_workspace_bytes(int64_t n, int64_t k, int64_t m,
 /* Diagnostics (builds with -DDBF_BATCHED_TRACE, tools/batched_trace.py; DBF_ERR_UNSUPPORTED
  * otherwise): reset the per-launch trace slots (restart_slots != 0 also restarts their numbering),
  * and copy n slots of {kind (1 quantize, 2 GEMV, 3 finalize), first CTA start, last return from
- * the grid dependency wait, last warp end} (%globaltimer ns). */
+ * the grid dependency wait, last warp end, last mid-kernel mark (quantize: inputs loaded;
+ * finalize: y stored)} (%globaltimer ns). */
 int dbf_batched_debug_reset(int restart_slots);
 int dbf_batched_debug_trace(unsigned long long* host, int n);
 int dbf_forward_batched_frag(const void* A_tiled, const void* B_tiled, const void* a,

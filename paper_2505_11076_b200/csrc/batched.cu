@@ -82,7 +82,7 @@ __device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddep
 // Diagnostics build only (-DDBF_BATCHED_TRACE, tools/batched_trace.py): per launch slot, the
 // earliest CTA start, the latest return from grid_wait and the latest CTA end (%globaltimer ns)
 #ifdef DBF_BATCHED_TRACE
-__device__ unsigned long long g_btrace[8192][4];
+__device__ unsigned long long g_btrace[8192][5];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -96,7 +96,10 @@ __device__ __forceinline__ unsigned long long gtime() {
   }
 #define BT_END(slot)                                                           \
   if ((slot) >= 0 && (threadIdx.x & 31) == 0) atomicMax(&g_btrace[slot][3], gtime());
+#define BT_MARK(slot)                                                          \
+  if ((slot) >= 0 && (threadIdx.x & 31) == 0) atomicMax(&g_btrace[slot][4], gtime());
 #else
+#define BT_MARK(slot)
 #define BT_START(slot)
 #define BT_WAITED(slot)
 #define BT_END(slot)
@@ -248,6 +251,39 @@ __device__ __forceinline__ void sum_splits4(const float* part, int splits, int64
         for (int s = 0; s < splits; ++s) v[e] += __ldcg(part + (size_t)s * stride + row_off + j0 + e);
   }
 }
+// 16-byte L2 load (ld.global.cg) the compiler keeps in program order: the two groups' loads of
+// every split below go out back to back (left to the compiler, they went out two or three at a
+// time, one L2 round trip each: 2.3 us to load a chunk's partials, tools/batched_trace.py)
+__device__ __forceinline__ float4 ldcg4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+// this lane's two groups (columns j0 .. j0+3 for j0 = ja, jb) of token row t summed over the
+// splits in split order; all loads issued before the first add
+__device__ __forceinline__ void sum_splits4x2(const float* part, int splits, int64_t stride, int64_t row_off, int ja,
+                                              int jb, int cols, float (&va)[4], float (&vb)[4]) {
+  if (ja + 3 < cols && jb + 3 < cols) {
+    float4 pa[kMaxSplits], pb[kMaxSplits];
+#pragma unroll
+    for (int s = 0; s < kMaxSplits; ++s) {
+      if (s < splits) {
+        pa[s] = ldcg4(part + (size_t)s * stride + row_off + ja);
+        pb[s] = ldcg4(part + (size_t)s * stride + row_off + jb);
+      }
+    }
+    va[0] = va[1] = va[2] = va[3] = vb[0] = vb[1] = vb[2] = vb[3] = 0.f;
+#pragma unroll
+    for (int s = 0; s < kMaxSplits; ++s)
+      if (s < splits) {
+        va[0] += pa[s].x, va[1] += pa[s].y, va[2] += pa[s].z, va[3] += pa[s].w;
+        vb[0] += pb[s].x, vb[1] += pb[s].y, vb[2] += pb[s].z, vb[3] += pb[s].w;
+      }
+    return;
+  }
+  sum_splits4(part, splits, stride, row_off, ja, cols, va);
+  sum_splits4(part, splits, stride, row_off, jb, cols, vb);
+}
 
 // One warp per (chunk, token): 64 groups of 4 columns, lane holds groups lane and lane + 32.
 __global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, FragView fv, int nj) {
@@ -272,12 +308,13 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, FragView
     return;
   }
   float u[2][4];
+  if (in.part)  // the previous stage's split partials (rows padded to 4 floats), in split order
+    sum_splits4x2(in.part, in.splits, in.part_stride, (int64_t)t * in.ldx, c * kChunkCols + 4 * lane,
+                  c * kChunkCols + 4 * (lane + 32), in.cols, u[0], u[1]);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j0 = c * kChunkCols + 4 * (lane + 32 * h);  // this lane's group of 4 columns
     if (in.part) {
-      // the previous stage's split partials (rows padded to 4 floats), summed in split order
-      sum_splits4(in.part, in.splits, in.part_stride, (int64_t)t * in.ldx, j0, in.cols, u[h]);
     } else if (j0 + 3 < in.cols && in.x_dtype == DBF_F16 && ((in.ldx | (int64_t)(uintptr_t)in.x / 2) & 3) == 0) {
       const uint2 r = __ldg((const uint2*)((const __half*)in.x + (int64_t)t * in.ldx + j0));
       const float2 lo = __half22float2(*(const __half2*)&r.x), hi = __half22float2(*(const __half2*)&r.y);
@@ -289,6 +326,7 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(QuantIn in, FragView
 #pragma unroll
     for (int e = 0; e < 4; ++e) u[h][e] *= sc[h][e];
   }
+  BT_MARK(in.tslot)
   emit_chunk(u, c, t, fv, in.tpad, nj);
   BT_END(in.tslot)
 }
@@ -493,12 +531,14 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs f) {
   const bool store = k == 0;
   float yr[2][4];  // the output as stored (what a later reader of y sees), 0 past the rows
   unsigned bad = 0;
+  float vs[2][4];
+  sum_splits4x2(f.part, f.splits, f.part_stride, (int64_t)t * f.ldp, c * kChunkCols + 4 * lane,
+                c * kChunkCols + 4 * (lane + 32), f.rows, vs[0], vs[1]);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j0 = c * kChunkCols + 4 * (lane + 32 * h);
     const bool full = j0 + 3 < f.rows;
-    float v[4];
-    sum_splits4(f.part, f.splits, f.part_stride, (int64_t)t * f.ldp, j0, f.rows, v);
+    const float (&v)[4] = vs[h];
     float w[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -556,6 +596,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs f) {
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0 && f.status) atomicOr(f.status, bad);
   }
+  BT_MARK(f.tslot)
   if (f.ncons == 0) {
     BT_END(f.tslot)
     return;
@@ -774,8 +815,8 @@ int dbf_forward_batched(const void* A_tiled, const void* B_tiled, const void* a,
 // restart slot numbering, and copy n slots (kind, first CTA start, last grid_wait exit, last end)
 int dbf_batched_debug_reset(int restart_slots) {
 #ifdef DBF_BATCHED_TRACE
-  static unsigned long long init[8192][4];
-  for (int i = 0; i < 8192; ++i) init[i][0] = 0, init[i][1] = ~0ull, init[i][2] = 0, init[i][3] = 0;
+  static unsigned long long init[8192][5];
+  for (int i = 0; i < 8192; ++i) init[i][0] = 0, init[i][1] = ~0ull, init[i][2] = 0, init[i][3] = 0, init[i][4] = 0;
   if (restart_slots) batched::g_next_slot = 0;
   return cudaMemcpyToSymbol(batched::g_btrace, init, sizeof(init)) == cudaSuccess ? DBF_OK : DBF_ERR_CUDA;
 #else
@@ -786,8 +827,8 @@ int dbf_batched_debug_reset(int restart_slots) {
 int dbf_batched_debug_trace(unsigned long long* host, int n) {
 #ifdef DBF_BATCHED_TRACE
   if (n > 8192) n = 8192;
-  if (cudaMemcpyFromSymbol(host, batched::g_btrace, (size_t)n * 32) != cudaSuccess) return DBF_ERR_CUDA;
-  for (int i = 0; i < n; ++i) host[4 * i] = (unsigned long long)batched::g_slot_kind[i];
+  if (cudaMemcpyFromSymbol(host, batched::g_btrace, (size_t)n * 40) != cudaSuccess) return DBF_ERR_CUDA;
+  for (int i = 0; i < n; ++i) host[5 * i] = (unsigned long long)batched::g_slot_kind[i];
   return DBF_OK;
 #else
   (void)host, (void)n;

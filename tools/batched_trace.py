@@ -28,17 +28,19 @@ torch.cuda.synchronize()
 assert _lib.lib.dbf_batched_debug_reset(0) == 0
 plan.replay()
 torch.cuda.synchronize()
-buf = np.zeros((8192, 4), dtype=np.uint64)
+buf = np.zeros((8192, 5), dtype=np.uint64)
 assert _lib.lib.dbf_batched_debug_trace(buf.ctypes.data, 8192) == 0
 used = np.nonzero(buf[:, 3])[0]
 t = buf[used].astype(np.float64)
 t0 = t[:, 1].min()
 names = {1: "quantize", 2: "gemv", 3: "finalize"}
-rows = sorted(zip(used, t[:, 0], (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3, (t[:, 3] - t0) / 1e3), key=lambda r: r[2])
-print("slot kind      start   waited  end     dur    gap(start - latest earlier end)")
+mark = np.where(t[:, 4] > 0, (t[:, 4] - t0) / 1e3, np.nan)
+rows = sorted(zip(used, t[:, 0], (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3, mark, (t[:, 3] - t0) / 1e3),
+              key=lambda r: r[2])
+print("slot kind      start   waited  mark    end     dur    gap(start - latest earlier end)")
 latest = 0.0
-for s, k, st, wt, en in rows:
-    print(f"{s:5d} {names.get(int(k), k):9s} {st:7.2f} {wt:7.2f} {en:7.2f} {en - st:6.2f} {st - latest:7.2f}")
+for s, k, st, wt, mk, en in rows:
+    print(f"{s:5d} {names.get(int(k), k):9s} {st:7.2f} {wt:7.2f} {mk:7.2f} {en:7.2f} {en - st:6.2f} {st - latest:7.2f}")
     latest = max(latest, en)
-span = max(r[4] for r in rows)
+span = max(r[5] for r in rows)
 print(f"{len(rows)} launches, span {span:.1f} us, {span / blocks:.1f} us per block")

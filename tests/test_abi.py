@@ -123,3 +123,35 @@ def test_python_struct_mirrors_match_the_c_layout(tmp_path):
         assert c[(t, "size")] == dt.itemsize, t
         for n in dt.names:
             assert c[(t, n)] == dt.fields[n][1], (t, n)
+
+
+def test_batched_entry_points_validate_without_a_gpu():
+    """The single-pass batched decode entry points (csrc/batched.cu): sizes on the host, argument
+    and shape errors before any launch."""
+    L = _lib.lib
+    # up to 32 tokens; 0 (invalid) beyond
+    assert L.dbf_forward_batched_workspace_bytes(4096, 2048, 4096, 16) > 0
+    assert L.dbf_forward_batched_workspace_bytes(4096, 2048, 4096, 33) == 0
+    assert L.dbf_forward_batched_workspace_bytes(4096, 2048, 4096, 0) == 0
+    # fragments: chunks(cols) x 8 k-blocks x (tokens/4) x 32 lanes x 8 B, plus F and T per chunk
+    # and token slot, rounded to 256 B
+    for cols, batch in [(4096, 16), (300, 3), (11008, 32)]:
+        tpad = -(-batch // 4) * 4
+        ch = -(-cols // 256)
+        want = ch * 8 * (tpad // 4) * 32 * 8 + 2 * ch * tpad * 4
+        assert L.dbf_batched_frag_bytes(cols, batch) == -(-want // 256) * 256
+    # the full call needs more workspace than the chained one (it quantizes x itself)
+    assert L.dbf_forward_batched_workspace_bytes(4096, 2048, 4096, 8) > L.dbf_forward_batched_frag_workspace_bytes(
+        4096, 2048, 4096, 8)
+    args = [None, None, None, None, None, 0, 64, 32, 64, None, 0, 4, 64, None, 0, 64, None, 0, None, None]
+    assert L.dbf_forward_batched(*args) == _lib.ERR_INVALID_ARGUMENT
+    dummy = 0x1000
+    ok = [dummy, dummy, dummy, dummy, dummy, 0, 64, 32, 64, dummy, 0, 4, 64, dummy, 0, 64, None, 0, None, None]
+    assert L.dbf_forward_batched(*(ok[:11] + [33] + ok[12:])) == _lib.ERR_UNSUPPORTED   # > 32 tokens
+    assert L.dbf_forward_batched(*(ok[:12] + [63] + ok[13:])) == _lib.ERR_SHAPE          # ldx < m
+    assert L.dbf_forward_batched(*ok) == _lib.ERR_WORKSPACE                             # no workspace
+    assert L.dbf_batched_quantize(None, 0, 64, 4, 64, None, 0, None, None) == _lib.ERR_INVALID_ARGUMENT
+    assert L.dbf_batched_quantize(dummy, 0, 32, 4, 64, None, 0, dummy, None) == _lib.ERR_SHAPE
+    fr = [dummy, dummy, dummy, dummy, 0, 64, 32, 64, dummy, 4, dummy, 0, 64, None, 5, None, 0, None, None]
+    assert L.dbf_forward_batched_frag(*fr) == _lib.ERR_INVALID_ARGUMENT                 # consumers=NULL, n=5
+    assert L.dbf_forward_batched_frag(*(fr[:13] + [dummy, 5] + fr[15:])) == _lib.ERR_UNSUPPORTED  # > 4 consumers

@@ -65,6 +65,11 @@ class DecodePlan:
     def kernel_launches_per_step(self) -> int:
         if self.engine is not None:
             return self.engine.kernel_launches_per_step()
+        if getattr(self, "_mode", None) == "batched":
+            # per layer GEMV, quantize, GEMV, finalize (+ a quantize for inputs from outside the
+            # chain); per group of <= 32 tokens
+            groups = self._bgroups or [self]
+            return sum(4 * len(g.ops) + len(g._bchain[2]) for g in groups)
         return 2 * len(self.ops)  # one GEMV launch per stage (B, then A)
 
     # ---- execution --------------------------------------------------------------------------

@@ -127,6 +127,9 @@ def test_batched_plan_chain_matches_layer_kernels(batch):
     g.manual_seed(40 + batch)
     plan = llama_decode_plan("llama2-7b", bpw=2.0, batch=batch, blocks=2, generator=g)
     assert plan.default_path() == "batched"
+    # four kernels per layer, plus a quantize for each of the first block's q/k/v (their input
+    # comes from outside the chain)
+    assert plan.use_batched().kernel_launches_per_step() == 4 * 14 + 3
     x = torch.randn(plan.buffers[plan.input_buffer].shape, generator=g, device="cuda").half()
     outs = []
     for use in (plan.use_layer_kernels, plan.use_batched):

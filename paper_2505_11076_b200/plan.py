@@ -44,6 +44,40 @@ class PlanOp:
     name: str = ""
 
 
+def batched_dataflow(ops, max_readers: int = 4):
+    """Dataflow of a batched chain (DecodePlan.use_batched) from the op list alone.
+
+    readers[w]: the ops whose first-GEMV fragments op w's finalize writes -- every op reading the
+    buffer w wrote, until the next write to it (at most max_readers; more read it on their own).
+    standalone: the ops that quantize their input themselves (input from outside the chain, or a
+    reader beyond max_readers).  deps[i]: the ops op i must follow when independent ops run on
+    concurrent streams -- the producer of its input, the previous writer of its output buffer and
+    every op that read that buffer's previous contents (chained readers read fragments, not the
+    buffer; they are ordered conservatively)."""
+    last_writer, readers, standalone = {}, {i: [] for i in range(len(ops))}, set()
+    for i, op in enumerate(ops):
+        w = last_writer.get(op.src)
+        if w is None or len(readers[w]) >= max_readers:
+            standalone.add(i)
+        else:
+            readers[w].append(i)
+        last_writer[op.dst] = i
+    deps, last_w, reads_since = [], {}, {}
+    for i, op in enumerate(ops):
+        d = set()
+        if op.src in last_w:
+            d.add(last_w[op.src])
+        if op.dst in last_w:
+            d.add(last_w[op.dst])
+        d.update(reads_since.get(op.dst, ()))
+        d.discard(i)
+        deps.append(sorted(d))
+        reads_since.setdefault(op.src, []).append(i)
+        last_w[op.dst] = i
+        reads_since[op.dst] = []
+    return readers, standalone, deps
+
+
 @dataclass
 class DecodePlan:
     layers: list
@@ -125,35 +159,11 @@ class DecodePlan:
         return self
 
     def _batched_chain(self, batch: int):
-        """Dataflow of the batched chain: every op's input fragments are written by the finalize
-        of the op that last wrote its input buffer (up to 4 readers per writer), or -- for inputs
-        from outside the plan, or a fifth reader -- quantized on their own just before the op."""
+        """Fragment buffers (one per op: its first-GEMV input) and the dataflow of the batched
+        chain (batched_dataflow)."""
         device = self.buffers[0].device
-        last_writer, readers, standalone = {}, {i: [] for i in range(len(self.ops))}, set()
-        for i, op in enumerate(self.ops):
-            w = last_writer.get(op.src)
-            if w is None or len(readers[w]) >= 4:
-                standalone.add(i)
-            else:
-                readers[w].append(i)
-            last_writer[op.dst] = i
+        readers, standalone, deps = batched_dataflow(self.ops)
         frags = [batched_frag(self.layers[op.layer].m_dim, batch, device) for op in self.ops]
-        # dependencies for concurrent streams: the op that produced the input (its fragments), the
-        # previous writer of the output buffer, and every op that read the output buffer's
-        # previous contents (standalone readers read it; chained ones are ordered conservatively)
-        deps, last_w, reads_since = [], {}, {}
-        for i, op in enumerate(self.ops):
-            d = set()
-            if op.src in last_w:
-                d.add(last_w[op.src])
-            if op.dst in last_w:
-                d.add(last_w[op.dst])
-            d.update(reads_since.get(op.dst, ()))
-            d.discard(i)
-            deps.append(sorted(d))
-            reads_since.setdefault(op.src, []).append(i)
-            last_w[op.dst] = i
-            reads_since[op.dst] = []
         return frags, readers, standalone, deps
 
     def use_prefill(self):

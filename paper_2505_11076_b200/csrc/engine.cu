@@ -12,13 +12,14 @@
 //   16 compute warps     warp w OWNS the 256-column chunks c = w, w+16, ... of the run's input.
 //                        Per chunk it polls the chunk's LL words straight from L2 (streaming: a
 //                        chunk is processed as soon as ITS producers are done), quantizes the 256
-//                        values to a 22-bit grid relative to the CHUNK's max |value| (warp-local:
-//                        no CTA-wide barrier, no global max), builds the int8 digit-plane B
-//                        fragments, and runs the int8 tensor-core sign GEMV of every unit of the
+//                        values to a 13-bit grid relative to the CHUNK's max |value| (|X| <= 4079;
+//                        warp-local: no CTA-wide barrier, no global max), builds the two int8
+//                        digit-plane B fragments, and runs the int8 tensor-core sign GEMV of every unit of the
 //                        run against that chunk.  The chunk's exact integer sum is scaled by
 //                        2^-F_c and accumulated in fp32 registers, per unit, in chunk order.
-//   finalizer warp       sums the 16 warps' partials of each unit in warp order (deterministic),
-//                        applies the output scale and publishes fp16 outputs as LL words.
+//   finalizer warps      warp 15 - u sums the 16 warps' partials of unit u in warp order
+//                        (deterministic), applies the output scale and publishes fp16 outputs as
+//                        LL words (plain stores for outputs no later stage reads).
 //
 // Inter-CTA dependencies use an LL ("low latency", as in NCCL's LL protocol) handoff: each value
 // is one 32-bit word {fp16 value, 16-bit epoch}; consumers poll the words themselves, so there is

@@ -80,6 +80,7 @@ struct Params {
   int kb_per_split;
   float* part;
   int ks_global;           // kscale read from global memory (L1-cached) when the smem copy does not fit
+  int tma_out;             // epilogue: fp16 tile staged in shared memory, one TMA store (out_map)
 };
 
 template <int NST>
@@ -101,7 +102,7 @@ static_assert(MH * BN + STAGES * kAColsPerStage <= kTmemCols, "TMEM budget (A sl
 static_assert(MH * kSmallBN + kSmallStages * kAColsPerStage <= kTmemCols, "TMEM budget (small tiles)");
 template <int TBN, int NST>
 inline size_t smem_bytes_for(int num_kb, bool kscale) {
-  return 1024 /*align slack*/ + (size_t)NST * TBN * BK * 2 + sizeof(BarriersT<NST>) + 64 +
+  return 1024 /*align slack*/ + (size_t)NST * TBN * BK * 2 + sizeof(BarriersT<NST>) + 64 + 16 +
          (kscale ? (size_t)num_kb * BK * 2 : 0);
 }
 inline size_t smem_bytes(int num_kb, bool kscale) { return smem_bytes_for<BN, STAGES>(num_kb, kscale); }
@@ -117,7 +118,8 @@ __device__ __forceinline__ void expand_word(uint32_t w, const uint32_t* ks, uint
 
 template <bool KSCALE, int TBN = BN, int NST = STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-    sign_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const Params p) {
+    sign_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap out_map,
+                     const Params p) {
   // tile configuration: the namespace defaults, or the small-token tiles
   constexpr int BN = TBN, STAGES = NST;
   constexpr int kActStageBytes = BN * BK * 2;
@@ -127,8 +129,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* act = smem;
   Barriers& bar = *reinterpret_cast<Barriers*>(smem + (size_t)STAGES * kActStageBytes);
-  uint32_t* ks_smem = reinterpret_cast<uint32_t*>(smem + (size_t)STAGES * kActStageBytes + sizeof(Barriers) + 64);
+  uint32_t* ks_smem =  // 16-byte aligned (uint4 copies)
+      reinterpret_cast<uint32_t*>(smem + (((size_t)STAGES * kActStageBytes + sizeof(Barriers) + 64 + 15) & ~(size_t)15));
 
+#ifdef DBF_PREFILL_TRACE
+  const long long cta_c0_ = clock64();
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = blockIdx.x * BM;
   const int tok0 = blockIdx.y * BN;
@@ -148,11 +154,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_alloc<kTmemCols>(&bar.tmem_base);
   if (KSCALE && !p.ks_global) {
     // kscale as fp16 pairs, zero beyond K (those columns meet TMA zero-fill anyway)
+    // 8 columns (4 pairs) per thread and load: one round trip for K <= 8 * kThreads
     const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
-    for (int i = threadIdx.x; i < p.num_kb * (BK / 2); i += kThreads) {
-      const int c = 2 * i;
-      const uint32_t lo = c < p.K ? src[c] : 0u, hi = c + 1 < p.K ? src[c + 1] : 0u;
-      ks_smem[i] = lo | (hi << 16);
+    const bool vec = ((uintptr_t)p.kscale & 15) == 0;
+    for (int i = threadIdx.x; i < p.num_kb * (BK / 8); i += kThreads) {
+      const int c = 8 * i;
+      uint4 u;
+      if (vec && c + 8 <= p.K) {
+        u = __ldg(reinterpret_cast<const uint4*>(src + c));
+      } else {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int cq = c + 2 * q;
+          w[q] = (cq < p.K ? (uint32_t)src[cq] : 0u) | ((cq + 1 < p.K ? (uint32_t)src[cq + 1] : 0u) << 16);
+        }
+        u = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      reinterpret_cast<uint4*>(ks_smem)[i] = u;
     }
   }
   tc_fence_before();
@@ -160,6 +179,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
   const bool tracing = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
+  // programmatic dependent launch: the next kernel on the stream may start its own setup on SMs as
+  // they free up; everything that reads the activations or writes the output waits for the
+  // previous kernel (griddepcontrol.wait) -- the setup above touches layer constants only
+  asm volatile("griddepcontrol.launch_dependents;");
+#ifdef DBF_PREFILL_TRACE
+  unsigned long long cta_t0 = 0;
+  long long* cslot = nullptr;
+  {
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (p.trace && cta < 4096) cslot = p.trace + 6 * 4096 + 16 * (size_t)cta;
+  }
+#define CT(i) do { if (cslot) cslot[i] = clock64(); } while (0)
+  if (threadIdx.x == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(cta_t0));
+    if (cslot) cslot[4] = cta_c0_;
+  }
+  if (threadIdx.x == 0) CT(5);
+#else
+#define CT(i) do { } while (0)
+#endif
 
   if (warp == 0 || warp == 2 || warp == 3) {
     // ---------------- TMA producers ----------------
@@ -172,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane < kPerWarp) {
       const int prod = (warp == 0 ? 0 : warp - 1) * kPerWarp + lane;
       const uint64_t pol = policy_evict_last();  // activations are re-read by every row tile
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int kb = kb0 + prod; kb < kb1; kb += kIssuers) {
         const int s = (kb - kb0) % STAGES;
         const uint32_t ph = ((kb - kb0) / STAGES) & 1;
@@ -193,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bar.full_a[s], ph);
         tc_fence_after();
         if (tracing) p.trace[4 * p.num_kb + kb] = clock64();
+        if (kb == kb0) CT(6);
         const uint32_t a_base = tmem + kACol0 + s * kAColsPerStage;
         const uint32_t b_base = smem_u32(act + (size_t)s * kActStageBytes);
 #pragma unroll
@@ -206,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&bar.empty[s]);
       }
       mma_commit(&bar.acc_full);
+      CT(7);
     }
   } else if (warp >= kExpWarp0) {
     // ---------------- sign expanders + epilogue ----------------
@@ -305,13 +347,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < 4; ++i) q[i] = nq[i];
     }
     // epilogue: this warp stores tokens [half*64, half*64+64) of its 32 rows (accumulator mh)
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel may still read the output
     if (lane == 0) mbar_wait(&bar.acc_full, 0);
+    if (threadIdx.x == 32 * kExpWarp0) CT(8);
     __syncwarp();
     tc_fence_after();
     const float rs = (live && p.rscale) ? __half2float(p.rscale[grow]) : 1.f;
+    if (p.tma_out) {
+      // the ring is idle once the accumulator is complete: stage the fp16 tile there as
+      // [token][row] (the output's layout) and write it with one TMA store (clipped at rows / T)
+      __half* stile = reinterpret_cast<__half*>(smem);
+#pragma unroll 1
+      for (int c = 0; c < BN / 64; ++c) {
+        const int col = half * (BN / 2) + c * 32;
+        if (tok0 + col >= p.T) break;
+        uint32_t acc[32];
+        tmem_ld32(tmem + lane_addr + kAccCol + mh * BN + col, acc);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stile[(col + j) * BM + r] = __float2half_rn(__uint_as_float(acc[j]) * rs);
+      }
+      fence_proxy_async_smem();
+      if (threadIdx.x == 32 * kExpWarp0) CT(10);
+      asm volatile("bar.sync 1, %0;" ::"n"(kExpWarps * 32) : "memory");
+      if (threadIdx.x == 32 * kExpWarp0) {
+        CT(11);
+        tma_store_2d(&out_map, stile, row0, tok0);
+        bulk_commit_group();
+        bulk_wait_group_read0();
+        CT(12);
+      }
+    }
     float* part = p.part ? p.part + (size_t)blockIdx.z * p.T * p.rows : nullptr;
 #pragma unroll 1
-    for (int c = 0; c < BN / 64; ++c) {
+    for (int c = 0; c < (p.tma_out ? 0 : BN / 64); ++c) {
       const int col = half * (BN / 2) + c * 32;
       if (tok0 + col >= p.T) break;  // columns past the tokens present (the MMA N may be smaller)
       uint32_t acc[32];
@@ -328,9 +397,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (threadIdx.x == 32 * kExpWarp0) CT(9);
   }
   tc_fence_before();
   __syncthreads();
+#ifdef DBF_PREFILL_TRACE
+  if (threadIdx.x == 0 && p.trace) {
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (cta < 4096) {
+      unsigned long long t1, smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      asm volatile("{.reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r;}" : "=l"(smid));
+      long long* c = cslot;
+      c[0] = (long long)cta_t0, c[1] = (long long)t1, c[2] = clock64(), c[3] = (long long)smid;
+    }
+  }
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -366,6 +448,19 @@ static int make_act_map(CUtensorMap* map, const void* act, int64_t T, int64_t K,
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(act), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? DBF_OK : DBF_ERR_CUDA;
+}
+
+// out: T x rows fp16, row stride ldo elements; box = one BM x BN tile
+static int make_out_map(CUtensorMap* map, void* out, int64_t T, int64_t rows, int64_t ldo) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return DBF_ERR_CUDA;
+  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)T};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldo * 2};
+  const cuuint32_t box[2] = {BM, BN};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? DBF_OK : DBF_ERR_CUDA;
 }
 
@@ -445,10 +540,21 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
       p.part = split_ws;
     }
   }
+  // TMA-store epilogue: full-size tiles writing fp16 with a 16-byte row stride (the staged tile,
+  // BN x BM fp16 = 64 KB, lives in the activation ring)
+  CUtensorMap omap;
+  std::memset(&omap, 0, sizeof(omap));
+  p.tma_out = 0;
+  if (!small && splits == 1 && (ldo * 2) % 16 == 0 && ((uintptr_t)out & 15) == 0 &&
+      (size_t)STAGES * BN * BK * 2 >= (size_t)BM * BN * 2) {
+    st = make_out_map(&omap, out, T, rows, ldo);
+    if (st != DBF_OK) return st;
+    p.tma_out = 1;
+  }
   p.trace = nullptr;
 #ifdef DBF_PREFILL_TRACE  // diagnostics build only (tools/prefill_trace.py)
   {
-    if (!trace_buf) cudaMalloc(&trace_buf, 8 * 6 * 4096);
+    if (!trace_buf) cudaMalloc(&trace_buf, 8 * 24 * 4096);
     p.trace = trace_buf;
   }
 #endif
@@ -466,14 +572,16 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, map, p);
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kern, map, omap, p);
   };
   cudaError_t e;
   if (small)
@@ -503,6 +611,17 @@ int dbf_prefill_debug_trace(long long* host, int n) {
   return cudaMemcpy(host, prefill::trace_buf, 8 * (size_t)n, cudaMemcpyDeviceToHost) == cudaSuccess ? DBF_OK
                                                                                                     : DBF_ERR_CUDA;
 }
+
+#ifdef DBF_PREFILL_TRACE
+// debug: per-CTA {globaltimer start, end, clock end, smid, clock start, setup done, first MMA, last commit,
+// accumulator seen, -} of the last traced launch
+int dbf_prefill_debug_ctas(long long* host, int n) {
+  if (!prefill::trace_buf) return DBF_ERR_UNSUPPORTED;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, prefill::trace_buf + 6 * 4096, 8 * (size_t)n, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? DBF_OK : DBF_ERR_CUDA;
+}
+#endif
 
 int64_t dbf_prefill_ld(int64_t cols) { return ceil_div(cols, 64) * 64; }
 

@@ -99,6 +99,7 @@ struct __align__(8) BarriersT {
 constexpr int kSmallBN = 64, kSmallStages = 12;
 
 static_assert(MH * BN + STAGES * kAColsPerStage <= kTmemCols, "TMEM budget (A slots)");
+static_assert(MH == 1, "the TMA-store epilogue stages one 128-row accumulator per tile");
 static_assert(MH * kSmallBN + kSmallStages * kAColsPerStage <= kTmemCols, "TMEM budget (small tiles)");
 template <int TBN, int NST>
 inline size_t smem_bytes_for(int num_kb, bool kscale) {
@@ -152,6 +153,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&act_map);
   }
   if (warp == 1) tmem_alloc<kTmemCols>(&bar.tmem_base);
+  // expanders: the first 8 K blocks' sign words and the epilogue's row scales are layer constants,
+  // requested before the setup barrier so their HBM latency overlaps it
+  uint4 q[4];
+  __half rs_pre[2][2];  // converted where used, so no thread waits for them at the barrier
+  if (warp >= kExpWarp0) {
+    const int sub = warp & 3, mh = ((warp - kExpWarp0) >> 2) % MH;
+    const int grow = row0 + mh * UM + sub * 32 + lane;
+    const bool live = grow < p.rows;
+    const uint4* wrow = reinterpret_cast<const uint4*>(p.words + (int64_t)(live ? grow : 0) * p.pitch);
+    const int nquads = (p.num_kb + 1) >> 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      q[i] = (live && (kb0 >> 1) + i < nquads) ? __ldg(wrow + (kb0 >> 1) + i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        const int rr = row0 + sub * 32 + lb * 16 + hi * 8 + (lane >> 2);
+        rs_pre[lb][hi] = (p.rscale && p.tma_out && rr < p.rows) ? p.rscale[rr] : __float2half(1.f);
+      }
+  }
   if (KSCALE && !p.ks_global) {
     // kscale as fp16 pairs, zero beyond K (those columns meet TMA zero-fill anyway)
     // 8 columns (4 pairs) per thread and load: one round trip for K <= 8 * kThreads
@@ -263,10 +285,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (4 quads): the next group's quads are loaded when a group starts, so each load has 8 K blocks
     // of MMA time to arrive (one quad ahead was too short for N = 64 tiles: HBM latency-bound)
     const int nquads = (p.num_kb + 1) >> 1;
-    uint4 q[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      q[i] = (live && (kb0 >> 1) + i < nquads) ? __ldg(wrow + (kb0 >> 1) + i) : make_uint4(0, 0, 0, 0);
     const bool tr = tracing && threadIdx.x == 32 * kExpWarp0;
     // the 16 kscale pairs of this lane's word of K block kb (+1.0 pairs without a kscale)
     auto load_ks = [&](int kb, uint32_t (&ks)[16]) {
@@ -354,25 +372,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const float rs = (live && p.rscale) ? __half2float(p.rscale[grow]) : 1.f;
     if (p.tma_out) {
-      // the ring is idle once the accumulator is complete: stage the fp16 tile there as
-      // [token][row] (the output's layout) and write it with one TMA store (clipped at rows / T)
-      __half* stile = reinterpret_cast<__half*>(smem);
-#pragma unroll 1
-      for (int c = 0; c < BN / 64; ++c) {
-        const int col = half * (BN / 2) + c * 32;
-        if (tok0 + col >= p.T) break;
-        uint32_t acc[32];
-        tmem_ld32(tmem + lane_addr + kAccCol + mh * BN + col, acc);
+      // The ring is idle once the accumulator is complete: stage the fp16 tile there in the
+      // output's [token][row] layout as two 64-row sub-tiles (128-byte rows, 128-byte swizzle) and
+      // write each with one TMA store (clipped at rows / T).  16x256b TMEM loads give every thread
+      // two tokens of two rows (C-fragment layout); stmatrix.trans turns each 8 x 8 block into 8
+      // token rows of 8 sign rows (16 bytes), conflict-free under the swizzle.
+      const int mi = lane >> 3, mr = lane & 7;  // stmatrix: matrix / memory row this lane addresses
+      const uint32_t sub_base = smem_u32(smem) + (uint32_t)(sub >> 1) * (BN * 128);
+#pragma unroll
+      for (int lb = 0; lb < 2; ++lb) {
+        const float rs_lo = __half2float(rs_pre[lb][0]), rs_hi = __half2float(rs_pre[lb][1]);  // rows sub*32 + lb*16 + g (+8)
+        const int ch = ((sub & 1) * 32 + lb * 16) / 8 + (mi & 1);  // 16-byte chunk this lane's row lands in
+        // all four 32-token loads in flight before one wait (tokens past T are staged too; the
+        // TMA store clips them)
+        uint32_t v[BN / 64][16];
+#pragma unroll
+        for (int c = 0; c < BN / 64; ++c)
+          tmem_ld16x256_x4(tmem + ((uint32_t)(sub * 32 + lb * 16) << 16) + kAccCol + mh * BN + half * (BN / 2) + c * 32,
+                           v[c]);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stile[(col + j) * BM + r] = __float2half_rn(__uint_as_float(acc[j]) * rs);
+        for (int c = 0; c < BN / 64; ++c) {
+          const int col = half * (BN / 2) + c * 32;
+#pragma unroll
+          for (int gp = 0; gp < 2; ++gp) {  // 16 tokens per stmatrix.x4
+            uint32_t m[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // matrix q: token group 2gp + q/2, rows lo (q even) / hi
+              const uint32_t* f = v[c] + 4 * (2 * gp + (q >> 1)) + 2 * (q & 1);
+              const float rs = (q & 1) ? rs_hi : rs_lo;
+              const __half2 h = __floats2half2_rn(__uint_as_float(f[0]) * rs, __uint_as_float(f[1]) * rs);
+              m[q] = *reinterpret_cast<const uint32_t*>(&h);
+            }
+            const int tk = col + 16 * gp + 8 * (mi >> 1) + mr;
+            stmatrix_x4_trans(sub_base + (uint32_t)tk * 128 + (uint32_t)((ch ^ (tk & 7)) * 16), m[0], m[1], m[2], m[3]);
+          }
+        }
       }
       fence_proxy_async_smem();
       if (threadIdx.x == 32 * kExpWarp0) CT(10);
       asm volatile("bar.sync 1, %0;" ::"n"(kExpWarps * 32) : "memory");
       if (threadIdx.x == 32 * kExpWarp0) {
         CT(11);
-        tma_store_2d(&out_map, stile, row0, tok0);
+        tma_store_2d(&out_map, smem, row0, tok0);
+        if (row0 + 64 < p.rows) tma_store_2d(&out_map, smem + BN * 128, row0 + 64, tok0);
         bulk_commit_group();
         bulk_wait_group_read0();
         CT(12);
@@ -451,16 +494,16 @@ static int make_act_map(CUtensorMap* map, const void* act, int64_t T, int64_t K,
   return r == CUDA_SUCCESS ? DBF_OK : DBF_ERR_CUDA;
 }
 
-// out: T x rows fp16, row stride ldo elements; box = one BM x BN tile
+// out: T x rows fp16, row stride ldo elements; box = 64 rows x BN tokens (half a tile), 128-byte swizzle
 static int make_out_map(CUtensorMap* map, void* out, int64_t T, int64_t rows, int64_t ldo) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return DBF_ERR_CUDA;
   const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)T};
   const cuuint64_t strides[1] = {(cuuint64_t)ldo * 2};
-  const cuuint32_t box[2] = {BM, BN};
+  const cuuint32_t box[2] = {64, BN};  // 64 rows = one 128-byte swizzle span
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? DBF_OK : DBF_ERR_CUDA;
 }
 

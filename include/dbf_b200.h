@@ -429,6 +429,22 @@ int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_
                         int64_t k, int64_t m, const void* X, int64_t tokens, int64_t ldx, void* Y,
                         int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The same forward with an explicit kernel path.  DBF_PREFILL_TWO_LAUNCHES: one per-tile sign GEMM
+ * launch per GEMM (T <= 256: split K).  DBF_PREFILL_ONE_LAUNCH (T > 256): both GEMMs in ONE persistent
+ * launch, one CTA per SM claiming 128 x 256 tiles from a global counter, GEMM2 tiles of a token
+ * block waiting on counters of its GEMM1 tiles; needs the workspace of dbf_prefill_workspace_bytes_nkm
+ * (tile counters after t) and a TMA-compatible Y (ldy % 8 == 0, 16-byte aligned), else
+ * DBF_ERR_UNSUPPORTED.  Both paths give bitwise identical outputs (same K order and rounding).
+ * DBF_PREFILL_AUTO (what dbf_forward_prefill uses) = dbf_prefill_layer_path(n, k, m, tokens). */
+enum { DBF_PREFILL_AUTO = 0, DBF_PREFILL_TWO_LAUNCHES = 1, DBF_PREFILL_ONE_LAUNCH = 2 };
+int dbf_forward_prefill_ex(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired,
+                           int64_t B_pitch, const void* a, const void* mid, const void* b, int64_t n,
+                           int64_t k, int64_t m, const void* X, int64_t tokens, int64_t ldx, void* Y,
+                           int64_t ldy, void* workspace, size_t workspace_bytes, int path, void* stream);
+/* The path DBF_PREFILL_AUTO takes: one launch where GEMM1's tiles (k/128 x T/256) exceed the SM count
+ * (a partly idle second wave), two launches otherwise (measured). */
+int dbf_prefill_layer_path(int64_t n, int64_t k, int64_t m, int64_t tokens);
+
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,11 @@ SIGNATURES: dict[str, tuple] = {
         _int,
         [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _vp],
     ),
+    "dbf_forward_prefill_ex": (
+        _int,
+        [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _int, _vp],
+    ),
+    "dbf_prefill_layer_path": (_int, [_i64, _i64, _i64, _i64]),
 }
 
 

@@ -495,12 +495,12 @@ static int make_act_map(CUtensorMap* map, const void* act, int64_t T, int64_t K,
 }
 
 // out: T x rows fp16, row stride ldo elements; box = 64 rows x BN tokens (half a tile), 128-byte swizzle
-static int make_out_map(CUtensorMap* map, void* out, int64_t T, int64_t rows, int64_t ldo) {
+static int make_out_map(CUtensorMap* map, void* out, int64_t T, int64_t rows, int64_t ldo, int box_tokens = BN) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return DBF_ERR_CUDA;
   const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)T};
   const cuuint64_t strides[1] = {(cuuint64_t)ldo * 2};
-  const cuuint32_t box[2] = {64, BN};  // 64 rows = one 128-byte swizzle span
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_tokens};  // 64 rows = one 128-byte swizzle span
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -640,6 +640,490 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   return check_launch();
 }
 
+// ================================================================================================
+// The whole layer in ONE persistent launch (T > 256 tokens):
+//
+//   GEMM1 tiles 0 .. N1-1        t[T, k] = mid (.) (X . (B (.) b)^T)    token-block-major order
+//   GEMM2 tiles N1 .. N1+N2-1    Y[T, n] = a (.) (t . A^T)
+//
+// claimed dynamically by one CTA per SM (a global tile counter).  Traced on the per-tile kernel
+// (tools/prefill_ctas.py): a 128 x 256 tile spends 2.7 us before its first MMA and 2.4 us after its
+// last one, and 128-192 tiles on 148 SMs leave whole waves idle, so a 7B q layer took 67 us for 40
+// us of MMA K loops.  Here a GEMM2 tile of token block tb only waits for the k/128 GEMM1 tiles of
+// tb (per-token-block counters, release/acquire), the epilogue has its own 4 warps that drain the
+// accumulator into registers (the MMA's only wait) and store straight to global memory while the
+// next tile's K loop runs, and the activation ring and the sign expansion run continuously across
+// tiles.  Tile mechanics and numerics are the per-tile kernel's (same K order, fp32 TMEM
+// accumulation, same rounding): the outputs are bitwise those of the two-launch path.
+//
+// Warp roles (16 warps): lanes of warps 0, 2, 3 issue the activation TMA loads (one issuer per ring
+// stage -- a thread's TMA loads complete one after another; issuer 0 also claims the tiles),
+// warp 1 allocates TMEM and issues the MMAs, 4..11 expand signs, 12..15 run the epilogue.
+namespace layer {
+
+constexpr int S = 6;                            // ring stages (32 KB activation box + 32-column TMEM A slot)
+constexpr int kStagingBytes = 128 * 128 * 2;    // half a tile: fp16 [128 tokens][128 rows], two 64-row TMA boxes
+constexpr int kActBytes = 256 * BK * 2;         // one 256-token x 64-column fp16 box
+constexpr int kACol0 = 256;                     // A slots after the 256-column accumulator
+constexpr int kExp0 = 4, kExpN = 8, kEpi0 = 12, kEpiN = 4;
+constexpr int kThreadsL = 16 * 32;
+constexpr int kRing = 2;                        // tile-id ring
+constexpr int kIssuers = S;                     // lanes 0-1 of warps 0, 2, 3
+static_assert(kIssuers <= 6, "issuers are lanes 0-1 of warps 0, 2 and 3");
+static_assert(kACol0 + S * kAColsPerHalf <= kTmemCols, "TMEM budget");
+
+struct LParams {
+  const uint32_t* B_words; int64_t B_pitch;     // k x m paired words
+  const uint32_t* A_words; int64_t A_pitch;     // n x k paired words
+  const __half* a; const __half* mid; const __half* b;
+  __half* t; int64_t ldt;                       // GEMM1 output (GEMM2 input, read back through t_map)
+  __half* Y; int64_t ldy;
+  int n, k, m, T;
+  int rt1, rt2, tbs;                            // row tiles of GEMM1 (k/128), GEMM2 (n/128); token blocks
+  int nkb1, nkb2;                               // K blocks of GEMM1 (m/64) and GEMM2 (k/64)
+  int* sched;                                   // [0] tile counter, [1..tbs] GEMM1 tiles done per token block
+  long long* trace;                             // debug: per-tile globaltimer stamps, or nullptr
+  long long* ktrace;                            // debug: per-K-block clock64 stamps of CTA 0 (first 1024), or nullptr
+};
+
+struct __align__(8) LBar {
+  uint64_t full_act[S], full_a[S], empty[S];
+  uint64_t acc_full, acc_empty;
+  uint64_t tile_full[kRing], tile_empty[kRing];
+  int tile_id[kRing];
+  uint32_t tmem_base;
+};
+
+inline size_t layer_smem_bytes() { return 1024 + (size_t)S * kActBytes + kStagingBytes + sizeof(LBar); }
+
+struct Tile {
+  int g1;      // 1: GEMM1, 0: GEMM2
+  int rt, tb;
+  bool valid;
+};
+__device__ __forceinline__ Tile decode(const LParams& p, int t) {
+  Tile ti;
+  const int n1 = p.rt1 * p.tbs;
+  ti.valid = t >= 0 && t < n1 + p.rt2 * p.tbs;
+  if (t < n1) {
+    ti.g1 = 1, ti.tb = t / p.rt1, ti.rt = t % p.rt1;
+  } else {
+    t -= n1;
+    ti.g1 = 0, ti.tb = t / p.rt2, ti.rt = t % p.rt2;
+  }
+  return ti;
+}
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// the tile id of local tile j (whole warp; lane 0 waits), then this warp is done reading the slot
+__device__ __forceinline__ int warp_read_tile(LBar& bar, int j, int lane) {
+  const int slot = j % kRing;
+  if (lane == 0) mbar_wait(&bar.tile_full[slot], (j / kRing) & 1);
+  __syncwarp();
+  const int t = *reinterpret_cast<volatile int*>(&bar.tile_id[slot]);
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&bar.tile_empty[slot]);
+  return t;
+}
+
+__global__ void __launch_bounds__(kThreadsL, 1)
+    sign_layer_kernel(const __grid_constant__ CUtensorMap x_map, const __grid_constant__ CUtensorMap t_map,
+                      const __grid_constant__ CUtensorMap t_store, const __grid_constant__ CUtensorMap y_store,
+                      const LParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* act = smem;
+  uint8_t* staging = smem + (size_t)S * kActBytes;
+  LBar& bar = *reinterpret_cast<LBar*>(staging + kStagingBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&bar.full_act[s], 1);
+      mbar_init(&bar.full_a[s], kExpN);
+      mbar_init(&bar.empty[s], 1);
+    }
+    mbar_init(&bar.acc_full, 1);
+    mbar_init(&bar.acc_empty, kEpiN);
+    for (int j = 0; j < kRing; ++j) {
+      mbar_init(&bar.tile_full[j], 1);
+      // the other issuers + MMA thread + expander warps + epilogue warps
+      mbar_init(&bar.tile_empty[j], (kIssuers - 1) + 1 + kExpN + kEpiN);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&x_map);
+    tma_prefetch_desc(&t_map);
+    tma_prefetch_desc(&t_store);
+    tma_prefetch_desc(&y_store);
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(&bar.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bar.tmem_base;
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // ---------------- TMA issuers (issuer 0 also schedules) ----------------
+    const int issuer = (warp == 0 ? 0 : warp - 1) * 2 + lane;
+    if (lane < 2 && issuer < kIssuers) {
+      const uint64_t pol = policy_evict_last();  // activations are re-read by every row tile
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // the tile counters, X and t belong to the stream
+      int g = 0;                                          // ring position (K blocks of all tiles so far)
+      for (int j = 0;; ++j) {
+        const int slot = j % kRing;
+        int t;
+        if (issuer == 0) {
+          mbar_wait(&bar.tile_empty[slot], ((j / kRing) & 1) ^ 1);
+          // claimed once issuer 0 has issued its loads of the current tile (just in time: the ring
+          // holds S K blocks, so dynamic claiming balances the tail)
+          t = atomicAdd(p.sched, 1);
+          bar.tile_id[slot] = t;
+          mbar_arrive(&bar.tile_full[slot]);
+        } else {
+          mbar_wait(&bar.tile_full[slot], (j / kRing) & 1);
+          t = *reinterpret_cast<volatile int*>(&bar.tile_id[slot]);
+          mbar_arrive(&bar.tile_empty[slot]);
+        }
+        const Tile ti = decode(p, t);
+        if (!ti.valid) break;
+        if (issuer == 0 && p.trace) p.trace[8 * t + 0] = gtimer();
+        const int nkb = ti.g1 ? p.nkb1 : p.nkb2;
+        // this issuer's first K block of the tile: the one landing in ring stage `issuer`
+        int kb = ((issuer - g) % S + S) % S;
+        if (!ti.g1 && kb < nkb) {  // t of this token block must be complete (the GEMM1 epilogues)
+          while (true) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.sched + 1 + ti.tb) : "memory");
+            if (v >= p.rt1) break;
+            __nanosleep(128);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          if (issuer == 0 && p.trace) p.trace[8 * t + 1] = gtimer();
+        }
+        const CUtensorMap* map = ti.g1 ? &x_map : &t_map;
+        for (; kb < nkb; kb += S) {
+          const int gg = g + kb;
+          const int s = gg % S;
+          const uint32_t ph = (gg / S) & 1;
+          mbar_wait(&bar.empty[s], ph ^ 1);
+          if (p.ktrace && blockIdx.x == 0 && gg < 1024) p.ktrace[4 * gg + 0] = clock64();
+          mbar_arrive_expect_tx(&bar.full_act[s], kActBytes);
+          tma_load_2d(act + (size_t)s * kActBytes, map, kb * BK, ti.tb * 256, &bar.full_act[s], pol);
+        }
+        g += nkb;
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16_f32(UM, 256);
+      int g = 0;
+      for (int j = 0;; ++j) {
+        const int slot = j % kRing;
+        mbar_wait(&bar.tile_full[slot], (j / kRing) & 1);
+        const int t = *reinterpret_cast<volatile int*>(&bar.tile_id[slot]);
+        mbar_arrive(&bar.tile_empty[slot]);
+        const Tile ti = decode(p, t);
+        if (!ti.valid) break;
+        const int nkb = ti.g1 ? p.nkb1 : p.nkb2;
+        mbar_wait(&bar.acc_empty, (j & 1) ^ 1);  // the epilogue drained the previous tile's accumulator
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % S;
+          const uint32_t ph = (g / S) & 1;
+          mbar_wait(&bar.full_act[s], ph);
+          if (p.ktrace && blockIdx.x == 0 && g < 1024) p.ktrace[4 * g + 1] = clock64();
+          mbar_wait(&bar.full_a[s], ph);
+          if (p.ktrace && blockIdx.x == 0 && g < 1024) p.ktrace[4 * g + 2] = clock64();
+          tc_fence_after();
+          if (kb == 0 && p.trace) p.trace[8 * t + 2] = gtimer();
+          const uint32_t a_base = tmem + kACol0 + s * kAColsPerHalf;
+          const uint32_t b_base = smem_u32(act + (size_t)s * kActBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk)
+            mma_f16_ts(tmem, a_base + kk * (UK / 2), sdesc_k_sw128(b_base + kk * UK * 2), idesc, (kb | kk) != 0);
+          mma_commit(&bar.empty[s]);
+        }
+        mma_commit(&bar.acc_full);
+        if (p.trace) p.trace[8 * t + 3] = gtimer();
+      }
+    }
+  } else if (warp >= kExp0 && warp < kExp0 + kExpN) {
+    // ---------------- sign expanders (the per-tile kernel's loop, ring position carried across tiles) ----
+    const int sub = warp & 3, half = (warp - kExp0) >> 2;
+    const uint32_t col = tmem + ((uint32_t)(sub * 32) << 16) + kACol0 + half * 16;
+    int g = 0;
+    for (int j = 0;; ++j) {
+      const int t = warp_read_tile(bar, j, lane);
+      const Tile ti = decode(p, t);
+      if (!ti.valid) break;
+      const int rows = ti.g1 ? p.k : p.n, nkb = ti.g1 ? p.nkb1 : p.nkb2;
+      const int grow = ti.rt * UM + sub * 32 + lane;
+      const bool live = grow < rows;
+      const uint4* wrow = reinterpret_cast<const uint4*>((ti.g1 ? p.B_words : p.A_words) +
+                                                         (int64_t)(live ? grow : 0) * (ti.g1 ? p.B_pitch : p.A_pitch));
+      const bool has_ks = ti.g1 && p.b != nullptr;  // GEMM1's K scale b; GEMM2 has none
+      const int nquads = (nkb + 1) >> 1;
+      // K scales live in registers: for the 8 K blocks of a group, lane L holds in ksr[jp] the fp16 pair
+      // (L & 15) of this warp's 32 columns of K block kg + 2 jp + (L >> 4); a K block's 16 pairs are
+      // then one shuffle each (no shared memory for them, no L1 traffic in the loop)
+      const unsigned short* bsrc = reinterpret_cast<const unsigned short*>(p.b);
+      auto load_ksr = [&](int kg, uint32_t (&r)[4]) {
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {
+          const int c = (kg + 2 * jp + (lane >> 4)) * BK + half * 32 + 2 * (lane & 15);
+          r[jp] = !has_ks ? 0x3C003C00u
+                          : ((c < p.m ? (uint32_t)__ldg(bsrc + c) : 0u) |
+                             ((c + 1 < p.m ? (uint32_t)__ldg(bsrc + c + 1) : 0u) << 16));
+        }
+      };
+      uint32_t ksr[4];
+      load_ksr(0, ksr);
+      uint4 q[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) q[i] = (live && i < nquads) ? __ldg(wrow + i) : make_uint4(0, 0, 0, 0);
+      for (int kg = 0; kg < nkb; kg += 8) {
+        uint4 nq[4];
+        uint32_t nksr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int qi = (kg >> 1) + 4 + i;
+          nq[i] = (live && qi < nquads) ? __ldg(wrow + qi) : make_uint4(0, 0, 0, 0);
+        }
+        load_ksr(kg + 8, nksr);
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {
+          const int kb = kg + 2 * jp;
+          if (kb >= nkb) break;
+          const bool two = kb + 1 < nkb;
+          const int s0 = g % S, s1 = (g + 1) % S;
+          const uint32_t ph0 = (g / S) & 1, ph1 = ((g + 1) / S) & 1;
+          uint32_t ks[16], v0[16], v1[16];
+#pragma unroll
+          for (int w = 0; w < 16; ++w) ks[w] = __shfl_sync(0xffffffffu, ksr[jp], w);
+          expand_word(half ? q[jp].y : q[jp].x, ks, v0);
+          if (two) {
+#pragma unroll
+            for (int w = 0; w < 16; ++w) ks[w] = __shfl_sync(0xffffffffu, ksr[jp], 16 + w);
+            expand_word(half ? q[jp].w : q[jp].z, ks, v1);
+          }
+          if (lane == 0) {
+            mbar_wait(&bar.empty[s0], ph0 ^ 1);
+            if (two) mbar_wait(&bar.empty[s1], ph1 ^ 1);
+          }
+          __syncwarp();
+          tc_fence_after();
+          tmem_st16(col + s0 * kAColsPerHalf, v0);
+          if (two) tmem_st16(col + s1 * kAColsPerHalf, v1);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&bar.full_a[s0]);
+            if (two) mbar_arrive(&bar.full_a[s1]);
+            if (p.ktrace && blockIdx.x == 0 && warp == kExp0 && g < 1023) p.ktrace[4 * g + 3] = p.ktrace[4 * g + 7] = clock64();
+          }
+          g += two ? 2 : 1;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[i] = nq[i], ksr[i] = nksr[i];
+      }
+    }
+  } else if (warp >= kEpi0) {
+    // ---------------- epilogue: accumulator -> fp16 staging (half a tile) -> TMA stores ----------------
+    // 16x256b TMEM loads give every thread two tokens of two rows (C-fragment layout); stmatrix.trans
+    // turns each 8 x 8 block into 8 token rows of 8 sign rows in the staging tile ([token][row],
+    // 128-byte rows, 128-byte swizzle: two 64-row TMA boxes of 128 tokens).  Tokens 0-127 go through
+    // staging first; tokens 128-255 are converted to fp16 in registers, the accumulator is released
+    // (the next tile's MMAs start), and they are staged once the first stores have read the tile.
+    const int sub = warp & 3;
+    const bool storer = threadIdx.x == kEpi0 * 32;
+    const int mi = lane >> 3, mr = lane & 7;  // stmatrix: matrix / memory row this lane addresses
+    const uint32_t sub_base = smem_u32(staging) + (uint32_t)(sub >> 1) * (128 * 128);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel may still read t / Y
+    for (int j = 0;; ++j) {
+      const int t = warp_read_tile(bar, j, lane);
+      const Tile ti = decode(p, t);
+      if (!ti.valid) break;
+      const int rows = ti.g1 ? p.k : p.n;
+      const __half* rsrc = ti.g1 ? p.mid : p.a;
+      const CUtensorMap* om = ti.g1 ? &t_store : &y_store;
+      float rs[2][2];
+#pragma unroll
+      for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+          const int rr = ti.rt * UM + sub * 32 + lb * 16 + hi * 8 + (lane >> 2);
+          rs[lb][hi] = rr < rows ? __half2float(rsrc[rr]) : 0.f;
+        }
+      // stmatrix of one 32-token group (16 packed registers: gp x qd) of row group lb at token tk0
+      auto stage = [&](int lb, int tk0, const uint32_t (&mm)[8]) {
+        const int ch = ((sub & 1) * 32 + lb * 16) / 8 + (mi & 1);
+#pragma unroll
+        for (int gp = 0; gp < 2; ++gp) {
+          const int tk = tk0 + 16 * gp + 8 * (mi >> 1) + mr;
+          stmatrix_x4_trans(sub_base + (uint32_t)tk * 128 + (uint32_t)((ch ^ (tk & 7)) * 16), mm[4 * gp], mm[4 * gp + 1],
+                            mm[4 * gp + 2], mm[4 * gp + 3]);
+        }
+      };
+      auto pack = [&](int lb, const uint32_t (&v)[16], uint32_t (&mm)[8]) {
+#pragma unroll
+        for (int gp = 0; gp < 2; ++gp)
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) {  // matrix qd: token group 2gp + qd/2, rows lo (qd even) / hi
+            const uint32_t* f = v + 4 * (2 * gp + (qd >> 1)) + 2 * (qd & 1);
+            const float r = rs[lb][qd & 1];
+            const __half2 h = __floats2half2_rn(__uint_as_float(f[0]) * r, __uint_as_float(f[1]) * r);
+            mm[4 * gp + qd] = *reinterpret_cast<const uint32_t*>(&h);
+          }
+      };
+      if (storer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free again
+      if (lane == 0) {  // a long wait (a whole K loop): back off instead of spinning next to the MMA issuer
+        while (!mbar_test(&bar.acc_full, j & 1)) __nanosleep(256);
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(kEpiN * 32) : "memory");
+      tc_fence_after();
+      if (storer && p.trace) p.trace[8 * t + 4] = gtimer();
+      // phase A: tokens 0-127 straight into staging
+#pragma unroll
+      for (int lb = 0; lb < 2; ++lb) {
+        uint32_t v[4][16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          tmem_ld16x256_x4(tmem + ((uint32_t)(sub * 32 + lb * 16) << 16) + c * 32, v[c]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t mm[8];
+          pack(lb, v[c], mm);
+          stage(lb, c * 32, mm);
+        }
+      }
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 2, %0;" ::"n"(kEpiN * 32) : "memory");
+      if (storer) {
+        tma_store_2d(om, staging, ti.rt * UM, ti.tb * 256);
+        if (ti.rt * UM + 64 < rows) tma_store_2d(om, staging + 128 * 128, ti.rt * UM + 64, ti.tb * 256);
+        bulk_commit_group();
+      }
+      // phase B: tokens 128-255 into registers as fp16, then the accumulator is free
+      uint32_t hold[2][4][8];
+#pragma unroll
+      for (int lb = 0; lb < 2; ++lb) {
+        uint32_t v[4][16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          tmem_ld16x256_x4(tmem + ((uint32_t)(sub * 32 + lb * 16) << 16) + 128 + c * 32, v[c]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) pack(lb, v[c], hold[lb][c]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar.acc_empty);
+      if (storer && p.trace) p.trace[8 * t + 6] = gtimer();
+      if (storer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // phase A's stores read the tile
+      asm volatile("bar.sync 2, %0;" ::"n"(kEpiN * 32) : "memory");
+#pragma unroll
+      for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) stage(lb, c * 32, hold[lb][c]);
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 2, %0;" ::"n"(kEpiN * 32) : "memory");
+      if (storer) {
+        tma_store_2d(om, staging, ti.rt * UM, ti.tb * 256 + 128);
+        if (ti.rt * UM + 64 < rows) tma_store_2d(om, staging + 128 * 128, ti.rt * UM + 64, ti.tb * 256 + 128);
+        bulk_commit_group();
+        if (ti.g1) {  // publish t of this tile before counting it done
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.sched + 1 + ti.tb) : "memory");
+        }
+        if (p.trace) p.trace[8 * t + 5] = gtimer();
+      }
+    }
+    if (storer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+inline size_t counter_bytes(int64_t tokens) { return (size_t)(ceil_div(tokens, 256) + 1) * 4; }
+
+#ifdef DBF_PREFILL_TRACE
+static long long* layer_trace = nullptr;
+#endif
+
+// Both GEMMs of one layer as one persistent launch.  t: T x ldt fp16 workspace, counters: zeroed here.
+static int launch_layer(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired, int64_t B_pitch,
+                        const __half* a, const __half* mid, const __half* b, int64_t n, int64_t k, int64_t m,
+                        const void* X, int64_t T, int64_t ldx, void* Y, int64_t ldy, __half* t, int64_t ldt,
+                        int* counters, cudaStream_t stream) {
+  CUtensorMap xm, tm, ts, ys;
+  int st = make_act_map(&xm, X, T, m, ldx, 256);
+  if (st == DBF_OK) st = make_act_map(&tm, t, T, k, ldt, 256);
+  if (st == DBF_OK) st = make_out_map(&ts, t, T, k, ldt, 128);
+  if (st == DBF_OK) st = make_out_map(&ys, Y, T, n, ldy, 128);
+  if (st != DBF_OK) return st;
+  LParams p;
+  p.B_words = B_paired, p.B_pitch = B_pitch, p.A_words = A_paired, p.A_pitch = A_pitch;
+  p.a = a, p.mid = mid, p.b = b;
+  p.t = t, p.ldt = ldt, p.Y = (__half*)Y, p.ldy = ldy;
+  p.n = (int)n, p.k = (int)k, p.m = (int)m, p.T = (int)T;
+  p.rt1 = (int)ceil_div(k, UM), p.rt2 = (int)ceil_div(n, UM), p.tbs = (int)ceil_div(T, 256);
+  p.nkb1 = (int)ceil_div(m, BK), p.nkb2 = (int)ceil_div(k, BK);
+  p.sched = counters;
+  p.trace = nullptr;
+  p.ktrace = nullptr;
+#ifdef DBF_PREFILL_TRACE
+  {
+    const size_t need = 8 * sizeof(long long) * (size_t)(p.rt1 + p.rt2) * p.tbs + 4 * 1024 * 8;
+    static size_t have = 0;
+    if (need > have) {
+      if (layer_trace) cudaFree(layer_trace);
+      cudaMalloc(&layer_trace, need);
+      have = need;
+    }
+    p.trace = layer_trace;
+    p.ktrace = layer_trace + 8 * (size_t)(p.rt1 + p.rt2) * p.tbs;
+  }
+#endif
+  cudaError_t e = cudaMemsetAsync(counters, 0, counter_bytes(T), stream);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  int dev = 0, sms = kNumSMs;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (int64_t)(p.rt1 + p.rt2) * p.tbs;
+  const size_t smem = layer_smem_bytes();
+  e = cudaFuncSetAttribute(sign_layer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::min<int64_t>(tiles, sms));
+  cfg.blockDim = dim3(kThreadsL);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, sign_layer_kernel, xm, tm, ts, ys, p);
+  if (e != cudaSuccess) { set_cuda_error(e); return DBF_ERR_CUDA; }
+  return check_launch();
+}
+
+}  // namespace layer
+
 }  // namespace prefill
 }  // namespace dbf
 
@@ -656,6 +1140,14 @@ int dbf_prefill_debug_trace(long long* host, int n) {
 }
 
 #ifdef DBF_PREFILL_TRACE
+// debug: per-tile {claim, dependency met, first MMA, last commit, accumulator seen, stored} globaltimer
+// stamps of the last one-launch layer (8 int64 per tile)
+int dbf_prefill_debug_layer(long long* host, int n) {
+  if (!prefill::layer::layer_trace) return DBF_ERR_UNSUPPORTED;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, prefill::layer::layer_trace, 8 * (size_t)n, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? DBF_OK : DBF_ERR_CUDA;
+}
 // debug: per-CTA {globaltimer start, end, clock end, smid, clock start, setup done, first MMA, last commit,
 // accumulator seen, -} of the last traced launch
 int dbf_prefill_debug_ctas(long long* host, int n) {
@@ -684,13 +1176,38 @@ int dbf_sign_gemm(const void* act, int64_t tokens, int64_t K, int64_t ld_act, co
 size_t dbf_prefill_workspace_bytes_nkm(int64_t n, int64_t k, int64_t m, int64_t tokens) {
   if (n < 1 || k < 1 || m < 1 || tokens < 1) return 0;
   const size_t t = (dbf_prefill_workspace_bytes(k, tokens) + 255) & ~(size_t)255;
-  return t + std::max(prefill::split_bytes(tokens, m, k), prefill::split_bytes(tokens, k, n));
+  // T <= 256: split-K partials; above: the one-launch layer kernel's tile counters
+  return t + std::max({prefill::split_bytes(tokens, m, k), prefill::split_bytes(tokens, k, n),
+                       tokens > prefill::BN ? prefill::layer::counter_bytes(tokens) : (size_t)0});
+}
+
+int dbf_prefill_layer_path(int64_t n, int64_t k, int64_t m, int64_t tokens) {
+  if (n < 1 || k < 1 || m < 1 || tokens <= prefill::BN) return DBF_PREFILL_TWO_LAUNCHES;
+  // Measured on the Llama-2-7B shapes at T = 2048 (tools/prefill_ab.py): the one-launch
+  // kernel wins where GEMM1's tiles spill into a second, partly idle wave (gate/up 1235 vs 1130 TF/s,
+  // down 1063 vs 1057) and loses where GEMM1 fits one wave (q 929 vs 1061: the CTAs beyond GEMM1's
+  // tiles wait for t, and its K loop runs ~10 % slower than the per-tile kernel's).
+  int dev = 0, sms = kNumSMs;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles1 = ceil_div(k, prefill::UM) * ceil_div(tokens, prefill::BN);
+  return tiles1 > sms ? DBF_PREFILL_ONE_LAUNCH : DBF_PREFILL_TWO_LAUNCHES;
 }
 
 int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired, int64_t B_pitch,
                         const void* a, const void* mid, const void* b, int64_t n, int64_t k, int64_t m,
                         const void* X, int64_t tokens, int64_t ldx, void* Y, int64_t ldy, void* workspace,
                         size_t workspace_bytes, void* stream) {
+  return dbf_forward_prefill_ex(A_paired, A_pitch, B_paired, B_pitch, a, mid, b, n, k, m, X, tokens, ldx, Y, ldy,
+                                workspace, workspace_bytes, DBF_PREFILL_AUTO, stream);
+}
+
+int dbf_forward_prefill_ex(const uint32_t* A_paired, int64_t A_pitch, const uint32_t* B_paired, int64_t B_pitch,
+                           const void* a, const void* mid, const void* b, int64_t n, int64_t k, int64_t m,
+                           const void* X, int64_t tokens, int64_t ldx, void* Y, int64_t ldy, void* workspace,
+                           size_t workspace_bytes, int path, void* stream) {
+  if (path != DBF_PREFILL_AUTO && path != DBF_PREFILL_TWO_LAUNCHES && path != DBF_PREFILL_ONE_LAUNCH)
+    return DBF_ERR_INVALID_ARGUMENT;
   if (!A_paired || !B_paired || !a || !mid || !b || !X || !Y) return DBF_ERR_INVALID_ARGUMENT;
   if (n < 1 || k < 1 || m < 1 || tokens < 1) return DBF_ERR_INVALID_ARGUMENT;
   if (ldy < n || ldx < m) return DBF_ERR_SHAPE;
@@ -703,6 +1220,19 @@ int dbf_forward_prefill(const uint32_t* A_paired, int64_t A_pitch, const uint32_
   const size_t tb = (dbf_prefill_workspace_bytes(k, tokens) + 255) & ~(size_t)255;
   float* sw = workspace_bytes > tb ? (float*)((char*)workspace + tb) : nullptr;
   const size_t swb = workspace_bytes > tb ? workspace_bytes - tb : 0;
+  // more than one token tile: both GEMMs in one persistent launch when the workspace holds its tile
+  // counters and t / Y suit the TMA stores (16-byte aligned rows)
+  if (path == DBF_PREFILL_AUTO) path = dbf_prefill_layer_path(n, k, m, tokens);
+  const bool layer_ok =
+      tokens > prefill::BN && swb >= prefill::layer::counter_bytes(tokens) && (ldy * 2) % 16 == 0 &&
+      ((uintptr_t)Y & 15) == 0 && (ldx * 2) % 16 == 0 && ((uintptr_t)X & 15) == 0 &&
+      A_pitch * 32 >= ceil_div(k, prefill::BK) * prefill::BK && B_pitch * 32 >= ceil_div(m, prefill::BK) * prefill::BK &&
+      ((uintptr_t)A_paired & 15) == 0 && ((uintptr_t)B_paired & 15) == 0 && A_pitch % 4 == 0 && B_pitch % 4 == 0 &&
+      tokens <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX && m <= INT32_MAX;
+  if (path == DBF_PREFILL_ONE_LAUNCH && !layer_ok) return DBF_ERR_UNSUPPORTED;
+  if (path == DBF_PREFILL_ONE_LAUNCH)
+    return prefill::layer::launch_layer(A_paired, A_pitch, B_paired, B_pitch, (const __half*)a, (const __half*)mid,
+                                        (const __half*)b, n, k, m, X, tokens, ldx, Y, ldy, t, ldt, (int*)sw, s);
   int st = prefill::launch_sign_gemm(X, tokens, m, ldx, B_paired, B_pitch, k, (const __half*)b,
                                      (const __half*)mid, t, ldt, s, sw, swb);
   if (st != DBF_OK) return st;

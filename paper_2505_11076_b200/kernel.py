@@ -94,11 +94,16 @@ def _prefill_eligible(X2, layer: DeviceLayer, out_dtype) -> bool:
     )
 
 
-def forward_prefill(X, layer: DeviceLayer, out=None):
+PREFILL_PATHS = {"auto": 0, "two_launches": 1, "one_launch": 2}
+
+
+def forward_prefill(X, layer: DeviceLayer, out=None, path: str = "auto"):
     """Y = forward(X, layer) for a token batch on the tcgen05 tensor cores (prefill path).
 
     X: CUDA fp16 tensor tokens x m; layer: fp16 scales with canonical words kept.  The two sign
-    GEMMs run with fp32 accumulation in tensor memory and an fp16 intermediate t."""
+    GEMMs run with fp32 accumulation in tensor memory and an fp16 intermediate t.
+    path: "auto" (dbf_prefill_layer_path), "two_launches" (one per-tile launch per GEMM) or
+    "one_launch" (both GEMMs in one persistent launch, T > 256); all give the same bits."""
     import torch
 
     if X.ndim != 2:
@@ -116,15 +121,18 @@ def forward_prefill(X, layer: DeviceLayer, out=None):
         X = Xp[:, :m]
     Y = out if out is not None else torch.empty((T, layer.n), dtype=torch.float16, device=X.device)
     A, B = layer.A.paired, layer.B.paired
-    name = "dbf_forward_prefill"
-    # room for the split-K partials of small token counts
+    name = "dbf_forward_prefill_ex"
+    if path not in PREFILL_PATHS:
+        raise ValueError(f"path must be one of {sorted(PREFILL_PATHS)}, got {path!r}")
+    # room for the split-K partials of small token counts / the one-launch kernel's tile counters
     ws_bytes = _lib.lib.dbf_prefill_workspace_bytes_nkm(layer.n, layer.k, layer.m_dim, T)
     ws = _workspace(ws_bytes, X.device)
     _lib.check(
         getattr(_lib.lib, name)(
             A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1],
             layer.a.data_ptr(), layer.mid.data_ptr(), layer.b.data_ptr(), layer.n, layer.k, layer.m_dim,
-            X.data_ptr(), T, X.stride(0), Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(), _lib.stream_ptr(),
+            X.data_ptr(), T, X.stride(0), Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(),
+            PREFILL_PATHS[path], _lib.stream_ptr(),
         ),
         name,
     )

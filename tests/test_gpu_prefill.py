@@ -141,3 +141,62 @@ def test_small_batch_split_k_is_deterministic():
         _lib.stream_ptr()), "dbf_forward_prefill")
     err = (Y0.float() - Y1.float()).abs().max().item() / Y0.float().abs().max().item()
     assert err <= TOL
+
+
+def _two_launch(X, dl):
+    """The same layer as two per-tile sign GEMM launches (dbf_sign_gemm): t = mid * (X . (B*b)^T),
+    Y = a * (t . A^T) -- the path forward_prefill took before the one-launch layer kernel."""
+    T, m = X.shape
+    n, k = dl.n, dl.k
+    ldt = _lib.lib.dbf_prefill_ld(k)
+    t = torch.empty((T, ldt), dtype=torch.half, device="cuda")
+    Y = torch.empty((T, n), dtype=torch.half, device="cuda")
+    A, B = dl.A.paired, dl.B.paired
+    _lib.check(_lib.lib.dbf_sign_gemm(X.data_ptr(), T, m, X.stride(0), B.data_ptr(), B.shape[1], k, dl.b.data_ptr(),
+                                      dl.mid.data_ptr(), t.data_ptr(), ldt, _lib.stream_ptr()), "gemm1")
+    _lib.check(_lib.lib.dbf_sign_gemm(t.data_ptr(), T, k, ldt, A.data_ptr(), A.shape[1], n, None,
+                                      dl.a.data_ptr(), Y.data_ptr(), n, _lib.stream_ptr()), "gemm2")
+    return Y
+
+
+@pytest.mark.parametrize(
+    "T,n,k,m",
+    [
+        (2048, 4096, 2048, 4096),    # Llama-2-7B q at 1 bpw (128 GEMM1 + 256 GEMM2 tiles; auto: two launches)
+        (2048, 4096, 2976, 11008),   # 7B down: long GEMM1 K, ragged k (last row tile 32 rows)
+        (768, 11008, 2976, 4096),    # 7B gate, 3 token blocks
+        (300, 200, 96, 130),         # ragged everything, partial second token block
+        (1000, 1000, 160, 1000),
+        (520, 256, 2048, 28672),     # GEMM1 K = 28672: the kscale from global memory
+    ],
+)
+def test_layer_kernel_bitwise_equals_two_launches(T, n, k, m):
+    """T > 256 runs the whole layer as ONE persistent launch (GEMM2 tiles wait on per-token-block
+    counters of GEMM1 tiles).  Same K order, same fp32 accumulation, same rounding: bitwise equal to
+    the two per-tile launches, on every run (dynamic tile claiming must not change any bit)."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(T + n)
+    dl = P.random_device_layer(n, k, m, generator=g, keep_words=True)
+    # rows padded to 16 bytes (the TMA row pitch), as forward_prefill pads a ragged X
+    X = torch.randn((T, (m + 7) // 8 * 8), generator=g, device="cuda").half()[:, :m]
+    ref = _two_launch(X, dl)
+    assert torch.equal(P.forward_prefill(X, dl, path="two_launches"), ref)
+    for _ in range(3):
+        Y = P.forward_prefill(X, dl, path="one_launch")
+        assert torch.equal(Y, ref)
+    assert torch.equal(P.forward_prefill(X, dl), ref)  # whichever path auto picks
+    assert torch.isfinite(ref).all()
+
+
+def test_prefill_auto_path_rule():
+    """dbf_prefill_layer_path: one launch where GEMM1's k/128 x T/256 tiles exceed the SM count,
+    two launches otherwise and for T <= 256 (measured crossover)."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    f = _lib.lib.dbf_prefill_layer_path
+    assert f(4096, 2048, 4096, 2048) == (2 if 16 * 8 > sms else 1)
+    assert f(11008, 2976, 4096, 2048) == (2 if 24 * 8 > sms else 1)
+    assert f(11008, 2976, 4096, 256) == 1
+    X = torch.zeros((300, 64), dtype=torch.half, device="cuda")
+    dl = P.random_device_layer(64, 64, 64, keep_words=True)
+    with pytest.raises(ValueError):
+        P.forward_prefill(X, dl, path="fastest")

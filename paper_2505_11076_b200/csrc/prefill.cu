@@ -8,24 +8,23 @@
 // One kernel, `sign_gemm_kernel`, runs either GEMM: out[T, rows] = rscale (.) (act . (S (.) kscale)^T)
 // with S a rows x K sign matrix in the PAIRED word layout (include/dbf_b200.h, dbf_pair_signs).
 //
-// Per CTA: a 256 (sign rows) x 128 (tokens) output tile = two M=128 halves, each accumulated in
-// TMEM (2 x 128 fp32 columns).  256 rows per activation tile halve the L2->SM activation stream
-// per MMA (32 B/clk/SM at full tensor rate) -- the first bottleneck of a 128-row tile.
-//   warps 0,2,3  TMA producers: 128 x 64 fp16 activation tiles (128-byte swizzle) into a smem ring.
-//   warp 1       TMEM allocator + MMA issuer (one thread): tcgen05.mma.kind::f16, M=128 N=128 K=16,
-//                twice per K step (both M halves share the B tile), A operand (the expanded signs)
-//                from TMEM, B operand (activations) from smem.
-//   warps 4..19  sign expanders, then epilogue.  Warp w owns TMEM sub-partition w%4 (32 sign rows,
-//                one per lane) of M half ((w-4)/4)%2 and word (w-4)/8 of every 64-column K block:
-//                per K block a lane turns
-//                ONE 32-bit word of packed signs into 32 fp16 values +-kscale[c] -- one shift + one
-//                LOP3 per fp16 pair, the fp16 sign bit XORed in from the packed bit -- and writes
-//                them straight into TMEM with tcgen05.st (32x32b.x16).  The +-1 expansion never
-//                touches shared memory; the activation ring is the only smem traffic of the MMAs.
-//   epilogue     tcgen05.ld of the accumulator (lane = sign row, column = token), scale by
-//                rscale[row], fp16 store.
-// Ring stage s couples a smem activation tile and a TMEM A slot; both are released by the
-// tcgen05.commit of the MMAs that read them.
+// Per CTA (sign_gemm_kernel, one output tile per CTA): 128 sign rows (MMA M, TMEM lanes) x 256 tokens
+// (MMA N), accumulated in TMEM (256 fp32 columns).
+//   warps 0,2,3  TMA producers: 256 x 64 fp16 activation boxes (128-byte swizzle) into a 6-stage smem
+//                ring, one issuing lane per stage.
+//   warp 1       TMEM allocator + MMA issuer (one thread): tcgen05.mma.kind::f16, M=128 N=256 K=16,
+//                A operand (the expanded signs) from TMEM, B operand (activations) from smem.
+//   warps 4..11  sign expanders, then epilogue.  Warp w owns TMEM sub-partition w%4 (32 sign rows, one
+//                per lane) and word (w-4)/4 of every 64-column K block: per K block a lane turns ONE
+//                32-bit word of packed signs into 32 fp16 values +-kscale[c] -- one shift + one LOP3 per
+//                fp16 pair, the fp16 sign bit XORed in from the packed bit -- and writes them straight
+//                into TMEM with tcgen05.st (32x32b.x16).  The +-1 expansion never touches shared memory
+//                or HBM; the activation ring is the only smem traffic of the MMAs.
+//   epilogue     16x256b tcgen05.ld of the accumulator, row scale, fp16, stmatrix.trans into the idle
+//                ring (128-byte swizzle), two TMA stores.
+// Ring stage s couples a smem activation box and a TMEM A slot; both are released by the
+// tcgen05.commit of the MMAs that read them.  T <= 256 uses N = the tokens present and splits K.
+// sign_layer_kernel (namespace layer, below) runs both GEMMs of a layer as one persistent launch.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>

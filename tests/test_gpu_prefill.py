@@ -200,3 +200,16 @@ def test_prefill_auto_path_rule():
     dl = P.random_device_layer(64, 64, 64, keep_words=True)
     with pytest.raises(ValueError):
         P.forward_prefill(X, dl, path="fastest")
+
+
+def test_one_launch_needs_tma_compatible_output():
+    """The one-launch kernel stores Y with TMA (16-byte row pitch).  Asked for explicitly with a
+    ragged Y it reports DBF_ERR_UNSUPPORTED; the auto path falls back to two launches, same bits."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    n, k, m, T = 100, 2048, 512, 600      # ldy = 100 halves = 200 bytes per row
+    dl = P.random_device_layer(n, k, m, generator=g, keep_words=True)
+    X = torch.randn((T, m), generator=g, device="cuda").half()
+    with pytest.raises(_lib.DbfNativeError):
+        P.forward_prefill(X, dl, path="one_launch")
+    assert torch.equal(P.forward_prefill(X, dl), _two_launch(X, dl))

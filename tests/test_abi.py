@@ -155,3 +155,18 @@ def test_batched_entry_points_validate_without_a_gpu():
     fr = [dummy, dummy, dummy, dummy, 0, 64, 32, 64, dummy, 4, dummy, 0, 64, None, 5, None, 0, None, None]
     assert L.dbf_forward_batched_frag(*fr) == _lib.ERR_INVALID_ARGUMENT                 # consumers=NULL, n=5
     assert L.dbf_forward_batched_frag(*(fr[:13] + [dummy, 5] + fr[15:])) == _lib.ERR_UNSUPPORTED  # > 4 consumers
+
+
+def test_prefill_path_rule_and_workspace_without_a_gpu():
+    """Host-side prefill queries: the auto path rule (no GPU: 148 SMs assumed) and the workspace,
+    which covers t plus the split-K partials (T <= 256) or the one-launch tile counters (T > 256)."""
+    L = _lib.lib
+    assert L.dbf_prefill_layer_path(4096, 2048, 4096, 2048) == 1     # q: 16 x 8 = 128 GEMM1 tiles
+    assert L.dbf_prefill_layer_path(11008, 2976, 4096, 2048) == 2    # gate: 24 x 8 = 192 > 148
+    assert L.dbf_prefill_layer_path(11008, 2976, 4096, 256) == 1     # one token tile: split-K path
+    assert L.dbf_prefill_layer_path(0, 2976, 4096, 2048) == 1
+    t_bytes = L.dbf_prefill_workspace_bytes(2976, 2048)
+    assert t_bytes == 2048 * L.dbf_prefill_ld(2976) * 2 and L.dbf_prefill_ld(2976) % 64 == 0
+    assert L.dbf_prefill_workspace_bytes_nkm(11008, 2976, 4096, 2048) > t_bytes
+    bad = L.dbf_forward_prefill_ex(None, 1, None, 1, None, None, None, 1, 1, 1, None, 1, 1, None, 1, None, 0, 2, None)
+    assert bad == _lib.ERR_INVALID_ARGUMENT

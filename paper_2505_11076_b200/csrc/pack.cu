@@ -1,6 +1,7 @@
 // Sign packing kernels: the B200 replacement of bitcore.pack / bitcore.unpack
 // (/root/reference/pkg/src/dbf/bitcore.py:72-91) plus the conversions between the reference's
 // uint8 row bytes, the canonical uint32 device layout and the tiled decode layout.
+#include <algorithm>
 #include "common.cuh"
 
 namespace dbf {
@@ -20,54 +21,94 @@ template <> struct SignBits<double> {
   static constexpr U kAbs = 0x7FFFFFFFFFFFFFFFull, kOne = 0x3FF0000000000000ull, kSign = 0x8000000000000000ull;
 };
 
-constexpr int kPackSegs = 1;  // segments per warp (4 measured slower: fewer resident warps at 66 registers)
+// Segments per warp per iteration: four 16-byte loads per lane in flight whatever the dtype (fp16 /
+// bf16: 4 segments, fp32: 2, fp64: 1); measured against 2 and 8 for fp16 (0.47 / 0.45 vs 0.52 of
+// HBM) and against register caps for higher occupancy (6 CTAs/SM 0.37, 8 CTAs/SM 0.35).
+template <typename T> constexpr int pack_segs() { return sizeof(T) <= 2 ? 4 : sizeof(T) == 4 ? 2 : 1; }
 
 template <typename T>
-__global__ void pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols, int64_t ld,
-                            uint32_t* __restrict__ words, int64_t pitch,
-                            unsigned long long* __restrict__ first_bad) {
+__global__ void __launch_bounds__(256) pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols, int64_t ld,
+                                                   uint32_t* __restrict__ words, int64_t pitch,
+                                                   unsigned long long* __restrict__ first_bad, int vec_rows) {
   using SB = SignBits<T>;
   using U = typename SB::U;
+  constexpr int SEGS = pack_segs<T>();
   const int lane = threadIdx.x & 31;
-  const int64_t segs = (pitch + 7) / 8;  // 8 words = 256 columns per segment
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  U v[kPackSegs][8];
-  int64_t rr[kPackSegs], ss[kPackSegs];
+  const int64_t spr = (pitch + 7) / 8;  // segments per row: 8 words = 256 columns each
+  const int64_t nseg = rows * spr;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // grid-stride over groups of SEGS consecutive segments (mostly of one row: contiguous bytes)
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * SEGS; base < nseg;
+       base += nwarps * SEGS) {
+    U v[SEGS][8];
+    int64_t rr[SEGS], ss[SEGS];
+    {
+      int64_t r = base / spr, sg = base - r * spr;
 #pragma unroll
-  for (int q = 0; q < kPackSegs; ++q) {
-    const int64_t id = warp * kPackSegs + q;
-    rr[q] = id / segs;
-    ss[q] = id - rr[q] * segs;
-    const int64_t c0 = ss[q] * 256 + 8 * lane;
-    if (rr[q] >= rows) continue;
-    const U* row = reinterpret_cast<const U*>(dense + rr[q] * ld);
-    if (c0 + 8 <= cols && ((reinterpret_cast<uintptr_t>(row + c0) & 15) == 0)) {
+      for (int q = 0; q < SEGS; ++q) {  // every load of the group issued before any test
+        rr[q] = r, ss[q] = sg;
+        if (r < rows) {
+          const int64_t c0 = sg * 256 + 8 * lane;
+          const U* row = reinterpret_cast<const U*>(dense + r * ld);
+          if (vec_rows && c0 + 8 <= cols) {
 #pragma unroll
-      for (int p = 0; p < (int)(8 * sizeof(U) / 16); ++p)
-        *reinterpret_cast<uint4*>(&v[q][p * 16 / sizeof(U)]) = __ldg(reinterpret_cast<const uint4*>(row + c0) + p);
-    } else {
+            for (int p = 0; p < (int)(8 * sizeof(U) / 16); ++p)
+              *reinterpret_cast<uint4*>(&v[q][p * 16 / sizeof(U)]) = __ldcs(reinterpret_cast<const uint4*>(row + c0) + p);
+          } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) v[q][e] = c0 + e < cols ? row[c0 + e] : SB::kOne;  // padding: bit 0 below
+            for (int e = 0; e < 8; ++e) v[q][e] = c0 + e < cols ? row[c0 + e] : SB::kOne;  // padding: bit 0 below
+          }
+        }
+        if (++sg == spr) sg = 0, ++r;
+      }
     }
-  }
 #pragma unroll
-  for (int q = 0; q < kPackSegs; ++q) {
-    if (rr[q] >= rows) break;  // warp-uniform
-    const int64_t c0 = ss[q] * 256 + 8 * lane;
-    uint32_t byte = 0;
-    int bad = -1;
+    for (int q = 0; q < SEGS; ++q) {
+      if (rr[q] >= rows) break;  // warp-uniform
+      const int64_t c0 = ss[q] * 256 + 8 * lane;
+      uint32_t byte = 0;
+      bool ok = true;
+      if (sizeof(U) <= 4 && c0 + 8 <= cols) {
+        // whole group, 32 bits at a time: validity as one masked compare per word, sign bits
+        // gathered with shifts (per element, the loop below costs ~4x the instructions and made
+        // the kernel issue-bound: fp16 and fp32 inputs packed in the same time)
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(v[q]);
+        if constexpr (sizeof(U) == 2) {
+          constexpr uint32_t kAbs2 = 0x7FFF7FFFu, kOne2 = ((uint32_t)SB::kOne << 16) | SB::kOne;
+          uint32_t x = 0;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const bool in = c0 + e < cols;
-      if (in && (v[q][e] & SB::kAbs) != SB::kOne && bad < 0) bad = e;
-      byte |= (uint32_t)(in && !(v[q][e] & SB::kSign)) << e;
+          for (int i = 0; i < 4; ++i) {
+            ok &= (w[i] & kAbs2) == kOne2;
+            x |= ((~w[i] >> 15) & 0x10001u) << (2 * i);  // element 2i -> bit 2i, element 2i+1 -> bit 16 + 2i
+          }
+          byte = (x & 0x55u) | ((x >> 15) & 0xAAu);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            ok &= (w[i] & 0x7FFFFFFFu) == (uint32_t)SB::kOne;
+            byte |= (~w[i] >> 31) << i;
+          }
+        }
+      } else {
+        ok = false;  // ragged tail / fp64: per element below
+      }
+      if (!ok) {
+        byte = 0;
+        int bad = -1;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const bool in = c0 + e < cols;
+          if (in && (v[q][e] & SB::kAbs) != SB::kOne && bad < 0) bad = e;
+          byte |= (uint32_t)(in && !(v[q][e] & SB::kSign)) << e;
+        }
+        if (bad >= 0) atomicMin(first_bad, (unsigned long long)(rr[q] * cols + c0 + bad));
+      }
+      // word j of the segment = bytes of lanes 4j..4j+3
+      const uint32_t b1 = __shfl_down_sync(0xffffffffu, byte, 1), b2 = __shfl_down_sync(0xffffffffu, byte, 2),
+                     b3 = __shfl_down_sync(0xffffffffu, byte, 3);
+      const int64_t wj = ss[q] * 8 + (lane >> 2);
+      if ((lane & 3) == 0 && wj < pitch) words[rr[q] * pitch + wj] = byte | (b1 << 8) | (b2 << 16) | (b3 << 24);
     }
-    if (bad >= 0) atomicMin(first_bad, (unsigned long long)(rr[q] * cols + c0 + bad));
-    // word j of the segment = bytes of lanes 4j..4j+3
-    const uint32_t b1 = __shfl_down_sync(0xffffffffu, byte, 1), b2 = __shfl_down_sync(0xffffffffu, byte, 2),
-                   b3 = __shfl_down_sync(0xffffffffu, byte, 3);
-    const int64_t wj = ss[q] * 8 + (lane >> 2);
-    if ((lane & 3) == 0 && wj < pitch) words[rr[q] * pitch + wj] = byte | (b1 << 8) | (b2 << 16) | (b3 << 24);
   }
 }
 
@@ -261,11 +302,15 @@ extern "C" int dbf_pack_signs(const void* dense, int dtype, int64_t rows, int64_
   cudaStream_t s = (cudaStream_t)stream;
   auto* fb = reinterpret_cast<unsigned long long*>(d_first_bad);
   init_first_bad_kernel<<<1, 1, 0, s>>>(fb);
-  const int64_t threads = ceil_div(rows * ((word_pitch + 7) / 8), kPackSegs) * 32;
   return dispatch_float(dtype, [&](auto tag) {
     using T = decltype(tag);
-    pack_kernel<T><<<grid_for(threads, 256), 256, 0, s>>>((const T*)dense, rows, cols, ld, words,
-                                                          word_pitch, fb);
+    // rows start 16-byte aligned: every full 8-element group is one (fp16) or more 16-byte loads
+    const int vec_rows = ((uintptr_t)dense & 15) == 0 && (ld * (int64_t)sizeof(T)) % 16 == 0;
+    const int64_t groups = ceil_div(rows * ((word_pitch + 7) / 8), pack_segs<T>());
+    // grid: 8 CTAs of 8 warps per SM (grid-stride), fewer when the matrix is small
+    const int64_t blocks = std::min<int64_t>(ceil_div(groups, 8), (int64_t)kNumSMs * 8);
+    pack_kernel<T><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>((const T*)dense, rows, cols, ld, words,
+                                                                         word_pitch, fb, vec_rows);
     return check_launch();
   });
 }

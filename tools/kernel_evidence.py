@@ -33,6 +33,27 @@ def timed(fn, reps=20, warm=3):
     return e0.elapsed_time(e1) / reps * 1e-3  # seconds per call
 
 
+def timed_graph(fn, per_graph=20, replays=10):
+    """Device time per call with the host out of the loop: `per_graph` calls captured in one CUDA
+    graph, replayed (a short kernel launched from Python through ctypes is otherwise host-bound:
+    round 2's first pack measurement timed ~20 us of launch overhead per call)."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(per_graph):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(replays):
+        g.replay()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / (replays * per_graph) * 1e-3
+
+
 peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
 out = {"peak_gbs": peak, "pack": [], "xor_vs_int8": []}
 g = torch.Generator(device="cuda")
@@ -49,7 +70,7 @@ for (rows, cols) in [(4096, 4096), (11008, 4096), (4096, 11008), (5952, 11008)]:
                                                words.data_ptr(), pitch, bad.data_ptr(), _lib.stream_ptr()),
                        "dbf_pack_signs")
 
-        t = timed(run)
+        t = timed_graph(run)
         nbytes = rows * cols * dense.element_size() + rows * pitch * 4 + 8
         out["pack"].append({"rows": rows, "cols": cols, "dtype": str(dt).split(".")[-1], "us": t * 1e6,
                             "gbs": nbytes / t / 1e9, "frac": nbytes / t / 1e9 / peak})

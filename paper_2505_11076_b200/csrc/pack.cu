@@ -129,15 +129,47 @@ __global__ void pack_sign_of_kernel(const T* __restrict__ dense, int64_t rows, i
 
 __global__ void init_first_bad_kernel(unsigned long long* p) { *p = ~0ull; }
 
-// ---- unpack: one thread per element (coalesced stores).
+// ---- unpack: the inverse of pack's layout -- a warp per 256-column segment (grid-stride), lane l
+// expands byte l & 3 of word l >> 2 into its 8 columns and writes them with 16-byte stores (one
+// for fp16 / bf16) when its row is 16-byte aligned; ragged tails element by element.
+template <typename T> struct PlusMinus;
+template <> struct PlusMinus<__half> { using U = uint16_t; static constexpr U kPlus = 0x3C00, kMinus = 0xBC00; };
+template <> struct PlusMinus<__nv_bfloat16> { using U = uint16_t; static constexpr U kPlus = 0x3F80, kMinus = 0xBF80; };
+template <> struct PlusMinus<float> { using U = uint32_t; static constexpr U kPlus = 0x3F800000u, kMinus = 0xBF800000u; };
+template <> struct PlusMinus<double> {
+  using U = unsigned long long;
+  static constexpr U kPlus = 0x3FF0000000000000ull, kMinus = 0xBFF0000000000000ull;
+};
+
 template <typename T>
-__global__ void unpack_kernel(const uint32_t* __restrict__ words, int64_t rows, int64_t cols,
-                              int64_t pitch, T* __restrict__ dense, int64_t ld) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= rows * cols) return;
-  const int64_t r = i / cols, c = i % cols;
-  const uint32_t w = __ldg(words + r * pitch + (c >> 5));
-  dense[r * ld + c] = from_f64<T>(((w >> (c & 31)) & 1u) ? 1.0 : -1.0);
+__global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict__ words, int64_t rows, int64_t cols,
+                                                     int64_t pitch, T* __restrict__ dense, int64_t ld, int vec_rows) {
+  using PM = PlusMinus<T>;
+  using U = typename PM::U;
+  const int lane = threadIdx.x & 31;
+  const int64_t spr = (pitch + 7) / 8;
+  const int64_t nseg = rows * spr;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sgid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sgid < nseg; sgid += nwarps) {
+    const int64_t r = sgid / spr, sg = sgid - r * spr;
+    const int64_t c0 = sg * 256 + 8 * lane;
+    if (c0 >= cols) continue;
+    const int64_t wj = sg * 8 + (lane >> 2);
+    const uint32_t byte = (__ldg(words + r * pitch + wj) >> (8 * (lane & 3))) & 0xFFu;
+    U v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = ((byte >> e) & 1u) ? PM::kPlus : PM::kMinus;
+    U* row = reinterpret_cast<U*>(dense + r * ld);
+    if (vec_rows && c0 + 8 <= cols) {
+#pragma unroll
+      for (int p = 0; p < (int)(8 * sizeof(U) / 16); ++p)
+        __stcs(reinterpret_cast<uint4*>(row + c0) + p, *reinterpret_cast<const uint4*>(&v[p * 16 / sizeof(U)]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (c0 + e < cols) row[c0 + e] = v[e];
+    }
+  }
 }
 
 // ---- reference bytes (rows x ceil(cols/8)) -> canonical words; padding bits cleared.
@@ -323,8 +355,11 @@ extern "C" int dbf_unpack_signs(const uint32_t* words, int64_t rows, int64_t col
   cudaStream_t s = (cudaStream_t)stream;
   return dispatch_float(dtype, [&](auto tag) {
     using T = decltype(tag);
-    unpack_kernel<T><<<grid_for(rows * cols, 256), 256, 0, s>>>(words, rows, cols, word_pitch,
-                                                                (T*)dense, ld);
+    const int vec_rows = ((uintptr_t)dense & 15) == 0 && (ld * (int64_t)sizeof(T)) % 16 == 0;
+    const int64_t segs = rows * ((word_pitch + 7) / 8);
+    const int64_t blocks = std::min<int64_t>(ceil_div(segs, 8), (int64_t)kNumSMs * 8);
+    unpack_kernel<T><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(words, rows, cols, word_pitch, (T*)dense,
+                                                                          ld, vec_rows);
     return check_launch();
   });
 }

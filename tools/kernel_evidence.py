@@ -74,6 +74,17 @@ for (rows, cols) in [(4096, 4096), (11008, 4096), (4096, 11008), (5952, 11008)]:
         nbytes = rows * cols * dense.element_size() + rows * pitch * 4 + 8
         out["pack"].append({"rows": rows, "cols": cols, "dtype": str(dt).split(".")[-1], "us": t * 1e6,
                             "gbs": nbytes / t / 1e9, "frac": nbytes / t / 1e9 / peak})
+        back = torch.empty_like(dense)
+
+        def run_unpack():
+            _lib.check(_lib.lib.dbf_unpack_signs(words.data_ptr(), rows, cols, pitch, back.data_ptr(),
+                                                 _lib.dtype_code(dt), cols, _lib.stream_ptr()), "dbf_unpack_signs")
+
+        t = timed_graph(run_unpack)
+        assert torch.equal(back, dense), "unpack(pack(x)) != x"
+        out.setdefault("unpack", []).append({"rows": rows, "cols": cols, "dtype": str(dt).split(".")[-1],
+                                             "us": t * 1e6, "gbs": nbytes / t / 1e9, "frac": nbytes / t / 1e9 / peak})
+        del back
         del dense, words
 
 for name, rows, cols in [("q.B / q.A 4096x4096", 4096, 4096), ("gate.A 11008x5952", 11008, 5952),

@@ -26,29 +26,31 @@ template <> struct SignBits<double> {
 // HBM) and against register caps for higher occupancy (6 CTAs/SM 0.37, 8 CTAs/SM 0.35).
 template <typename T> constexpr int pack_segs() { return sizeof(T) <= 2 ? 4 : sizeof(T) == 4 ? 2 : 1; }
 
-template <typename T>
-__global__ void __launch_bounds__(256) pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols, int64_t ld,
-                                                   uint32_t* __restrict__ words, int64_t pitch,
+// I: index type -- int when every element and word offset fits (fewer instructions per segment:
+// the loop is issue-bound at fp16), int64_t otherwise
+template <typename T, typename I>
+__global__ void __launch_bounds__(256) pack_kernel(const T* __restrict__ dense, I rows, I cols, I ld,
+                                                   uint32_t* __restrict__ words, I pitch,
                                                    unsigned long long* __restrict__ first_bad, int vec_rows) {
   using SB = SignBits<T>;
   using U = typename SB::U;
   constexpr int SEGS = pack_segs<T>();
   const int lane = threadIdx.x & 31;
-  const int64_t spr = (pitch + 7) / 8;  // segments per row: 8 words = 256 columns each
-  const int64_t nseg = rows * spr;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const I spr = (pitch + 7) / 8;  // segments per row: 8 words = 256 columns each
+  const I nseg = rows * spr;
+  const I nwarps = (I)(((int64_t)gridDim.x * blockDim.x) >> 5);
   // grid-stride over groups of SEGS consecutive segments (mostly of one row: contiguous bytes)
-  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * SEGS; base < nseg;
+  for (I base = (I)((((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * SEGS); base < nseg;
        base += nwarps * SEGS) {
     U v[SEGS][8];
-    int64_t rr[SEGS], ss[SEGS];
+    I rr[SEGS], ss[SEGS];
     {
-      int64_t r = base / spr, sg = base - r * spr;
+      I r = base / spr, sg = base - r * spr;
 #pragma unroll
       for (int q = 0; q < SEGS; ++q) {  // every load of the group issued before any test
         rr[q] = r, ss[q] = sg;
         if (r < rows) {
-          const int64_t c0 = sg * 256 + 8 * lane;
+          const I c0 = sg * 256 + 8 * lane;
           const U* row = reinterpret_cast<const U*>(dense + r * ld);
           if (vec_rows && c0 + 8 <= cols) {
 #pragma unroll
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const T* __restrict__ dense, 
 #pragma unroll
     for (int q = 0; q < SEGS; ++q) {
       if (rr[q] >= rows) break;  // warp-uniform
-      const int64_t c0 = ss[q] * 256 + 8 * lane;
+      const I c0 = ss[q] * 256 + 8 * lane;
       uint32_t byte = 0;
       bool ok = true;
       if (sizeof(U) <= 4 && c0 + 8 <= cols) {
@@ -75,13 +77,13 @@ __global__ void __launch_bounds__(256) pack_kernel(const T* __restrict__ dense, 
         const uint32_t* w = reinterpret_cast<const uint32_t*>(v[q]);
         if constexpr (sizeof(U) == 2) {
           constexpr uint32_t kAbs2 = 0x7FFF7FFFu, kOne2 = ((uint32_t)SB::kOne << 16) | SB::kOne;
-          uint32_t x = 0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            ok &= (w[i] & kAbs2) == kOne2;
-            x |= ((~w[i] >> 15) & 0x10001u) << (2 * i);  // element 2i -> bit 2i, element 2i+1 -> bit 16 + 2i
-          }
-          byte = (x & 0x55u) | ((x >> 15) & 0xAAu);
+          ok = (((w[0] & kAbs2) ^ kOne2) | ((w[1] & kAbs2) ^ kOne2) | ((w[2] & kAbs2) ^ kOne2) |
+                ((w[3] & kAbs2) ^ kOne2)) == 0u;
+          // the sign bits are bit 7 of bytes 1 and 3 of every word: gather those bytes (elements 0-3,
+          // 4-7), keep the negated sign bits, and one multiply moves bits 7/15/23/31 to 28-31
+          const uint32_t lo = ~__byte_perm(w[0], w[1], 0x7531) & 0x80808080u;
+          const uint32_t hi = ~__byte_perm(w[2], w[3], 0x7531) & 0x80808080u;
+          byte = ((lo * 0x00204081u) >> 28) | (((hi * 0x00204081u) >> 28) << 4);
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -101,12 +103,12 @@ __global__ void __launch_bounds__(256) pack_kernel(const T* __restrict__ dense, 
           if (in && (v[q][e] & SB::kAbs) != SB::kOne && bad < 0) bad = e;
           byte |= (uint32_t)(in && !(v[q][e] & SB::kSign)) << e;
         }
-        if (bad >= 0) atomicMin(first_bad, (unsigned long long)(rr[q] * cols + c0 + bad));
+        if (bad >= 0) atomicMin(first_bad, (unsigned long long)((int64_t)rr[q] * cols + c0 + bad));
       }
       // word j of the segment = bytes of lanes 4j..4j+3
       const uint32_t b1 = __shfl_down_sync(0xffffffffu, byte, 1), b2 = __shfl_down_sync(0xffffffffu, byte, 2),
                      b3 = __shfl_down_sync(0xffffffffu, byte, 3);
-      const int64_t wj = ss[q] * 8 + (lane >> 2);
+      const I wj = ss[q] * 8 + (lane >> 2);
       if ((lane & 3) == 0 && wj < pitch) words[rr[q] * pitch + wj] = byte | (b1 << 8) | (b2 << 16) | (b3 << 24);
     }
   }
@@ -129,9 +131,10 @@ __global__ void pack_sign_of_kernel(const T* __restrict__ dense, int64_t rows, i
 
 __global__ void init_first_bad_kernel(unsigned long long* p) { *p = ~0ull; }
 
-// ---- unpack: the inverse of pack's layout -- a warp per 256-column segment (grid-stride), lane l
-// expands byte l & 3 of word l >> 2 into its 8 columns and writes them with 16-byte stores (one
-// for fp16 / bf16) when its row is 16-byte aligned; ragged tails element by element.
+// ---- unpack: the inverse of pack's layout -- a warp per 256-column segment (grid-stride); in each
+// pass a lane expands the bits of its 16 bytes of output (8 fp16 / 4 fp32 / 2 fp64 columns) and
+// writes them with one 16-byte store when its row is 16-byte aligned (a warp store = 512
+// contiguous bytes); ragged tails element by element.
 template <typename T> struct PlusMinus;
 template <> struct PlusMinus<__half> { using U = uint16_t; static constexpr U kPlus = 0x3C00, kMinus = 0xBC00; };
 template <> struct PlusMinus<__nv_bfloat16> { using U = uint16_t; static constexpr U kPlus = 0x3F80, kMinus = 0xBF80; };
@@ -141,33 +144,36 @@ template <> struct PlusMinus<double> {
   static constexpr U kPlus = 0x3FF0000000000000ull, kMinus = 0xBFF0000000000000ull;
 };
 
-template <typename T>
-__global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict__ words, int64_t rows, int64_t cols,
-                                                     int64_t pitch, T* __restrict__ dense, int64_t ld, int vec_rows) {
+template <typename T, typename I>  // I: index type, as pack_kernel
+__global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict__ words, I rows, I cols,
+                                                     I pitch, T* __restrict__ dense, I ld, int vec_rows) {
   using PM = PlusMinus<T>;
   using U = typename PM::U;
   const int lane = threadIdx.x & 31;
-  const int64_t spr = (pitch + 7) / 8;
-  const int64_t nseg = rows * spr;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t sgid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sgid < nseg; sgid += nwarps) {
-    const int64_t r = sgid / spr, sg = sgid - r * spr;
-    const int64_t c0 = sg * 256 + 8 * lane;
-    if (c0 >= cols) continue;
-    const int64_t wj = sg * 8 + (lane >> 2);
-    const uint32_t byte = (__ldg(words + r * pitch + wj) >> (8 * (lane & 3))) & 0xFFu;
-    U v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = ((byte >> e) & 1u) ? PM::kPlus : PM::kMinus;
+  const I spr = (pitch + 7) / 8;
+  const I nseg = rows * spr;
+  const I nwarps = (I)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  for (I sgid = (I)((((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5)); sgid < nseg; sgid += nwarps) {
+    const I r = sgid / spr, sg = sgid - r * spr;
     U* row = reinterpret_cast<U*>(dense + r * ld);
-    if (vec_rows && c0 + 8 <= cols) {
+    // E columns (16 bytes) per lane per pass, so each store instruction writes 512 contiguous bytes
+    constexpr int E = 16 / (int)sizeof(U);
 #pragma unroll
-      for (int p = 0; p < (int)(8 * sizeof(U) / 16); ++p)
-        __stcs(reinterpret_cast<uint4*>(row + c0) + p, *reinterpret_cast<const uint4*>(&v[p * 16 / sizeof(U)]));
-    } else {
+    for (int pass = 0; pass < 256 / (32 * E); ++pass) {
+      const int o = pass * 32 * E + E * lane;  // column offset inside the segment
+      const I c0 = sg * 256 + o;
+      if (c0 >= cols) break;
+      const uint32_t bits = __ldg(words + r * pitch + sg * 8 + (o >> 5)) >> (o & 31);
+      U v[E];
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (c0 + e < cols) row[c0 + e] = v[e];
+      for (int e = 0; e < E; ++e) v[e] = ((bits >> e) & 1u) ? PM::kPlus : PM::kMinus;
+      if (vec_rows && c0 + E <= cols) {
+        __stcs(reinterpret_cast<uint4*>(row + c0), *reinterpret_cast<const uint4*>(v));
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (c0 + e < cols) row[c0 + e] = v[e];
+      }
     }
   }
 }
@@ -341,8 +347,12 @@ extern "C" int dbf_pack_signs(const void* dense, int dtype, int64_t rows, int64_
     const int64_t groups = ceil_div(rows * ((word_pitch + 7) / 8), pack_segs<T>());
     // grid: 8 CTAs of 8 warps per SM (grid-stride), fewer when the matrix is small
     const int64_t blocks = std::min<int64_t>(ceil_div(groups, 8), (int64_t)kNumSMs * 8);
-    pack_kernel<T><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>((const T*)dense, rows, cols, ld, words,
-                                                                         word_pitch, fb, vec_rows);
+    const unsigned g = (unsigned)std::max<int64_t>(blocks, 1);
+    if (rows * ld < INT32_MAX / 2 && rows * word_pitch < INT32_MAX / 2)
+      pack_kernel<T, int><<<g, 256, 0, s>>>((const T*)dense, (int)rows, (int)cols, (int)ld, words, (int)word_pitch, fb,
+                                            vec_rows);
+    else
+      pack_kernel<T, int64_t><<<g, 256, 0, s>>>((const T*)dense, rows, cols, ld, words, word_pitch, fb, vec_rows);
     return check_launch();
   });
 }
@@ -358,8 +368,11 @@ extern "C" int dbf_unpack_signs(const uint32_t* words, int64_t rows, int64_t col
     const int vec_rows = ((uintptr_t)dense & 15) == 0 && (ld * (int64_t)sizeof(T)) % 16 == 0;
     const int64_t segs = rows * ((word_pitch + 7) / 8);
     const int64_t blocks = std::min<int64_t>(ceil_div(segs, 8), (int64_t)kNumSMs * 8);
-    unpack_kernel<T><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(words, rows, cols, word_pitch, (T*)dense,
-                                                                          ld, vec_rows);
+    const unsigned g = (unsigned)std::max<int64_t>(blocks, 1);
+    if (rows * ld < INT32_MAX / 2 && rows * word_pitch < INT32_MAX / 2)
+      unpack_kernel<T, int><<<g, 256, 0, s>>>(words, (int)rows, (int)cols, (int)word_pitch, (T*)dense, (int)ld, vec_rows);
+    else
+      unpack_kernel<T, int64_t><<<g, 256, 0, s>>>(words, rows, cols, word_pitch, (T*)dense, ld, vec_rows);
     return check_launch();
   });
 }

@@ -59,7 +59,6 @@ constexpr int kNumProducers = 3;              // warps 0, 2, 3
 constexpr int kExpWarps = 8 * MH;
 constexpr int kThreads = (kExpWarp0 + kExpWarps) * 32;
 constexpr int kMaxKScale = 1 << 20;           // K columns a kscale may have (beyond the smem copy: global)
-constexpr int kMaxSmemOptin = 227 * 1024;
 
 struct Params {
   const uint32_t* words;   // rows x pitch PAIRED words
@@ -78,7 +77,6 @@ struct Params {
   int act_bytes;
   int kb_per_split;
   float* part;
-  int ks_global;           // kscale read from global memory (L1-cached) when the smem copy does not fit
   int tma_out;             // epilogue: fp16 tile staged in shared memory, one TMA store (out_map)
 };
 
@@ -129,8 +127,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* act = smem;
   Barriers& bar = *reinterpret_cast<Barriers*>(smem + (size_t)STAGES * kActStageBytes);
-  uint32_t* ks_smem =  // 16-byte aligned (uint4 copies)
-      reinterpret_cast<uint32_t*>(smem + (((size_t)STAGES * kActStageBytes + sizeof(Barriers) + 64 + 15) & ~(size_t)15));
 
 #ifdef DBF_PREFILL_TRACE
   const long long cta_c0_ = clock64();
@@ -155,8 +151,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   // expanders: the first 8 K blocks' sign words and the epilogue's row scales are layer constants,
   // requested before the setup barrier so their HBM latency overlaps it
   uint4 q[4];
+  uint32_t ksr[4];      // K scales of the first 8 K blocks (see load_ksr below)
   __half rs_pre[2][2];  // converted where used, so no thread waits for them at the barrier
+  // K scales live in registers: for the 8 K blocks of a group, lane L holds in ksr[jp] the fp16 pair
+  // (L & 15) of its warp's 32 columns of K block kg + 2 jp + (L >> 4); a K block's 16 pairs are one
+  // shuffle each.  (They used to be copied to shared memory before the setup barrier: ~0.8 us on
+  // every GEMM1 CTA's critical path, and shared memory a 7th ring stage can use.)
+  const int half_w = ((warp - kExpWarp0) >> 2) / MH;
+  auto load_ksr = [&](int kg, uint32_t (&r)[4]) {
+    const unsigned short* bsrc = reinterpret_cast<const unsigned short*>(p.kscale);
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      const int c = (kg + 2 * jp + (lane >> 4)) * BK + half_w * 32 + 2 * (lane & 15);
+      r[jp] = !KSCALE ? 0x3C003C00u
+                      : ((c < p.K ? (uint32_t)__ldg(bsrc + c) : 0u) | ((c + 1 < p.K ? (uint32_t)__ldg(bsrc + c + 1) : 0u) << 16));
+    }
+  };
   if (warp >= kExpWarp0) {
+    load_ksr(kb0, ksr);
     const int sub = warp & 3, mh = ((warp - kExpWarp0) >> 2) % MH;
     const int grow = row0 + mh * UM + sub * 32 + lane;
     const bool live = grow < p.rows;
@@ -172,28 +184,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rr = row0 + sub * 32 + lb * 16 + hi * 8 + (lane >> 2);
         rs_pre[lb][hi] = (p.rscale && p.tma_out && rr < p.rows) ? p.rscale[rr] : __float2half(1.f);
       }
-  }
-  if (KSCALE && !p.ks_global) {
-    // kscale as fp16 pairs, zero beyond K (those columns meet TMA zero-fill anyway)
-    // 8 columns (4 pairs) per thread and load: one round trip for K <= 8 * kThreads
-    const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
-    const bool vec = ((uintptr_t)p.kscale & 15) == 0;
-    for (int i = threadIdx.x; i < p.num_kb * (BK / 8); i += kThreads) {
-      const int c = 8 * i;
-      uint4 u;
-      if (vec && c + 8 <= p.K) {
-        u = __ldg(reinterpret_cast<const uint4*>(src + c));
-      } else {
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int cq = c + 2 * q;
-          w[q] = (cq < p.K ? (uint32_t)src[cq] : 0u) | ((cq + 1 < p.K ? (uint32_t)src[cq + 1] : 0u) << 16);
-        }
-        u = make_uint4(w[0], w[1], w[2], w[3]);
-      }
-      reinterpret_cast<uint4*>(ks_smem)[i] = u;
-    }
   }
   tc_fence_before();
   __syncthreads();
@@ -285,44 +275,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // of MMA time to arrive (one quad ahead was too short for N = 64 tiles: HBM latency-bound)
     const int nquads = (p.num_kb + 1) >> 1;
     const bool tr = tracing && threadIdx.x == 32 * kExpWarp0;
-    // the 16 kscale pairs of this lane's word of K block kb (+1.0 pairs without a kscale)
-    auto load_ks = [&](int kb, uint32_t (&ks)[16]) {
-      if constexpr (KSCALE) {
-        const int c0 = kb * BK + half * 32;  // first of this word's 32 columns
-        if (!p.ks_global) {
-          const uint4* src = reinterpret_cast<const uint4*>(ks_smem + kb * (BK / 2) + half * 16);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint4 u = src[i];
-            ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
-          }
-        } else if (c0 + 32 <= p.K) {  // wide K (e.g. 70B down, K = 28672): straight from L1/L2
-          const uint4* src = reinterpret_cast<const uint4*>(p.kscale + c0);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint4 u = __ldg(src + i);
-            ks[4 * i] = u.x, ks[4 * i + 1] = u.y, ks[4 * i + 2] = u.z, ks[4 * i + 3] = u.w;
-          }
-        } else {
-          const unsigned short* src = reinterpret_cast<const unsigned short*>(p.kscale);
-#pragma unroll
-          for (int qq = 0; qq < 16; ++qq) {
-            const int c = c0 + 2 * qq;
-            ks[qq] = (c < p.K ? (uint32_t)src[c] : 0u) | ((c + 1 < p.K ? (uint32_t)src[c + 1] : 0u) << 16);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) ks[i] = 0x3C003C00u;
-      }
-    };
     for (int kg = kb0; kg < kb1; kg += 8) {  // kb0 is even (splits are whole quads)
       uint4 nq[4];
+      uint32_t nksr[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int qi = (kg >> 1) + 4 + i;
         nq[i] = (live && qi < nquads && 2 * qi < kb1) ? __ldg(wrow + qi) : make_uint4(0, 0, 0, 0);
       }
+      load_ksr(kg + 8, nksr);
 #pragma unroll
       // two K blocks per iteration (one slot wait, one tcgen05 store wait and one arrive round per
       // pair): at small token counts the per-K-block bookkeeping bounded the expanders
@@ -331,37 +292,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb = kg + 2 * jp;
         if (kb >= kb1) break;
         const bool two = kb + 1 < kb1;
-        const int s = (kb - kb0) % STAGES;  // even (kb - kb0 and STAGES are even): s + 1 < STAGES
-        const uint32_t ph = ((kb - kb0) / STAGES) & 1;
+        const int s = (kb - kb0) % STAGES, s1 = (kb + 1 - kb0) % STAGES;
+        const uint32_t ph = ((kb - kb0) / STAGES) & 1, ph1 = ((kb + 1 - kb0) / STAGES) & 1;
         uint32_t ks[16], v0[16], v1[16];
-        load_ks(kb, ks);
+#pragma unroll
+        for (int w = 0; w < 16; ++w) ks[w] = __shfl_sync(0xffffffffu, ksr[jp], w);
         expand_word(half ? q[jp].y : q[jp].x, ks, v0);
         if (two) {
-          load_ks(kb + 1, ks);
+#pragma unroll
+          for (int w = 0; w < 16; ++w) ks[w] = __shfl_sync(0xffffffffu, ksr[jp], 16 + w);
           expand_word(half ? q[jp].w : q[jp].z, ks, v1);
         }
         if (tr) p.trace[4 * kb] = clock64();
         if (lane == 0) {  // one poller per warp
           mbar_wait(&bar.empty[s], ph ^ 1);
-          if (two) mbar_wait(&bar.empty[s + 1], ph ^ 1);
+          if (two) mbar_wait(&bar.empty[s1], ph1 ^ 1);
         }
         __syncwarp();
         if (tr) p.trace[4 * kb + 1] = clock64();
         tc_fence_after();
         const uint32_t col = tmem + lane_addr + kACol0 + mh * kAColsPerHalf + half * 16;
         tmem_st16(col + s * kAColsPerStage, v0);
-        if (two) tmem_st16(col + (s + 1) * kAColsPerStage, v1);
+        if (two) tmem_st16(col + s1 * kAColsPerStage, v1);
         tmem_wait_st();
         tc_fence_before();
         if (tr) p.trace[4 * kb + 2] = clock64();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&bar.full_a[s]);
-          if (two) mbar_arrive(&bar.full_a[s + 1]);
+          if (two) mbar_arrive(&bar.full_a[s1]);
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) q[i] = nq[i];
+      for (int i = 0; i < 4; ++i) q[i] = nq[i], ksr[i] = nksr[i];
     }
     // epilogue: this warp stores tokens [half*64, half*64+64) of its 32 rows (accumulator mh)
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel may still read the output
@@ -569,9 +532,6 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   p.act_bytes = n_mma * BK * 2;
   p.kb_per_split = p.num_kb;
   p.part = nullptr;
-  const size_t ks_fit = small ? smem_bytes_for<kSmallBN, kSmallStages>(p.num_kb, true) : smem_bytes(p.num_kb, true);
-  p.ks_global = kscale && ks_fit > (size_t)kMaxSmemOptin ? 1 : 0;
-  if (p.ks_global && ((uintptr_t)kscale & 15) != 0) return DBF_ERR_UNSUPPORTED;
   int splits = 1;
   if (T <= BN) {
     int kps = 0;
@@ -602,7 +562,7 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
 #endif
   const unsigned gx = (unsigned)ceil_div(rows, BM);
   dim3 grid(gx, (unsigned)ceil_div(T, small ? kSmallBN : BN), (unsigned)splits);
-  const bool ks_smem = kscale != nullptr && !p.ks_global;
+  const bool ks_smem = false;  // K scales are register-resident (shuffled), no shared-memory copy
   // the small configuration pads its shared memory so that one CTA per SM owns all of TMEM
   const size_t smem = small ? std::max<size_t>(smem_bytes_for<kSmallBN, kSmallStages>(p.num_kb, ks_smem), 120 * 1024)
                             : smem_bytes(p.num_kb, ks_smem);

@@ -58,7 +58,6 @@ constexpr int kExpWarp0 = 4;
 constexpr int kNumProducers = 3;              // warps 0, 2, 3
 constexpr int kExpWarps = 8 * MH;
 constexpr int kThreads = (kExpWarp0 + kExpWarps) * 32;
-constexpr int kMaxKScale = 1 << 20;           // K columns a kscale may have (beyond the smem copy: global)
 
 struct Params {
   const uint32_t* words;   // rows x pitch PAIRED words
@@ -510,7 +509,6 @@ static int launch_sign_gemm(const void* act, int64_t T, int64_t K, int64_t ld_ac
   if (((uintptr_t)words & 15) != 0 || pitch % 4 != 0) return DBF_ERR_UNSUPPORTED;
   if (pitch * 32 < ceil_div(K, BK) * BK) return DBF_ERR_SHAPE;  // a K block would read past the row
   if (T > INT32_MAX || rows > INT32_MAX || K > INT32_MAX) return DBF_ERR_UNSUPPORTED;
-  if (kscale && K > kMaxKScale) return DBF_ERR_UNSUPPORTED;
   // T <= BN: one token tile whose MMA N / activation box cover only the tokens present
   const bool small = T <= kSmallBN;
   const int n_mma = T >= BN ? BN : (int)ceil_div(T, 16) * 16;

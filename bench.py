@@ -469,6 +469,40 @@ def prefill_bench(model: str, bpw: float, tokens: int, steps: int, warmup: int):
                           "note": "7 layers back to back for ~2 s (power-capped); per-layer rows above are short bursts"}}
 
 
+def drop_in_call_us(n: int, k: int, m: int, calls: int = 20, replays: int = 10) -> dict:
+    """configs[0] through the per-call drop-in API, one fp16 token: forward_device (two GEMV
+    launches) and forward_engine (a one-layer engine program, one launch), `calls` calls captured in
+    one CUDA graph so the host is out of the loop; device us per call."""
+    import torch
+
+    import paper_2505_11076_b200 as P
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    layer = P.random_device_layer(n, k, m, generator=g)
+    x = torch.randn((1, m), generator=g, device="cuda").half()
+    y = torch.empty((1, n), dtype=torch.half, device="cuda")
+    out = {}
+    for api in ("forward_device", "forward_engine"):
+        fn = getattr(P, api)
+        fn(x, layer, out=y)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            for _ in range(calls):
+                fn(x, layer, out=y)
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(replays):
+            gr.replay()
+        e1.record()
+        e1.synchronize()
+        out[f"us_per_call_{api}"] = e0.elapsed_time(e1) * 1e3 / (calls * replays)
+    return out
+
+
 def sweep_bench(steps: int):
     """BASELINE configs[3] / [4] at one GPU: the decode engine over Llama-2-70B shapes at 2 bpw
     (batch 1, 4, 16) and Llama-2-13B shapes across bits/weight (batch 1, 4, 8), plus 13B at batch 8
@@ -875,6 +909,7 @@ def main():
         # per-layer GEMV kernels, cuBLAS fp16 GEMV of the dense layer
         cfg1 = layer_bench(args.model, 1.0, max(args.steps // 2, 5), 3,
                            shapes=[("cfg1 4096x4096 k=2048", 4096, 4096)], layer_kernels=True)["rows"][0]
+        cfg1.update(drop_in_call_us(4096, 2048, 4096))
 
     sweep = None
     if rank == 0 and not args.no_sweep:

@@ -31,6 +31,7 @@ from .kernel import (
     forward,
     forward_device,
     forward_batched,
+    forward_engine,
     forward_prefill,
     random_device_layer,
     sign_matvec,
@@ -58,6 +59,7 @@ __all__ = [
     "forward",
     "forward_device",
     "forward_batched",
+    "forward_engine",
     "forward_prefill",
     "load_dbf",
     "middle_dim",

@@ -142,6 +142,39 @@ def forward_prefill(X, layer: DeviceLayer, out=None, path: str = "auto"):
 BATCHED_MAX_TOKENS = 32
 
 
+def forward_engine(X, layer: DeviceLayer, out=None, out_dtype=None):
+    """Y = forward(X, layer) for 1-4 fp16 / fp32 token rows through the persistent decode engine as
+    a one-layer program: ONE launch runs GEMV1, the LL handoff of t and GEMV2 (forward_device takes
+    two GEMV launches).  Engine numerics: a 13-bit grid per 256-column input chunk,
+    t rounded to fp16 -- within the fp16 tolerance of the oracle, not bitwise forward_device.  The
+    program is built once per (batch, input dtype, output dtype) and cached on the layer; each call
+    then reads X and writes Y through the launch-time I/O overrides (dbf_engine_program
+    x_override / y_override) and costs one kernel launch."""
+    import torch
+
+    from .engine import EngineProgram
+    from .plan import DecodePlan, PlanOp
+
+    squeeze = X.ndim == 1
+    X2 = (X.unsqueeze(0) if squeeze else X).contiguous()
+    if X2.ndim != 2 or X2.shape[1] != layer.m_dim:
+        raise ValueError(f"X must be (batch, {layer.m_dim}), got {tuple(X.shape)}")
+    batch = X2.shape[0]
+    if not 1 <= batch <= 4 or X2.dtype not in (torch.float16, torch.float32):
+        raise ValueError("forward_engine runs 1..4 fp16 / fp32 token rows (forward_device / forward_batched for others)")
+    odt = out.dtype if out is not None else (out_dtype or X2.dtype)
+    key = (batch, X2.dtype, odt, X2.device)
+    progs = layer.__dict__.setdefault("_engine_progs", {})
+    if key not in progs:
+        bufs = [torch.zeros((batch, layer.m_dim), dtype=X2.dtype, device=X2.device),
+                torch.zeros((batch, layer.n), dtype=odt, device=X2.device)]
+        plan = DecodePlan([layer], [PlanOp(0, 0, 1, "forward")], bufs, input_buffer=0, output_buffer=1)
+        progs[key] = EngineProgram(plan)
+    Y = out if out is not None else torch.empty((batch, layer.n), dtype=odt, device=X2.device)
+    progs[key].launch_io(X2, Y)
+    return Y[0] if squeeze else Y
+
+
 def forward_batched(X, layer: DeviceLayer, out=None, status=None):
     """Y = forward(X, layer) (/root/reference/pkg/src/dbf/kernel.py:48-62) for a CUDA batch of
     1-32 token rows with ONE pass over each sign matrix for all tokens (dbf_forward_batched,

@@ -184,3 +184,34 @@ def test_use_fastest_keeps_the_faster_path_and_its_numbers():
     # keeps it, whatever the timings
     plan.use_fastest(steps=2, margin=1.0)
     assert plan.choice == plan.default_path() == "batched"
+
+
+@pytest.mark.parametrize("batch,xdt,ydt", [(1, "float16", "float16"), (2, "float16", "float32"),
+                                           (4, "float32", "float16"), (3, "float16", "float16")])
+def test_forward_engine_vs_oracle(batch, xdt, ydt):
+    """forward_engine: the drop-in per-call forward as ONE engine launch (BASELINE configs[0]:
+    4096 x 4096, k = 2048), 1-4 token rows, fp16/fp32 in and out; against the float64 oracle on the
+    same bytes; repeated calls (the cached program, new buffers through the I/O overrides) are
+    bitwise equal; bad shapes / batches are rejected."""
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(40 + batch)
+    n, k, m = 4096, 2048, 4096
+    layer = P.random_device_layer(n, k, m, generator=g, keep_words=True)  # words kept for the oracle's bytes
+    X = torch.randn((batch, m), generator=g, device="cuda").to(getattr(torch, xdt))
+    Y = P.forward_engine(X, layer, out_dtype=getattr(torch, ydt))
+    assert Y.dtype == getattr(torch, ydt) and Y.shape == (batch, n)
+    ref = oracle.c_forward(X.double().cpu().numpy(), layer.a.double().cpu().numpy(), layer.A.to_host().bits,
+                           layer.mid.double().cpu().numpy(), layer.B.to_host().bits, layer.b.double().cpu().numpy())
+    y = Y.float().cpu().numpy()
+    assert rel_max(y, ref) <= TOL and rel_norm(y, ref) <= TOL, (rel_max(y, ref), rel_norm(y, ref))
+    Y2 = torch.empty_like(Y)
+    P.forward_engine(X.clone(), layer, out=Y2)
+    assert torch.equal(Y, Y2)
+    if batch == 1:
+        assert torch.equal(P.forward_engine(X[0], layer, out_dtype=getattr(torch, ydt)), Y[0])
+    with pytest.raises(ValueError):
+        P.forward_engine(torch.zeros((5, m), device="cuda", dtype=torch.float16), layer)
+    with pytest.raises(ValueError):
+        P.forward_engine(torch.zeros((1, m + 1), device="cuda", dtype=torch.float16), layer)

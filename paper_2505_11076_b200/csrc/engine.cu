@@ -942,6 +942,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
             fetched = in.kind == 1 && c + kWarps < nch;
             if (fetched) fetch_issue(in, c + kWarps, lane, nf);
             if (tr && first && warp == 0 && lane == 0) tr[1] = gtimer();
+            if (first) WT(2);  // (trace build) first owned chunk quantized
             first = false;
           }
           uint2 b[8];
@@ -964,6 +965,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
             pu[16 + g + 8] = a1[1];
           }
         }
+        if (p < 3) WT(5 + p);  // (trace build) unit pair p computed
       }
       if (tr && warp == 0 && lane == 0) tr[2] = gtimer();
     } else {

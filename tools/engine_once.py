@@ -14,7 +14,7 @@ indep = len(sys.argv) > 3 and sys.argv[3] == "indep"
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
 import os
-plan = llama_decode_plan("llama2-7b", bpw=2.0, blocks=blocks, generator=g, batch=int(os.environ.get("ENGINE_BATCH", "1")))
+plan = llama_decode_plan(os.environ.get("DBF_MODEL", "llama2-7b"), bpw=2.0, blocks=blocks, generator=g, batch=int(os.environ.get("ENGINE_BATCH", "1")))
 plan.buffers[plan.input_buffer].normal_(generator=g)
 if indep:  # every op reads a fixed external input of its width, writes its own scratch buffer
     ins = {}

@@ -743,6 +743,46 @@ __device__ __forceinline__ void pair_mma(const uint8_t* ring, int ring_slots, in
         }
 }
 
+// pair_mma with the two units' chunk addresses already resolved (the caller walks them through the
+// ring incrementally: the unit-pair-outer mode's per-chunk address arithmetic, ~16 instructions per
+// 16 IMMAs, was the bulk of its loop overhead at 70B widths; 70B 16 blocks 1597 -> 1579 us)
+__device__ __forceinline__ void pair_mma_p(const uint4* p0, const uint4* p1, bool has1, const uint2 (&b)[8],
+                                           int Tt, float (&v)[2][2]) {
+        uint4 w[2];
+        w[0] = *p0;
+        w[1] = *p1;
+        int ac[2][DBF_CHAINS][4] = {};
+        if (has1) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const uint32_t m = 0x01010101u << (r & 3);
+          const int sh = 4 * (r >> 2);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            imma(ac[h][r % DBF_CHAINS], (w[h].x >> sh) & m, (w[h].y >> sh) & m, (w[h].z >> sh) & m, (w[h].w >> sh) & m,
+                 b[r].x, b[r].y);
+        }
+        } else {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const uint32_t m = 0x01010101u << (r & 3);
+            const int sh = 4 * (r >> 2);
+            imma(ac[r & 1][0], (w[0].x >> sh) & m, (w[0].y >> sh) & m, (w[0].z >> sh) & m, (w[0].w >> sh) & m,
+                 b[r].x, b[r].y);
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ac[0][0][e] += ac[1][0][e];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int s0 = ac[h][0][0], s1 = ac[h][0][1], s2 = ac[h][0][2], s3 = ac[h][0][3];
+#pragma unroll
+          for (int q = 1; q < DBF_CHAINS; ++q) s0 += ac[h][q][0], s1 += ac[h][q][1], s2 += ac[h][q][2], s3 += ac[h][q][3];
+          v[h][0] = (float)(((s0 + 256 * s1) >> 2) - Tt);
+          v[h][1] = (float)(((s2 + 256 * s3) >> 2) - Tt);
+        }
+}
+
 // AR: the program's last stage carries the fused all-reduce (dbf_engine_program.ar_*); a separate
 // instantiation, so the plain engine carries none of its code (measured +1.3-7 % when shared)
 template <int NB, int XS, bool AR>
@@ -926,8 +966,18 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
         if (u0 >= nunits) break;
         const bool has1 = u0 + 1 < nunits;
         float a0[2] = {0.f, 0.f}, a1[2] = {0.f, 0.f};  // units u0, u0 + 1: rows g, g + 8
-        for (int c = warp; c < nch; c += kWarps) {
-          const int qs = (c / kWarps) % xsc;
+        // ring byte positions of this lane's 16 bytes of (unit, chunk c) for both units, advanced by
+        // kWarps chunks per iteration and wrapped at the ring's end
+        const int ring_bytes = ring_slots * kSlotBytes;
+        int pos0 = slot0 * kSlotBytes + (u0 * nch + warp) * kChunkBytes + lane * 16;
+        int pos1 = pos0 + (has1 ? nch * kChunkBytes : 0);
+        if (pos0 >= ring_bytes) pos0 -= ring_bytes;
+        if (pos1 >= ring_bytes) pos1 -= ring_bytes;
+        // the store holds every owned chunk (the host admits batch-1 programs up to 16 x xsc chunks
+        // wide, dbf_engine_smem_bytes), so slot = the warp's chunk index; later unit pairs read the
+        // stored digits (a wrapped slot index or a width guard in this loop cost 2.6 % on 70B)
+        int qs = 0;
+        for (int c = warp; c < nch; c += kWarps, ++qs) {
           uint8_t* xq = xs + qs * kChunkQ;
           int Ft, Tt;
           if (p > 0 || reuse) {
@@ -950,7 +1000,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineCore prog, in
           for (int r = 0; r < 8; ++r) b[r] = *(const uint2*)(xq + r * 64 + xlane);
           const float inv = __int_as_float((127 - Ft) << 23) * kQInv;
           float v[2][2];
-          pair_mma(sm.ring, ring_slots, slot0, nch, c, u0, has1, b, Tt, lane, v);
+          pair_mma_p((const uint4*)(sm.ring + pos0), (const uint4*)(sm.ring + pos1), has1, b, Tt, v);
+          pos0 += kWarps * kChunkBytes;
+          pos1 += kWarps * kChunkBytes;
+          if (pos0 >= ring_bytes) pos0 -= ring_bytes;
+          if (pos1 >= ring_bytes) pos1 -= ring_bytes;
           a0[0] = __fmaf_rn(v[0][0], inv, a0[0]);
           a1[0] = __fmaf_rn(v[0][1], inv, a1[0]);
           a0[1] = __fmaf_rn(v[1][0], inv, a0[1]);
@@ -1273,6 +1327,9 @@ extern "C" int dbf_engine_smem_bytes(int32_t max_cols, int32_t batch, size_t* by
   // one 16-row unit of the widest segment must fit half the ring
   if (slots < engine::kMinSlots || chunks(max_cols) * kChunkBytes > (int64_t)(slots / 2) * engine::kSlotBytes)
     return DBF_ERR_UNSUPPORTED;
+  // batch 1 keeps every quantized input chunk of a warp in shared memory (up to 16 x 7 chunks =
+  // 28672 columns: the widest Llama-2 input); wider inputs take the batched kernels
+  if (nb == 1 && chunks(max_cols) > (int64_t)engine::kWarps * DBF_XS_CHUNKS1_MAX) return DBF_ERR_UNSUPPORTED;
   *bytes = engine::smem_bytes(slots, nb, max_cols);
   return DBF_OK;
 }

@@ -56,6 +56,10 @@ def test_invalid_arguments_are_rejected_without_a_gpu():
     assert L.dbf_engine_smem_bytes(11008, 1, ctypes.byref(size)) == 0 and 200_000 < size.value <= 227 * 1024
     assert L.dbf_engine_smem_bytes(11008, 4, ctypes.byref(size)) == 0 and size.value <= 227 * 1024
     assert L.dbf_engine_smem_bytes(10**7, 1, ctypes.byref(size)) == _lib.ERR_UNSUPPORTED
+    # batch 1 keeps a warp's quantized input chunks in shared memory: at most 16 x 7 chunks wide
+    assert L.dbf_engine_smem_bytes(28672, 1, ctypes.byref(size)) == 0
+    assert L.dbf_engine_smem_bytes(28673, 1, ctypes.byref(size)) == _lib.ERR_UNSUPPORTED
+    assert L.dbf_engine_smem_bytes(29000, 2, ctypes.byref(size)) == 0
     assert L.dbf_engine_smem_bytes(4096, 5, ctypes.byref(size)) == _lib.ERR_INVALID_ARGUMENT
 
 

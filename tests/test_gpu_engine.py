@@ -130,10 +130,12 @@ def test_engine_batch_8_runs_in_groups_of_4():
 
 
 @pytest.mark.parametrize("batch,n,k,m,act", [(3, 1000, 300, 777, "f32"), (4, 200, 64, 4100, "f16"),
-                                              (1, 17, 32, 29000, "f32"), (2, 5000, 2000, 300, "f16")])
+                                              (1, 17, 32, 28500, "f32"), (2, 5000, 2000, 300, "f16"),
+                                              (2, 17, 32, 29000, "f32"), (1, 2048, 8192, 28672, "f16")])
 def test_engine_ragged_layers_vs_oracle(batch, n, k, m, act):
-    """Ragged shapes (rows not a multiple of 16, columns not of 256, inputs wider than 64 chunks),
-    fp32 or fp16 activations, 1-4 tokens; fp32 plain output is the unrounded sum.  Against the
+    """Ragged shapes (rows not a multiple of 16, columns not of 256, inputs wider than 64 chunks, up to
+    the batch-1 limit of 112 chunks, with several units per run), fp32 or fp16 activations, 1-4
+    tokens; fp32 plain output is the unrounded sum.  Against the
     float64 oracle on the same bytes, and launched again through the per-launch I/O overrides on
     other buffers: bitwise the same."""
     import torch
